@@ -1,0 +1,165 @@
+"""CPU oracle for the greedy ALC local-design path (arXiv 1310.5182).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / ``--impl reference`` legs may import this package. The product
+path (paper_1310_5182_b200) never imports it and shares no code with it.
+
+Thin ctypes marshalling over ``oracle/liblagp_oracle.so`` (plain C in
+``lagp_oracle.c``; every function there cites the passage it follows).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "lagp_oracle.c")
+_LIB = os.path.join(_HERE, "liblagp_oracle.so")
+
+FLAG_NEAR_TIE = 1
+FLAG_SENTINEL = 2
+FLAG_EXHAUSTED = 4
+FLAG_NONFINITE = 8
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (no fast-math, no implicit fp contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = [
+            "gcc", "-O2", "-mfma", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+            "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm",
+        ]
+        subprocess.check_call(cmd)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        D = ctypes.POINTER(ctypes.c_double)
+        I32 = ctypes.POINTER(ctypes.c_int32)
+        U32 = ctypes.POINTER(ctypes.c_uint32)
+        i64, i32, dbl = ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        _lib.oracle_nn.argtypes = [D, i64, i32, D, ctypes.c_int32, I32, D]
+        _lib.oracle_invert_spd.argtypes = [i32, D, D]
+        _lib.oracle_alc_scores.argtypes = [i32, i32, i32, D, D, D, D, dbl, dbl, D, D, D]
+        _lib.oracle_pinv_update.argtypes = [i32, D, D, dbl, D]
+        _lib.oracle_predict.argtypes = [i32, i32, D, D, D, dbl, dbl, D, D, D]
+        _lib.oracle_local_design.argtypes = [D, i64, i32, D, D, dbl, dbl, i32, i32, i32,
+                                             I32, D, D, D, U32, D, D, D]
+        _lib.oracle_alc_batch.argtypes = [D, i64, i32, D, D, i64, dbl, dbl, i32, i32, i32, i32,
+                                          I32, D, D, D, U32, D, D, D]
+        for f in ("oracle_nn", "oracle_invert_spd", "oracle_alc_scores", "oracle_pinv_update",
+                  "oracle_predict", "oracle_local_design", "oracle_alc_batch"):
+            getattr(_lib, f).restype = ctypes.c_int
+    return _lib
+
+
+def _d(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _p(a, t):
+    return a.ctypes.data_as(ctypes.POINTER(t))
+
+
+def nn(X, x, m):
+    """a1: exact m nearest rows by (d², index). Returns (idx int32[m], d2[m])."""
+    X, pX = _d(X)
+    x, px = _d(x)
+    N, p = X.shape
+    idx = np.empty(m, np.int32)
+    d2 = np.empty(m, np.float64)
+    rc = lib().oracle_nn(pX, N, p, px, m, _p(idx, ctypes.c_int32), _p(d2, ctypes.c_double))
+    if rc:
+        raise ValueError(f"oracle_nn rc={rc}")
+    return idx, d2
+
+
+def invert_spd(A):
+    A, pA = _d(A)
+    n = A.shape[0]
+    out = np.empty((n, n))
+    rc = lib().oracle_invert_spd(n, pA, _p(out, ctypes.c_double))
+    if rc:
+        raise np.linalg.LinAlgError(f"oracle_invert_spd rc={rc}")
+    return out
+
+
+def alc_scores(Xj, Kinv, cands, x, d, g):
+    """a3 diagnostic: (delta_closed_form, delta_eq5_literal, m_inv) per candidate."""
+    Xj, pXj = _d(Xj)
+    Kinv, pK = _d(Kinv)
+    cands, pc = _d(cands)
+    x, px = _d(x)
+    j, p = Xj.shape
+    nc = cands.shape[0]
+    dcf = np.empty(nc)
+    dlit = np.empty(nc)
+    minv = np.empty(nc)
+    rc = lib().oracle_alc_scores(j, p, nc, pXj, pK, pc, px, d, g, _p(dcf, ctypes.c_double),
+                                 _p(dlit, ctypes.c_double), _p(minv, ctypes.c_double))
+    if rc:
+        raise RuntimeError(rc)
+    return dcf, dlit, minv
+
+
+def pinv_update(Kinv, k, kdiag):
+    """a4: K_{j+1}^{-1} from K_j^{-1}, k = k_j(x_new), kdiag = K(x_new,x_new)+eta."""
+    Kinv, pK = _d(Kinv)
+    k, pk = _d(k)
+    j = Kinv.shape[0]
+    out = np.empty((j + 1, j + 1))
+    rc = lib().oracle_pinv_update(j, pK, pk, kdiag, _p(out, ctypes.c_double))
+    return out, rc
+
+
+def predict(Xn, Yn, x, d, g):
+    """a5: (mean, s2, var) from a fresh Cholesky of K_n."""
+    Xn, pX = _d(Xn)
+    Yn, pY = _d(Yn)
+    x, px = _d(x)
+    n, p = Xn.shape
+    m, s, v = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    rc = lib().oracle_predict(n, p, pX, pY, px, d, g, ctypes.byref(m), ctypes.byref(s), ctypes.byref(v))
+    if rc:
+        raise np.linalg.LinAlgError(f"oracle_predict rc={rc}")
+    return m.value, s.value, v.value
+
+
+def alc_batch(X, Z, XX, d, g, n0, n, Nprime, threads=0):
+    """Full path for every row of XX (OpenMP over locations)."""
+    X, pX = _d(X)
+    Z, pZ = _d(Z)
+    XX, pXX = _d(np.atleast_2d(XX))
+    N, p = X.shape
+    M = XX.shape[0]
+    G = n - n0
+    idx = np.empty((M, n), np.int32)
+    mean = np.empty(M)
+    s2 = np.empty(M)
+    var = np.empty(M)
+    flags = np.empty(M, np.uint32)
+    gaps = np.empty((M, G))
+    best = np.empty((M, G))
+    s2acc = np.empty(M)
+    used = lib().oracle_alc_batch(
+        pX, N, p, pZ, pXX, M, d, g, n0, n, Nprime, threads,
+        _p(idx, ctypes.c_int32), _p(mean, ctypes.c_double), _p(s2, ctypes.c_double),
+        _p(var, ctypes.c_double), _p(flags, ctypes.c_uint32), _p(gaps, ctypes.c_double),
+        _p(best, ctypes.c_double), _p(s2acc, ctypes.c_double))
+    return dict(idx=idx, mean=mean, s2=s2, var=var, flags=flags, gaps=gaps, best=best,
+                s2_acc=s2acc, threads=used)
+
+
+def local_design(X, Z, x, d, g, n0, n, Nprime):
+    r = alc_batch(X, Z, np.atleast_2d(x), d, g, n0, n, Nprime, threads=1)
+    return {k: (v[0] if isinstance(v, np.ndarray) else v) for k, v in r.items()}
