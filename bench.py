@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark of the greedy ALC local-design hot path (arXiv 1310.5182) on B200.
+
+Workload (BASELINE.json configs[1], the metric's single-GPU configuration):
+C2 — 8-d borehole, N = 100,000 LHS design, M = 10,000 LHS predictive locations
+per GPU, n0 = 6, n = 50, N' = 1000, d = q10 rule, g = 1e-4.
+A "step" is one laGP_alc_batch call over the rank's M locations (NN pool, ALC
+greedy loop, partitioned-inverse updates, prediction — every §8(a) row).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
+
+Weak scaling: every rank processes its own M = 10,000 rows of a global
+predictive set of N·10,000 LHS rows; X and Z are replicated. Rank 0 prints one
+JSON line. The oracle (oracle/, CPU) is executed only in the cpu_baseline leg
+and by --impl reference.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = "C2"
+METRIC = "local-GP predictions/sec"
+UNIT = "predictions/s"
+
+
+def alc_evals_per_location(n0, n, Nprime):
+    """ALC candidate evaluations per location: sum_{j=n0}^{n-1} (N' - j)."""
+    return sum(Nprime - j for j in range(n0, n))
+
+
+def alc_paper_flops_per_location(n0, n, Nprime):
+    """Paper-count ALC work: (N'-j)(2j^2 + 4j) flop per step j."""
+    return sum((Nprime - j) * (2 * j * j + 4 * j) for j in range(n0, n))
+
+
+def fp64_peak_tflops():
+    """ALU roofline denominator: 148 SMs x 64 FP64 FMA/clk x 2 flop
+    x 1.965 GHz (clocks.max.sm) = 37.2 TFLOP/s; the measured DFMA ceiling of
+    scripts/fp64_peak.cu is recorded beside it when profiles/ has it."""
+    nominal = 148 * 64 * 2 * 1.965e9 / 1e12
+    meas = None
+    p = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(p):
+        try:
+            meas = json.load(open(p)).get("dfma_tflops")
+        except Exception:
+            meas = None
+    return nominal, meas
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 9 for k in range(4) if r[5 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_inputs(world):
+    from lagp_data import borehole, lhs, make_config
+
+    cfg = make_config(WORKLOAD)
+    if world > 1:  # weak scaling: a global LHS of world x M rows
+        cfg["XX"] = lhs(cfg["XX"].shape[0] * world, cfg["X"].shape[1], 202)
+    cfg["borehole"] = borehole
+    return cfg
+
+
+def cpu_baseline(cfg, budget_s=15.0, lo=0):
+    """The oracle as it stands, on all host cores, on a bounded sample of the
+    workload's locations (consecutive rows of the rank-0 shard)."""
+    import oracle
+
+    cores = os.cpu_count() or 1
+    args = (cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"])
+    t0 = time.perf_counter()
+    oracle.alc_batch(cfg["X"], cfg["Z"], cfg["XX"][lo:lo + 1], *args, threads=1)
+    t1 = time.perf_counter() - t0
+    S = int(max(cores, min(cfg["XX"].shape[0] - lo, budget_s * cores / max(t1, 1e-4))))
+    S = min(S, cfg["XX"].shape[0] - lo)
+    t0 = time.perf_counter()
+    o = oracle.alc_batch(cfg["X"], cfg["Z"], cfg["XX"][lo:lo + S], *args, threads=cores)
+    el = time.perf_counter() - t0
+    return o, S, el, o["threads"]
+
+
+def run_reference(args):
+    """--impl reference: the oracle (the reference arm of this tier) timed on
+    the host cores on the same config, metric and unit; bounded samples."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg = make_inputs(1)
+    import oracle
+
+    cores = os.cpu_count() or 1
+    a = (cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"])
+    t0 = time.perf_counter()
+    oracle.alc_batch(cfg["X"], cfg["Z"], cfg["XX"][:1], *a, threads=1)
+    t1 = time.perf_counter() - t0
+    per_step_budget = max(2.0, 90.0 / max(1, args.steps + args.warmup))
+    S = int(min(cfg["XX"].shape[0], max(cores, per_step_budget * cores / max(t1, 1e-4))))
+    times = []
+    for it in range(args.warmup + args.steps):
+        lo = (it * S) % max(1, cfg["XX"].shape[0] - S + 1)
+        t0 = time.perf_counter()
+        o = oracle.alc_batch(cfg["X"], cfg["Z"], cfg["XX"][lo:lo + S], *a, threads=cores)
+        el = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(el)
+    ms = 1000.0 * sum(times) / len(times)
+    value = S / (ms / 1000.0)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{WORKLOAD}: 8-d borehole N=100000 LHS, n0=6 n=50 N'=1000, d=q10 g=1e-4",
+                   "sample_locations_per_step": S},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": o["threads"], "kind": "oracle",
+                         "sample": f"{S} consecutive C2 locations per step (of 10000), OpenMP over locations"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--form", default="explicit", choices=["explicit", "incremental"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1310_5182_b200 as lagp
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = make_inputs(world)
+    X = torch.from_numpy(cfg["X"]).to(dev)
+    Z = torch.from_numpy(cfg["Z"]).to(dev)
+    M_rank = 10_000
+    lo = rank * M_rank
+    XXr_np = np.ascontiguousarray(cfg["XX"][lo:lo + M_rank])
+    XX = torch.from_numpy(XXr_np).to(dev)
+    n0, n, Np, d, g = cfg["n0"], cfg["n"], cfg["Nprime"], cfg["d"], cfg["g"]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        lagp.alc_batch(X, Z, XX, d, g, n0, n, Np, form=args.form)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    total_ms = 0.0
+    alc_ms = nn_ms = 0.0
+    launches = 0
+    res = None
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flush between timed steps (untimed)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = lagp.alc_batch(X, Z, XX, d, g, n0, n, Np, form=args.form, timing=True)
+        e1.record(stream)
+        barrier()
+        total_ms += e0.elapsed_time(e1)
+        alc_ms += res["timing"]["alc_ms"]
+        nn_ms += res["timing"]["nn_ms"]
+        launches += res["timing"]["launches"]
+    clk = clocks.stop()
+    t = torch.tensor([total_ms, alc_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, alc_max = float(t[0]), float(t[1])
+    ms_step = total_ms / args.steps
+    M_all = M_rank * world
+    value = M_all / (ms_step / 1000.0)
+    evals = alc_evals_per_location(n0, n, Np)
+
+    # ---- e2e: the host-buffer public entry point, copies inside the timed region
+    pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+    Xh, Zh, XXh = pin(cfg["X"]), pin(cfg["Z"]), pin(XXr_np)
+    hout = dict(idx=torch.empty((M_rank, n), dtype=torch.int32).pin_memory().numpy(),
+                mean=torch.empty(M_rank, dtype=torch.float64).pin_memory().numpy(),
+                s2=torch.empty(M_rank, dtype=torch.float64).pin_memory().numpy(),
+                var=torch.empty(M_rank, dtype=torch.float64).pin_memory().numpy(),
+                flags=torch.empty(M_rank, dtype=torch.int32).pin_memory().numpy().view(np.uint32))
+    e2e_ms = 0.0
+    e2e_steps = max(1, min(args.steps, 3))
+    for _ in range(e2e_steps):
+        flush.fill_(1.0)
+        barrier()
+        t0 = time.perf_counter()
+        lagp.alc_batch_host(Xh, Zh, XXh, d, g, n0, n, Np, form=args.form, out=hout)
+        barrier()
+        e2e_ms += (time.perf_counter() - t0) * 1000.0
+    te = torch.tensor([e2e_ms / e2e_steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = M_all / (float(te[0]) / 1000.0)
+    h2d = (Xh.nbytes + Zh.nbytes + XXh.nbytes) * world
+    d2h = (M_rank * (n * 4 + 3 * 8 + 4)) * world
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (the fused ALC local-design kernel)
+    nominal, meas = fp64_peak_tflops()
+    alc_launch_ms = alc_max / args.steps  # one ALC launch per step at M = 10,000
+    flops_launch = M_rank * alc_paper_flops_per_location(n0, n, Np)
+    achieved = flops_launch / (alc_launch_ms / 1000.0) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(f"alc_{args.form}")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{WORKLOAD}: 8-d borehole, N=100000 LHS design, M=10000 LHS locations per GPU, "
+                               f"n0=6 n=50 N'=1000, d=q10={d:.4f} g=1e-4",
+                   "alc_form": args.form, "l2": "flushed (256 MiB write) before every timed step",
+                   "parallelism": f"dp{world} (XX sharded, X/Z replicated)"},
+        "alc_evals_per_sec": M_all * evals / (ms_step / 1000.0),
+        "phase_ms_per_step": {"nn": nn_ms / args.steps, "alc_loop_and_predict": alc_ms / args.steps},
+        "roofline": {"bound": "alu", "kernel": f"alc_{args.form}_kernel", "achieved": achieved,
+                     "peak": nominal, "unit": "TFLOP/s", "frac": achieved / nominal, "traffic": traffic,
+                     "work": "paper-count (N'-j)(2j^2+4j) flop per location-step (SURVEY §8d), FP64",
+                     "peak_basis": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz",
+                     "peak_measured_dfma": meas},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "status": int(res["status"]),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        o, S, el, used = cpu_baseline(cfg, budget_s=args.cpu_budget, lo=0)
+        line["cpu_baseline"] = {"value": S / el, "unit": UNIT, "cores": used, "kind": "oracle",
+                                "sample": f"first {S} of the 10000 C2 locations, OpenMP over locations"}
+        gi = res["idx"][:S].cpu().numpy()
+        line["sample_parity"] = {"locations": S, "identical_index_sequences": int((gi == o["idx"]).all(1).sum())}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,332 @@
+// abi.cu — the extern "C" boundary declared in include/lagp.h: argument
+// validation, per-call stream-ordered workspace, chunking of the predictive set,
+// phase timing, and the thread-local error string. No torch types anywhere.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "lagp_internal.cuh"
+
+#include "launch.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+lagp_status fail(lagp_status s, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+lagp_status fail(lagp_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+lagp_status cuda_fail(cudaError_t e, const char *where) {
+    return fail(LAGP_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define LAGP_CUDA(call)                                                       \
+    do {                                                                      \
+        cudaError_t _e = (call);                                              \
+        if (_e != cudaSuccess) { st_ret = cuda_fail(_e, #call); goto cleanup; } \
+    } while (0)
+
+int num_sms() {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 1;
+}
+
+bool finite_pos(double v) { return std::isfinite(v) && v > 0.0; }
+
+// Stream-ordered workspace allocations released in one place.
+struct Workspace {
+    cudaStream_t st;
+    void *ptrs[16];
+    int n = 0;
+    explicit Workspace(cudaStream_t s) : st(s) {}
+    cudaError_t alloc(void **p, size_t bytes) {
+        if (bytes == 0) bytes = 16;
+        cudaError_t e = cudaMallocAsync(p, bytes, st);
+        if (e == cudaSuccess) ptrs[n++] = *p;
+        return e;
+    }
+    ~Workspace() {
+        for (int i = 0; i < n; i++) cudaFreeAsync(ptrs[i], st);
+    }
+};
+
+lagp_status check_batch_args(const double *X, int64_t N, int32_t p, const double *Z, const double *XX, int64_t M,
+                             double d, double g, int32_t n0, int32_t n, int32_t Nprime, const int32_t *idx_out,
+                             const double *mean_out, const double *s2_out) {
+    if (N < 1) return fail(LAGP_EINVAL, "N must be >= 1 (got %lld)", (long long)N);
+    if (N > INT32_MAX) return fail(LAGP_EINVAL, "N must fit int32 row indices (got %lld)", (long long)N);
+    if (p < 1 || p > LAGP_PMAX) return fail(LAGP_EINVAL, "p must be in [1, %d] (got %d)", LAGP_PMAX, p);
+    if (M < 0) return fail(LAGP_EINVAL, "M must be >= 0 (got %lld)", (long long)M);
+    if (!finite_pos(d)) return fail(LAGP_EINVAL, "d (theta) must be finite and > 0 (got %g)", d);
+    if (!(std::isfinite(g) && g >= 0.0)) return fail(LAGP_EINVAL, "g (eta) must be finite and >= 0 (got %g)", g);
+    if (n0 < 1) return fail(LAGP_EINVAL, "n0 must be >= 1 (got %d)", n0);
+    if (n < n0) return fail(LAGP_EINVAL, "n must be >= n0 (got n=%d, n0=%d)", n, n0);
+    if (n > LAGP_NMAX) return fail(LAGP_EINVAL, "n must be <= LAGP_NMAX=%d (got %d)", LAGP_NMAX, n);
+    if (Nprime < n) return fail(LAGP_EINVAL, "Nprime must be >= n (got Nprime=%d, n=%d)", Nprime, n);
+    if (Nprime > N) return fail(LAGP_EINVAL, "Nprime must be <= N (got Nprime=%d, N=%lld)", Nprime, (long long)N);
+    if (Nprime > 8192) return fail(LAGP_EINVAL, "Nprime must be <= 8192 in this build (got %d)", Nprime);
+    if (!X || !Z) return fail(LAGP_EINVAL, "X and Z must be non-NULL");
+    if (M > 0 && (!XX || !idx_out || !mean_out || !s2_out))
+        return fail(LAGP_EINVAL, "XX, idx_out, mean_out and s2_out must be non-NULL when M > 0");
+    return LAGP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *lagp_last_error(void) { return g_err.c_str(); }
+int lagp_abi_version(void) { return LAGP_ABI_VERSION; }
+
+lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const double *Z, const double *XX, int64_t M,
+                              double d, double g, int32_t n0, int32_t n, int32_t Nprime, int32_t *idx_out,
+                              double *mean_out, double *s2_out, double *var_out, uint32_t *flags_out,
+                              double *gap_out, int32_t alc_form, lagp_timing *timing, void *cuda_stream) {
+    lagp_status chk = check_batch_args(X, N, p, Z, XX, M, d, g, n0, n, Nprime, idx_out, mean_out, s2_out);
+    if (chk != LAGP_OK) return chk;
+    if (alc_form != LAGP_ALC_EXPLICIT && alc_form != LAGP_ALC_INCREMENTAL)
+        return fail(LAGP_EINVAL, "alc_form must be LAGP_ALC_EXPLICIT or LAGP_ALC_INCREMENTAL (got %d)", alc_form);
+    if (alc_form == LAGP_ALC_INCREMENTAL)
+        return fail(LAGP_EINVAL, "alc_form LAGP_ALC_INCREMENTAL is not built yet");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    lagp_status st_ret = LAGP_OK;
+    if (timing) std::memset(timing, 0, sizeof *timing);
+    if (M == 0) return LAGP_OK;
+
+    const int sms = num_sms();
+    const int ld = (n + 3) & ~3;
+    const int alc_bps = lagp::alc_explicit_blocks_per_sm(ld, n, p);
+    const int alc_grid_max = alc_bps * sms;
+    // chunk of locations per NN+ALC round: bounds the pool buffer (chunk × N' int32)
+    const int64_t chunk = M < 65536 ? M : 65536;
+    const int nn_grid = lagp::nn_grid(chunk, sms);
+    const int alc_grid = (int)(chunk < alc_grid_max ? chunk : alc_grid_max);
+
+    Workspace ws(st);
+    int32_t *pool = nullptr;
+    void *nnws = nullptr;
+    double *cache = nullptr, *coords = nullptr, *kap = nullptr;
+    unsigned char *chosen = nullptr;
+    int *counters = nullptr;  // [0] = partial count, [1] = NN fallbacks
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    float nn_ms = 0.f, alc_ms = 0.f, tot_ms = 0.f;
+    int launches = 0;
+    int host_counters[2] = {0, 0};
+
+    LAGP_CUDA(ws.alloc((void **)&pool, (size_t)chunk * Nprime * sizeof(int32_t)));
+    LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(nn_grid)));
+    LAGP_CUDA(ws.alloc((void **)&cache, (size_t)alc_grid * n * Nprime * sizeof(double)));
+    LAGP_CUDA(ws.alloc((void **)&coords, (size_t)alc_grid * p * Nprime * sizeof(double)));
+    LAGP_CUDA(ws.alloc((void **)&kap, (size_t)alc_grid * Nprime * sizeof(double)));
+    LAGP_CUDA(ws.alloc((void **)&chosen, (size_t)alc_grid * Nprime));
+    LAGP_CUDA(ws.alloc((void **)&counters, 2 * sizeof(int)));
+    LAGP_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int), st));
+    if (timing)
+        for (int i = 0; i < 4; i++) LAGP_CUDA(cudaEventCreate(&ev[i]));
+    if (timing) LAGP_CUDA(cudaEventRecord(ev[0], st));
+
+    for (int64_t m0 = 0; m0 < M; m0 += chunk) {
+        const int64_t mc = (M - m0) < chunk ? (M - m0) : chunk;
+        if (timing) LAGP_CUDA(cudaEventRecord(ev[1], st));
+        LAGP_CUDA(lagp::launch_nn(X, N, p, XX + m0 * p, mc, Nprime, pool, nullptr, nnws,
+                                  lagp::nn_grid(mc, sms), counters + 1, st));
+        launches++;
+        if (timing) LAGP_CUDA(cudaEventRecord(ev[2], st));
+        lagp::AlcArgs a;
+        a.X = X; a.N = N; a.p = p; a.Z = Z; a.XX = XX + m0 * p; a.M = mc;
+        a.eta = g; a.rtheta = 1.0 / d;
+        a.n0 = n0; a.n = n; a.Nprime = Nprime; a.ld = ld;
+        a.pool = pool;
+        a.idx_out = idx_out + m0 * n;
+        a.mean = mean_out + m0; a.s2 = s2_out + m0;
+        a.var = var_out ? var_out + m0 : nullptr;
+        a.flags = flags_out ? flags_out + m0 : nullptr;
+        a.gap_out = gap_out ? gap_out + m0 * (n - n0) : nullptr;
+        a.cache = cache; a.coords = coords; a.kap = kap; a.chosen = chosen;
+        a.n_partial = counters;
+        int grid = (int)(mc < alc_grid ? mc : alc_grid);
+        LAGP_CUDA(lagp::launch_alc_explicit(a, grid, st));
+        launches++;
+        if (timing) {
+            LAGP_CUDA(cudaEventRecord(ev[3], st));
+            LAGP_CUDA(cudaEventSynchronize(ev[3]));
+            float t1 = 0.f, t2 = 0.f;
+            cudaEventElapsedTime(&t1, ev[1], ev[2]);
+            cudaEventElapsedTime(&t2, ev[2], ev[3]);
+            nn_ms += t1;
+            alc_ms += t2;
+        }
+    }
+    LAGP_CUDA(cudaMemcpyAsync(host_counters, counters, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (timing) LAGP_CUDA(cudaEventRecord(ev[3], st));
+    LAGP_CUDA(cudaStreamSynchronize(st));
+    if (timing) {
+        cudaEventElapsedTime(&tot_ms, ev[0], ev[3]);
+        timing->nn_ms = nn_ms;
+        timing->alc_ms = alc_ms;
+        timing->predict_ms = 0.f;
+        timing->total_ms = tot_ms;
+        timing->launches = launches;
+        timing->nn_fallbacks = host_counters[1];
+    }
+    if (host_counters[0] > 0) {
+        fail(LAGP_PARTIAL, "%d location(s) flagged EXHAUSTED or NONFINITE", host_counters[0]);
+        st_ret = LAGP_PARTIAL;
+    }
+cleanup:
+    for (int i = 0; i < 4; i++)
+        if (ev[i]) cudaEventDestroy(ev[i]);
+    return st_ret;
+}
+
+lagp_status laGP_alc_batch(const double *X, int64_t N, int32_t p, const double *Z, const double *XX, int64_t M,
+                           double d, double g, int32_t n0, int32_t n, int32_t Nprime, int32_t *idx_out,
+                           double *mean_out, double *s2_out, double *var_out, uint32_t *flags_out, double *gap_out,
+                           void *cuda_stream) {
+    return laGP_alc_batch_ex(X, N, p, Z, XX, M, d, g, n0, n, Nprime, idx_out, mean_out, s2_out, var_out, flags_out,
+                             gap_out, LAGP_ALC_EXPLICIT, nullptr, cuda_stream);
+}
+
+lagp_status laGP_alc_batch_host(const double *X, int64_t N, int32_t p, const double *Z, const double *XX, int64_t M,
+                                double d, double g, int32_t n0, int32_t n, int32_t Nprime, int32_t *idx_out,
+                                double *mean_out, double *s2_out, double *var_out, uint32_t *flags_out,
+                                double *gap_out, int32_t alc_form, void *cuda_stream) {
+    lagp_status chk = check_batch_args(X, N, p, Z, XX, M, d, g, n0, n, Nprime, idx_out, mean_out, s2_out);
+    if (chk != LAGP_OK) return chk;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    lagp_status st_ret = LAGP_OK;
+    const int G = n - n0;
+    double *dX = nullptr, *dZ = nullptr, *dXX = nullptr, *dmean = nullptr, *ds2 = nullptr, *dvar = nullptr,
+           *dgap = nullptr;
+    int32_t *didx = nullptr;
+    uint32_t *dfl = nullptr;
+    {
+        Workspace ws(st);
+        LAGP_CUDA(ws.alloc((void **)&dX, (size_t)N * p * sizeof(double)));
+        LAGP_CUDA(ws.alloc((void **)&dZ, (size_t)N * sizeof(double)));
+        LAGP_CUDA(ws.alloc((void **)&dXX, (size_t)M * p * sizeof(double)));
+        LAGP_CUDA(ws.alloc((void **)&didx, (size_t)M * n * sizeof(int32_t)));
+        LAGP_CUDA(ws.alloc((void **)&dmean, (size_t)M * sizeof(double)));
+        LAGP_CUDA(ws.alloc((void **)&ds2, (size_t)M * sizeof(double)));
+        if (var_out) LAGP_CUDA(ws.alloc((void **)&dvar, (size_t)M * sizeof(double)));
+        if (flags_out) LAGP_CUDA(ws.alloc((void **)&dfl, (size_t)M * sizeof(uint32_t)));
+        if (gap_out) LAGP_CUDA(ws.alloc((void **)&dgap, (size_t)M * G * sizeof(double)));
+        LAGP_CUDA(cudaMemcpyAsync(dX, X, (size_t)N * p * sizeof(double), cudaMemcpyHostToDevice, st));
+        LAGP_CUDA(cudaMemcpyAsync(dZ, Z, (size_t)N * sizeof(double), cudaMemcpyHostToDevice, st));
+        if (M > 0) LAGP_CUDA(cudaMemcpyAsync(dXX, XX, (size_t)M * p * sizeof(double), cudaMemcpyHostToDevice, st));
+        st_ret = laGP_alc_batch_ex(dX, N, p, dZ, dXX, M, d, g, n0, n, Nprime, didx, dmean, ds2, dvar, dfl, dgap,
+                                   alc_form, nullptr, cuda_stream);
+        if (st_ret != LAGP_OK && st_ret != LAGP_PARTIAL) goto cleanup;
+        if (M > 0) {
+            LAGP_CUDA(cudaMemcpyAsync(idx_out, didx, (size_t)M * n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            LAGP_CUDA(cudaMemcpyAsync(mean_out, dmean, (size_t)M * sizeof(double), cudaMemcpyDeviceToHost, st));
+            LAGP_CUDA(cudaMemcpyAsync(s2_out, ds2, (size_t)M * sizeof(double), cudaMemcpyDeviceToHost, st));
+            if (var_out) LAGP_CUDA(cudaMemcpyAsync(var_out, dvar, (size_t)M * sizeof(double), cudaMemcpyDeviceToHost, st));
+            if (flags_out)
+                LAGP_CUDA(cudaMemcpyAsync(flags_out, dfl, (size_t)M * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+            if (gap_out)
+                LAGP_CUDA(cudaMemcpyAsync(gap_out, dgap, (size_t)M * G * sizeof(double), cudaMemcpyDeviceToHost, st));
+        }
+    cleanup:;
+    }
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess && st_ret == LAGP_OK) st_ret = cuda_fail(e, "cudaStreamSynchronize");
+    return st_ret;
+}
+
+lagp_status laGP_nn_pool(const double *X, int64_t N, int32_t p, const double *XX, int64_t M, int32_t Nprime,
+                         int32_t *pool_out, double *d2_out, void *cuda_stream) {
+    if (N < 1 || N > INT32_MAX) return fail(LAGP_EINVAL, "N must be in [1, 2^31-1] (got %lld)", (long long)N);
+    if (p < 1 || p > LAGP_PMAX) return fail(LAGP_EINVAL, "p must be in [1, %d] (got %d)", LAGP_PMAX, p);
+    if (M < 0) return fail(LAGP_EINVAL, "M must be >= 0");
+    if (Nprime < 1 || Nprime > N || Nprime > 8192)
+        return fail(LAGP_EINVAL, "Nprime must be in [1, min(N, 8192)] (got %d)", Nprime);
+    if (!X || (M > 0 && (!XX || !pool_out))) return fail(LAGP_EINVAL, "X, XX and pool_out must be non-NULL");
+    if (M == 0) return LAGP_OK;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    lagp_status st_ret = LAGP_OK;
+    {
+        Workspace ws(st);
+        void *nnws = nullptr;
+        int *fb = nullptr;
+        const int grid = lagp::nn_grid(M, num_sms());
+        LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(grid)));
+        LAGP_CUDA(ws.alloc((void **)&fb, sizeof(int)));
+        LAGP_CUDA(cudaMemsetAsync(fb, 0, sizeof(int), st));
+        LAGP_CUDA(lagp::launch_nn(X, N, p, XX, M, Nprime, pool_out, d2_out, nnws, grid, fb, st));
+    cleanup:;
+    }
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess && st_ret == LAGP_OK) st_ret = cuda_fail(e, "cudaStreamSynchronize");
+    return st_ret;
+}
+
+lagp_status laGP_alc_scores(int32_t B, int32_t j, int32_t p, int32_t nc, const double *Xj, const double *Kinv,
+                            const double *cands, const int32_t *cand_idx, const double *x, double d, double g,
+                            double *delta_out, int32_t *best_out, double *gap_out, void *cuda_stream) {
+    if (B < 0) return fail(LAGP_EINVAL, "B must be >= 0");
+    if (j < 1 || j > LAGP_NMAX) return fail(LAGP_EINVAL, "j must be in [1, %d] (got %d)", LAGP_NMAX, j);
+    if (p < 1 || p > LAGP_PMAX) return fail(LAGP_EINVAL, "p must be in [1, %d] (got %d)", LAGP_PMAX, p);
+    if (nc < 1) return fail(LAGP_EINVAL, "nc must be >= 1 (got %d)", nc);
+    if (!finite_pos(d)) return fail(LAGP_EINVAL, "d (theta) must be finite and > 0");
+    if (!(std::isfinite(g) && g >= 0.0)) return fail(LAGP_EINVAL, "g (eta) must be finite and >= 0");
+    if (B > 0 && (!Xj || !Kinv || !cands || !cand_idx || !x || !best_out))
+        return fail(LAGP_EINVAL, "Xj, Kinv, cands, cand_idx, x and best_out must be non-NULL");
+    if (B == 0) return LAGP_OK;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    cudaError_t e = lagp::launch_alc_scores(B, j, p, nc, Xj, Kinv, cands, cand_idx, x, 1.0 / d, g, delta_out, best_out,
+                                            gap_out, st);
+    if (e != cudaSuccess) return cuda_fail(e, "alc_scores_kernel");
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    return LAGP_OK;
+}
+
+lagp_status laGP_pinv_update(int32_t B, int32_t j, const double *Kinv, const double *k, double kdiag,
+                             double *Kinv_out, void *cuda_stream) {
+    if (B < 0) return fail(LAGP_EINVAL, "B must be >= 0");
+    if (j < 1 || j >= LAGP_NMAX) return fail(LAGP_EINVAL, "j must be in [1, %d) (got %d)", LAGP_NMAX, j);
+    if (!std::isfinite(kdiag)) return fail(LAGP_EINVAL, "kdiag must be finite");
+    if (B > 0 && (!Kinv || !k || !Kinv_out)) return fail(LAGP_EINVAL, "Kinv, k and Kinv_out must be non-NULL");
+    if (B == 0) return LAGP_OK;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    cudaError_t e = lagp::launch_pinv_update(B, j, Kinv, k, kdiag, Kinv_out, st);
+    if (e != cudaSuccess) return cuda_fail(e, "pinv_update_kernel");
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    return LAGP_OK;
+}
+
+lagp_status laGP_predict(int32_t B, int32_t n, int32_t p, const double *Xn, const double *Yn, const double *x, double d,
+                         double g, double *mean_out, double *s2_out, double *var_out, void *cuda_stream) {
+    if (B < 0) return fail(LAGP_EINVAL, "B must be >= 0");
+    if (n < 1 || n > LAGP_NMAX) return fail(LAGP_EINVAL, "n must be in [1, %d] (got %d)", LAGP_NMAX, n);
+    if (p < 1 || p > LAGP_PMAX) return fail(LAGP_EINVAL, "p must be in [1, %d] (got %d)", LAGP_PMAX, p);
+    if (!finite_pos(d)) return fail(LAGP_EINVAL, "d (theta) must be finite and > 0");
+    if (!(std::isfinite(g) && g >= 0.0)) return fail(LAGP_EINVAL, "g (eta) must be finite and >= 0");
+    if (B > 0 && (!Xn || !Yn || !x || !mean_out || !s2_out))
+        return fail(LAGP_EINVAL, "Xn, Yn, x, mean_out and s2_out must be non-NULL");
+    if (B == 0) return LAGP_OK;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    cudaError_t e = lagp::launch_predict(B, n, p, Xn, Yn, x, 1.0 / d, g, mean_out, s2_out, var_out, st);
+    if (e != cudaSuccess) return cuda_fail(e, "predict_kernel");
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    return LAGP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,179 @@
+// block_ops.cuh — CTA-level building blocks for the local GP state kept in
+// shared memory: reductions, the partitioned-inverse append (row a4) and the
+// fresh-Cholesky prediction (row a5). Used by the fused local-design kernels
+// and by the single-row diagnostic kernels.
+#pragma once
+#include "lagp_internal.cuh"
+
+namespace lagp {
+
+// Sum over the CTA (blockDim.x multiple of 32, <= 1024). `scratch` >= 32 doubles.
+// Deterministic: fixed shuffle tree, then warp partials summed in warp order.
+__device__ __forceinline__ double block_sum(double v, double *scratch) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    double s = 0.0;
+    const int nw = blockDim.x >> 5;
+    for (int w = 0; w < nw; w++) s += scratch[w];
+    __syncthreads();
+    return s;
+}
+
+// Block-wide merge of per-thread Top2 records; every thread receives the result.
+__device__ __forceinline__ Top2 block_top2(Top2 t, double *scratch /* >= 4*32 doubles */) {
+    warp_merge_top2(t);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) {
+        scratch[4 * wid + 0] = t.d1;
+        scratch[4 * wid + 1] = t.d2;
+        scratch[4 * wid + 2] = int_bits_to_double(t.i1);
+        scratch[4 * wid + 3] = int_bits_to_double(t.pos);
+    }
+    __syncthreads();
+    Top2 r;
+    r.init();
+    const int nw = blockDim.x >> 5;
+    for (int w = 0; w < nw; w++)
+        r.merge(scratch[4 * w + 0], double_bits_to_int(scratch[4 * w + 2]),
+                double_bits_to_int(scratch[4 * w + 3]), scratch[4 * w + 1]);
+    __syncthreads();
+    return r;
+}
+
+// Partitioned-inverse append (a4; Eq (6)): given the
+// explicit K_j^{-1} in Kinv (leading dimension ld, symmetric), k = k_j(x_new)
+// and kdiag = K(x_new,x_new) + eta, overwrite Kinv with K_{j+1}^{-1}:
+//   u = K^{-1} k,  s = kdiag - k^T u,
+//   K_{j+1}^{-1} = [[K^{-1} + u u^T / s, -u/s], [-u^T/s, 1/s]].
+// Entry (a,b) and (b,a) use the same IEEE operations, so symmetry is exact.
+// `u` is scratch (>= j+1). Returns s (<= 0 means K_{j+1} is not PD).
+__device__ inline double pinv_append(double *Kinv, int ld, int j, const double *k, double kdiag, double *u,
+                              double *scratch) {
+    const int tid = threadIdx.x;
+    for (int a = tid; a < j; a += blockDim.x) {
+        double acc = 0.0;
+        const double *row = Kinv + a * ld;
+        for (int b = 0; b < j; b++) acc = fma(row[b], k[b], acc);
+        u[a] = acc;
+    }
+    __syncthreads();
+    double part = 0.0;
+    for (int a = tid; a < j; a += blockDim.x) part = fma(k[a], u[a], part);
+    const double s = kdiag - block_sum(part, scratch);
+    const int jj = j * j;
+    for (int e = tid; e < jj; e += blockDim.x) {
+        int a = e / j, b = e - a * j;
+        Kinv[a * ld + b] = __dadd_rn(Kinv[a * ld + b], __ddiv_rn(__dmul_rn(u[a], u[b]), s));
+    }
+    for (int a = tid; a < j; a += blockDim.x) {
+        double v = -__ddiv_rn(u[a], s);
+        Kinv[a * ld + j] = v;
+        Kinv[j * ld + a] = v;
+    }
+    if (tid == 0) Kinv[j * ld + j] = __ddiv_rn(1.0, s);
+    __syncthreads();
+    return s;
+}
+
+// w = Kinv * h for the leading j×j block.
+__device__ __forceinline__ void block_matvec(const double *Kinv, int ld, int j, const double *h, double *w) {
+    for (int a = threadIdx.x; a < j; a += blockDim.x) {
+        double acc = 0.0;
+        const double *row = Kinv + a * ld;
+        for (int b = 0; b < j; b++) acc = fma(row[b], h[b], acc);
+        w[a] = acc;
+    }
+    __syncthreads();
+}
+
+// a5 — Eq (1)-(2) with N -> n on D_n(x) (Fig 1 step 5):
+// fresh Cholesky of K_n = C(X_n) + eta I built in `A` (n×n, ld), then
+//   mean = h^T K^{-1} Y, psi = Y^T K^{-1} Y, s2 = psi (1 + eta - h^T K^{-1} h)/n,
+//   var = s2 n/(n-2) (NaN if n <= 2).
+// Xn [n×p] (row-major, smem or global), Yn [n], h [n]; y1,y2 scratch [n].
+// Returns false if K_n is not numerically PD.
+__device__ inline bool block_predict(double *A, int ld, int n, int p, const double *Xn, const double *Yn,
+                              const double *h, double rtheta, double eta, double *y1, double *y2,
+                              double *scratch, double *mean, double *s2, double *var) {
+    const int tid = threadIdx.x;
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        int a = e / n, b = e - a * n;
+        if (b <= a) {
+            double v = corr_from_d2(sqdist_fma(Xn + a * p, Xn + b * p, p), rtheta);
+            if (a == b) v += eta;
+            A[a * ld + b] = v;
+        }
+    }
+    __syncthreads();
+    // right-looking Cholesky, lower triangle in place
+    __shared__ int bad;
+    if (tid == 0) bad = 0;
+    __syncthreads();
+    for (int k = 0; k < n; k++) {
+        if (tid == 0) {
+            double dkk = A[k * ld + k];
+            if (!(dkk > 0.0)) bad = 1;
+            A[k * ld + k] = sqrt(dkk);
+        }
+        __syncthreads();
+        const double lkk = A[k * ld + k];
+        for (int i = k + 1 + tid; i < n; i += blockDim.x) A[i * ld + k] /= lkk;
+        __syncthreads();
+        const int m = n - k - 1;  // trailing (m×m lower) update
+        const int tri = m * (m + 1) / 2;
+        for (int e = tid; e < tri; e += blockDim.x) {
+            // map e -> (r, c) with c <= r in the trailing block
+            int r = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+            while ((r + 1) * (r + 2) / 2 <= e) r++;
+            while (r * (r + 1) / 2 > e) r--;
+            int c = e - r * (r + 1) / 2;
+            int i = k + 1 + r, jj = k + 1 + c;
+            A[i * ld + jj] = fma(-A[i * ld + k], A[jj * ld + k], A[i * ld + jj]);
+        }
+        __syncthreads();
+    }
+    // forward / back substitution, warp 0 on h, warp 1 on Y
+    const int lane = tid & 31, wid = tid >> 5;
+    if (wid < 2) {
+        const double *b = (wid == 0) ? h : Yn;
+        double *y = (wid == 0) ? y1 : y2;
+        for (int i = 0; i < n; i++) {
+            double acc = 0.0;
+            for (int t = lane; t < i; t += 32) acc = fma(A[i * ld + t], y[t], acc);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (lane == 0) y[i] = (b[i] - acc) / A[i * ld + i];
+            __syncwarp();
+        }
+        for (int i = n - 1; i >= 0; i--) {
+            double acc = 0.0;
+            for (int t = i + 1 + lane; t < n; t += 32) acc = fma(A[t * ld + i], y[t], acc);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (lane == 0) y[i] = (y[i] - acc) / A[i * ld + i];
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    double pm = 0.0, pp = 0.0, ph = 0.0;
+    for (int i = tid; i < n; i += blockDim.x) {
+        pm = fma(h[i], y2[i], pm);
+        pp = fma(Yn[i], y2[i], pp);
+        ph = fma(h[i], y1[i], ph);
+    }
+    double mu = block_sum(pm, scratch);
+    double psi = block_sum(pp, scratch);
+    double hKh = block_sum(ph, scratch);
+    double sc = psi * (1.0 + eta - hKh) / (double)n;
+    *mean = mu;
+    *s2 = sc;
+    *var = (n > 2) ? sc * (double)n / (double)(n - 2) : __longlong_as_double(0x7ff8000000000000LL);
+    return bad == 0;
+}
+
+}  // namespace lagp

@@ -1,0 +1,49 @@
+// launch.h — host-side launchers of the sm_100a kernels (one definition of the
+// argument structs, shared by the kernel TUs and abi.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lagp {
+
+// nn.cu (row a1)
+cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64_t M, int Nprime, int32_t *pool,
+                      double *d2, void *ws, int grid, int *fb, cudaStream_t st);
+size_t nn_ws_bytes(int grid);
+int nn_grid(int64_t M, int num_sms);
+
+// fused local-design kernels (rows a2-a5)
+struct AlcArgs {
+    const double *X;
+    int64_t N;
+    int p;
+    const double *Z;
+    const double *XX;
+    int64_t M;
+    double eta, rtheta;
+    int n0, n, Nprime, ld;
+    const int32_t *pool;  // [M][Nprime], first n0 = NN order
+    int32_t *idx_out;
+    double *mean, *s2, *var;
+    uint32_t *flags;
+    double *gap_out;
+    // per-CTA slabs in global memory
+    double *cache;          // [grid][n][Nprime] rows of K(X_j[a], x_c)
+    double *coords;         // [grid][p][Nprime] pool coordinates (SoA)
+    double *kap;            // [grid][Nprime]    kappa_c = K(x_c, x)
+    unsigned char *chosen;  // [grid][Nprime]
+    int *n_partial;         // count of EXHAUSTED/NONFINITE locations
+};
+cudaError_t launch_alc_explicit(const AlcArgs &a, int grid, cudaStream_t st);
+int alc_explicit_blocks_per_sm(int ld, int n, int p);
+
+// diag.cu (rows a3, a4, a5 alone)
+cudaError_t launch_alc_scores(int B, int j, int p, int nc, const double *Xj, const double *Kinv, const double *cands,
+                              const int32_t *cand_idx, const double *x, double rtheta, double eta, double *delta,
+                              int32_t *best, double *gap, cudaStream_t st);
+cudaError_t launch_pinv_update(int B, int j, const double *Kinv, const double *k, double kdiag, double *Kout,
+                               cudaStream_t st);
+cudaError_t launch_predict(int B, int n, int p, const double *Xn, const double *Yn, const double *x, double rtheta,
+                           double eta, double *mean, double *s2, double *var, cudaStream_t st);
+
+}  // namespace lagp

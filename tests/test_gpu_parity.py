@@ -1,0 +1,245 @@
+"""GPU parity tests: the sm_100a path, called through the C ABI, against the
+CPU oracle on the same seeded inputs (rules in tests/parity.py)."""
+import numpy as np
+import pytest
+
+import oracle
+from lagp_data import make_config
+from parity import compare, tau_for
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_dev():
+    import torch
+
+    return torch, torch.device("cuda", 0)
+
+
+@pytest.fixture(scope="module")
+def lagp():
+    import paper_1310_5182_b200 as m
+
+    m.lib()
+    return m
+
+
+def T(torch, dev, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+# ------------------------------------------------------------------ a1: NN
+@pytest.mark.parametrize(
+    "name,M,N,Nprime",
+    [("C1", 100, None, 500), ("C2", 48, None, 1000), ("C3", 64, None, 1000), ("C3j", 32, None, 1000),
+     ("C1", 9, 600, 600), ("C1", 5, 300, 1), ("C2", 7, 5000, 4096)],
+)
+def test_nn_pool_bit_exact(torch_dev, lagp, name, M, N, Nprime):
+    torch, dev = torch_dev
+    cfg = make_config(name, M=M, N=N)
+    pool, d2 = lagp.nn_pool(T(torch, dev, cfg["X"]), T(torch, dev, cfg["XX"]), Nprime, with_d2=True)
+    pool = pool.cpu().numpy()
+    d2 = d2.cpu().numpy()
+    for i in range(M):
+        ref, rd2 = oracle.nn(cfg["X"], cfg["XX"][i], Nprime)
+        assert np.array_equal(pool[i], ref), (i, np.where(pool[i] != ref)[0][:5])
+        assert np.array_equal(d2[i], rd2)
+
+
+def test_nn_pool_massive_ties_fallback(torch_dev, lagp):
+    """Every row at the same distance -> threshold filter cannot split; the exact
+    radix-select fallback must return the lowest indices."""
+    torch, dev = torch_dev
+    X = np.zeros((20000, 2))
+    XX = np.array([[0.5, 0.5], [0.0, 0.0]])
+    pool = lagp.nn_pool(T(torch, dev, X), T(torch, dev, XX), 300).cpu().numpy()
+    assert (pool == np.arange(300)[None, :]).all()
+
+
+# ------------------------------------------------------------ a3: ALC score
+@pytest.mark.parametrize("j,p,nc", [(1, 2, 40), (6, 2, 500), (23, 8, 300), (49, 3, 1000), (128, 8, 77)])
+def test_alc_scores_vs_oracle(torch_dev, lagp, j, p, nc):
+    torch, dev = torch_dev
+    rng = np.random.default_rng(j * 100 + p)
+    B = 4
+    d, g = 0.3 if p > 3 else 0.05, 1e-4
+    Xj = rng.random((B, j, p))
+    cands = rng.random((B, nc, p))
+    x = rng.random((B, p))
+    Kinv = np.stack([oracle.invert_spd(np.exp(-((Xj[b][:, None] - Xj[b][None]) ** 2).sum(-1) / d) + g * np.eye(j))
+                     for b in range(B)])
+    cidx = np.stack([rng.permutation(10 * nc)[:nc] for _ in range(B)]).astype(np.int32)
+    delta, best, gap = lagp.alc_scores(T(torch, dev, Xj), T(torch, dev, Kinv), T(torch, dev, cands),
+                                       T(torch, dev, cidx), T(torch, dev, x), d, g)
+    delta = delta.cpu().numpy()
+    best = best.cpu().numpy()
+    for b in range(B):
+        ref, _, minv = oracle.alc_scores(Xj[b], Kinv[b], cands[b], x[b], d, g)
+        ok = minv > 1e-12
+        scale = np.abs(ref[ok]).max()
+        # explicit-inverse noise: eps * cond * j / min(s) (pin P1 ill-conditioned bound)
+        assert np.abs(delta[b][ok] - ref[ok]).max() <= max(1e-9, 1e-5 if p <= 3 else 1e-8) * scale
+        assert np.all(np.isneginf(delta[b][~ok]))
+        o = np.lexsort((cidx[b][ok], -ref[ok]))[0]
+        ob = np.where(ok)[0][o]
+        srt = np.sort(ref[ok])[::-1]
+        if len(srt) < 2 or (srt[0] - srt[1]) / srt[0] > 1e-6:
+            assert best[b] == ob
+
+
+# ------------------------------------------------------------- a4: update
+@pytest.mark.parametrize("j", [1, 5, 31, 64, 127])
+def test_pinv_update_vs_oracle(torch_dev, lagp, j):
+    torch, dev = torch_dev
+    rng = np.random.default_rng(j)
+    B, p, d, g = 3, 3, 0.05, 1e-3
+    XS = rng.random((B, j + 1, p))
+    K = np.exp(-((XS[:, :, None] - XS[:, None]) ** 2).sum(-1) / d) + g * np.eye(j + 1)
+    Kinv = np.stack([np.linalg.inv(K[b, :j, :j]) for b in range(B)])
+    Kinv = 0.5 * (Kinv + Kinv.transpose(0, 2, 1))  # exactly symmetric input
+    k = np.ascontiguousarray(K[:, :j, j])
+    out = lagp.pinv_update(T(torch, dev, Kinv), T(torch, dev, k), 1.0 + g).cpu().numpy()
+    for b in range(B):
+        ref, rc = oracle.pinv_update(Kinv[b], k[b], 1.0 + g)
+        assert np.linalg.norm(out[b] - ref) <= 1e-10 * np.linalg.norm(ref)
+        assert np.array_equal(out[b], out[b].T)
+
+
+# ------------------------------------------------------------- a5: predict
+@pytest.mark.parametrize("n,p", [(3, 2), (8, 1), (50, 8), (128, 3)])
+def test_predict_vs_oracle(torch_dev, lagp, n, p):
+    torch, dev = torch_dev
+    rng = np.random.default_rng(n + p)
+    B, d, g = 5, 0.2 if p > 2 else 0.02, 1e-4
+    Xn = rng.random((B, n, p))
+    Yn = rng.normal(size=(B, n))
+    x = rng.random((B, p))
+    mean, s2, var = (t.cpu().numpy() for t in lagp.predict(T(torch, dev, Xn), T(torch, dev, Yn), T(torch, dev, x),
+                                                          d, g))
+    for b in range(B):
+        m, s, v = oracle.predict(Xn[b], Yn[b], x[b], d, g)
+        assert abs(mean[b] - m) <= 1e-8 * max(1.0, abs(m))
+        assert abs(s2[b] - s) <= 1e-8 * s
+        if n > 2:
+            assert abs(var[b] - v) <= 1e-8 * v
+        else:
+            assert np.isnan(var[b])
+
+
+# ------------------------------------------------------- full path (a1-a5)
+def run_both(torch, dev, lagp, cfg, form="explicit", threads=0):
+    X, Z, XX = cfg["X"], cfg["Z"], cfg["XX"]
+    r = lagp.alc_batch(T(torch, dev, X), T(torch, dev, Z), T(torch, dev, XX), cfg["d"], cfg["g"], cfg["n0"], cfg["n"],
+                       cfg["Nprime"], form=form, gaps=True)
+    g = {k: v.cpu().numpy() for k, v in r.items() if hasattr(v, "cpu")}
+    o = oracle.alc_batch(X, Z, XX, cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"], threads=threads)
+    return g, o
+
+
+@pytest.mark.parametrize(
+    "name,M,N,over",
+    [
+        ("C1", 100, None, {}),  # full C1
+        ("C2", 96, None, {}),  # C2 design, 96 locations
+        ("C3", 96, None, {}),  # LGBB grid (distance ties at the N'-th NN)
+        ("C3j", 48, None, {}),
+        ("C1", 33, 800, dict(n0=1, n=12, Nprime=40)),
+        ("C1", 17, 500, dict(n0=6, n=6, Nprime=6)),  # no greedy step: NN only
+        ("C2", 9, 3000, dict(n0=4, n=128, Nprime=300)),  # n = LAGP_NMAX
+        ("C1", 5, 60, dict(n0=5, n=60, Nprime=60)),  # n = N' = N: full GP
+    ],
+)
+def test_alc_batch_vs_oracle(torch_dev, lagp, name, M, N, over):
+    torch, dev = torch_dev
+    cfg = make_config(name, M=M, N=N, **over)
+    g, o = run_both(torch, dev, lagp, cfg)
+    p = cfg["X"].shape[1]
+    rep = compare(g, o, cfg["n0"], float(np.std(cfg["Z"])), tau_for(p))
+    print(name, rep)
+
+
+def test_full_gp_special_case(torch_dev, lagp):
+    """n = N' = N: the local design is all of X; prediction equals Eq (1)-(2)."""
+    torch, dev = torch_dev
+    rng = np.random.default_rng(5)
+    X = rng.random((40, 2))
+    Z = np.sin(3 * X[:, 0]) + X[:, 1]
+    XX = rng.random((6, 2))
+    d, g = 0.1, 1e-4
+    r = lagp.alc_batch(T(torch, dev, X), T(torch, dev, Z), T(torch, dev, XX), d, g, 3, 40, 40)
+    K = np.exp(-((X[:, None] - X[None]) ** 2).sum(-1) / d) + g * np.eye(40)
+    for i in range(6):
+        assert sorted(r["idx"][i].cpu().tolist()) == list(range(40))
+        k = np.exp(-((X - XX[i]) ** 2).sum(-1) / d)
+        mu = k @ np.linalg.solve(K, Z)
+        s2 = (Z @ np.linalg.solve(K, Z)) * (1 + g - k @ np.linalg.solve(K, k)) / 40
+        assert abs(r["mean"][i].item() - mu) <= 1e-8 * max(1, abs(mu))
+        assert abs(r["s2"][i].item() - s2) <= 1e-7 * s2
+
+
+def test_exhausted_and_sentinel(torch_dev, lagp):
+    torch, dev = torch_dev
+    X = np.array([[0.5, 0.5]] * 3 + [[0.9, 0.9]])
+    Z = np.array([1.0, 1.0, 1.0, 2.0])
+    XX = np.array([[0.4, 0.5]])
+    cfg = dict(X=X, Z=Z, XX=XX, d=0.1, g=0.0, n0=1, n=3, Nprime=3)
+    g, o = run_both(torch, dev, lagp, cfg)
+    assert g["idx"].tolist() == o["idx"].tolist() == [[0, -1, -1]]
+    assert g["flags"][0] & lagp.FLAG_EXHAUSTED and g["flags"][0] & lagp.FLAG_SENTINEL
+    assert abs(g["mean"][0] - o["mean"][0]) < 1e-14 and abs(g["s2"][0] - o["s2"][0]) < 1e-14
+    assert np.isnan(g["var"][0])
+
+
+def test_exact_tie_lowest_index(torch_dev, lagp):
+    torch, dev = torch_dev
+    X = np.array([[0.0], [0.1], [-0.1], [0.2], [-0.2]])
+    Z = X[:, 0].copy()
+    cfg = dict(X=X, Z=Z, XX=np.array([[0.0]]), d=0.05, g=1e-4, n0=1, n=3, Nprime=5)
+    g, o = run_both(torch, dev, lagp, cfg)
+    assert g["idx"][0, :2].tolist() == [0, 1]
+    assert g["flags"][0] & lagp.FLAG_NEAR_TIE
+    assert g["gaps"][0, 0] == 0.0
+
+
+def test_determinism_and_chunk_composition(torch_dev, lagp):
+    torch, dev = torch_dev
+    cfg = make_config("C2", M=300, N=20000)
+    X, Z, XX = (T(torch, dev, cfg[k]) for k in ("X", "Z", "XX"))
+    args = (cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"])
+    a = lagp.alc_batch(X, Z, XX, *args)
+    b = lagp.alc_batch(X, Z, XX, *args)
+    c1 = lagp.alc_batch(X, Z, XX[:113], *args)
+    c2 = lagp.alc_batch(X, Z, XX[113:], *args)
+    for k in ("idx", "mean", "s2", "var", "flags"):
+        assert torch.equal(a[k], b[k]), k
+        assert torch.equal(a[k], torch.cat([c1[k], c2[k]])), k
+
+
+def test_host_entry_point_matches_device(torch_dev, lagp):
+    torch, dev = torch_dev
+    cfg = make_config("C1", M=20)
+    args = (cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"])
+    h = lagp.alc_batch_host(cfg["X"], cfg["Z"], cfg["XX"], *args)
+    d = lagp.alc_batch(T(torch, dev, cfg["X"]), T(torch, dev, cfg["Z"]), T(torch, dev, cfg["XX"]), *args)
+    assert np.array_equal(h["idx"], d["idx"].cpu().numpy())
+    assert np.array_equal(h["mean"], d["mean"].cpu().numpy())
+
+
+def test_full_size_C2_sampled(torch_dev, lagp):
+    """The bench configuration (C2: N=1e5, M=1e4) in the bench's launch
+    configuration, checked on a seeded sample of 48 locations."""
+    torch, dev = torch_dev
+    cfg = make_config("C2")
+    r = lagp.alc_batch(T(torch, dev, cfg["X"]), T(torch, dev, cfg["Z"]), T(torch, dev, cfg["XX"]), cfg["d"], cfg["g"],
+                       cfg["n0"], cfg["n"], cfg["Nprime"], gaps=True)
+    sel = np.sort(np.random.default_rng(7).choice(cfg["XX"].shape[0], 48, replace=False))
+    g = {k: v.cpu().numpy()[sel] for k, v in r.items() if hasattr(v, "cpu")}
+    o = oracle.alc_batch(cfg["X"], cfg["Z"], cfg["XX"][sel], cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"])
+    compare(g, o, cfg["n0"], float(np.std(cfg["Z"])), tau_for(8))
+    # properties at every location: flags clean, s2 > 0, indices distinct and in range
+    idx = r["idx"].cpu().numpy()
+    assert (idx >= 0).all() and (idx < cfg["X"].shape[0]).all()
+    srt = np.sort(idx, axis=1)
+    assert (np.diff(srt, axis=1) > 0).all()
+    assert (r["s2"].cpu().numpy() > 0).all()
