@@ -109,7 +109,10 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
 
     const int sms = num_sms();
     const int ld = (n + 3) & ~3;
-    const int alc_bps = lagp::alc_explicit_blocks_per_sm(ld, n, p);
+    const int Npad = (Nprime + 3) & ~3;
+    const int64_t cache_stride = (int64_t)n * Npad + 1024;  // + max tile width (tile overrun)
+    const int alc_bps = lagp::alc_explicit_blocks_per_sm(ld, n, p, Npad);
+    if (alc_bps <= 0) return fail(LAGP_EINVAL, "local-design state does not fit in shared memory (n=%d, Nprime=%d)", n, Nprime);
     const int alc_grid_max = alc_bps * sms;
     // chunk of locations per NN+ALC round: bounds the pool buffer (chunk × N' int32)
     const int64_t chunk = M < 65536 ? M : 65536;
@@ -119,8 +122,7 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
     Workspace ws(st);
     int32_t *pool = nullptr;
     void *nnws = nullptr;
-    double *cache = nullptr, *coords = nullptr, *kap = nullptr;
-    unsigned char *chosen = nullptr;
+    double *cache = nullptr, *coords = nullptr;
     int *counters = nullptr;  // [0] = partial count, [1] = NN fallbacks
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     float nn_ms = 0.f, alc_ms = 0.f, tot_ms = 0.f;
@@ -129,10 +131,8 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
 
     LAGP_CUDA(ws.alloc((void **)&pool, (size_t)chunk * Nprime * sizeof(int32_t)));
     LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(nn_grid)));
-    LAGP_CUDA(ws.alloc((void **)&cache, (size_t)alc_grid * n * Nprime * sizeof(double)));
-    LAGP_CUDA(ws.alloc((void **)&coords, (size_t)alc_grid * p * Nprime * sizeof(double)));
-    LAGP_CUDA(ws.alloc((void **)&kap, (size_t)alc_grid * Nprime * sizeof(double)));
-    LAGP_CUDA(ws.alloc((void **)&chosen, (size_t)alc_grid * Nprime));
+    LAGP_CUDA(ws.alloc((void **)&cache, (size_t)alc_grid * cache_stride * sizeof(double)));
+    LAGP_CUDA(ws.alloc((void **)&coords, (size_t)alc_grid * p * Npad * sizeof(double)));
     LAGP_CUDA(ws.alloc((void **)&counters, 2 * sizeof(int)));
     LAGP_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int), st));
     if (timing)
@@ -149,14 +149,14 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
         lagp::AlcArgs a;
         a.X = X; a.N = N; a.p = p; a.Z = Z; a.XX = XX + m0 * p; a.M = mc;
         a.eta = g; a.rtheta = 1.0 / d;
-        a.n0 = n0; a.n = n; a.Nprime = Nprime; a.ld = ld;
+        a.n0 = n0; a.n = n; a.Nprime = Nprime; a.ld = ld; a.Npad = Npad; a.cache_stride = cache_stride;
         a.pool = pool;
         a.idx_out = idx_out + m0 * n;
         a.mean = mean_out + m0; a.s2 = s2_out + m0;
         a.var = var_out ? var_out + m0 : nullptr;
         a.flags = flags_out ? flags_out + m0 : nullptr;
         a.gap_out = gap_out ? gap_out + m0 * (n - n0) : nullptr;
-        a.cache = cache; a.coords = coords; a.kap = kap; a.chosen = chosen;
+        a.cache = cache; a.coords = coords;
         a.n_partial = counters;
         int grid = (int)(mc < alc_grid ? mc : alc_grid);
         LAGP_CUDA(lagp::launch_alc_explicit(a, grid, st));

@@ -22,20 +22,20 @@ struct AlcArgs {
     int64_t M;
     double eta, rtheta;
     int n0, n, Nprime, ld;
+    int Npad;             // Nprime rounded up to a multiple of 4 (16-byte rows)
+    int64_t cache_stride; // doubles per CTA cache slab (n*Npad + tile overrun pad)
     const int32_t *pool;  // [M][Nprime], first n0 = NN order
     int32_t *idx_out;
     double *mean, *s2, *var;
     uint32_t *flags;
     double *gap_out;
     // per-CTA slabs in global memory
-    double *cache;          // [grid][n][Nprime] rows of K(X_j[a], x_c)
-    double *coords;         // [grid][p][Nprime] pool coordinates (SoA)
-    double *kap;            // [grid][Nprime]    kappa_c = K(x_c, x)
-    unsigned char *chosen;  // [grid][Nprime]
+    double *cache;          // [grid][cache_stride]: rows a of K(X_j[a], x_c), row stride Npad
+    double *coords;         // [grid][p][Npad] pool coordinates (SoA)
     int *n_partial;         // count of EXHAUSTED/NONFINITE locations
 };
 cudaError_t launch_alc_explicit(const AlcArgs &a, int grid, cudaStream_t st);
-int alc_explicit_blocks_per_sm(int ld, int n, int p);
+int alc_explicit_blocks_per_sm(int ld, int n, int p, int Npad);
 
 // diag.cu (rows a3, a4, a5 alone)
 cudaError_t launch_alc_scores(int B, int j, int p, int nc, const double *Xj, const double *Kinv, const double *cands,
