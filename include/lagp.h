@@ -55,9 +55,14 @@ enum {
  *  LAGP_ALC_EXPLICIT    — the paper's: explicit K_j^{-1} kept per location and
  *                         s_c = 1 + eta - k_c^T K_j^{-1} k_c per candidate per
  *                         step (Eq (5)-(6), Fig 3 step 3), O(j^2) per candidate.
+ *                         For n <= 64 the j×j × j×T products run on the FP64
+ *                         tensor path (mma.sync m8n8k4 f64, SASS DMMA); for
+ *                         larger n on a register-blocked DFMA micro-kernel.
  *  LAGP_ALC_INCREMENTAL — SURVEY §8f row f1: per-candidate Schur-complement
- *                         downdates, O(j) per candidate per step. */
-typedef enum { LAGP_ALC_EXPLICIT = 0, LAGP_ALC_INCREMENTAL = 1 } lagp_alc_form;
+ *                         downdates, O(j) per candidate per step.
+ *  LAGP_ALC_EXPLICIT_DFMA — the explicit form forced onto the DFMA micro-kernel
+ *                         for every n (the comparison arm for the DMMA choice). */
+typedef enum { LAGP_ALC_EXPLICIT = 0, LAGP_ALC_INCREMENTAL = 1, LAGP_ALC_EXPLICIT_DFMA = 2 } lagp_alc_form;
 
 /* Phase timings (milliseconds, CUDA events on cuda_stream) filled when the
  * optional `timing` argument is non-NULL. */

@@ -35,7 +35,7 @@ from ._lib import (  # noqa: F401
 
 _LIB = None
 
-FORMS = {"explicit": ALC_EXPLICIT, "incremental": ALC_INCREMENTAL}
+FORMS = {"explicit": ALC_EXPLICIT, "incremental": ALC_INCREMENTAL, "explicit_dfma": _lib.ALC_EXPLICIT_DFMA}
 
 
 class LagpError(RuntimeError):

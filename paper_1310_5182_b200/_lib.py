@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(_PKG, "liblagp_b200.so")
 
 LAGP_OK, LAGP_PARTIAL, LAGP_EINVAL, LAGP_ECUDA, LAGP_ENOMEM = 0, 1, 2, 3, 4
 FLAG_NEAR_TIE, FLAG_SENTINEL, FLAG_EXHAUSTED, FLAG_NONFINITE = 1, 2, 4, 8
-ALC_EXPLICIT, ALC_INCREMENTAL = 0, 1
+ALC_EXPLICIT, ALC_INCREMENTAL, ALC_EXPLICIT_DFMA = 0, 1, 2
 NMAX, PMAX = 128, 16
 
 EXPORTS = (

@@ -98,8 +98,10 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
                               double *gap_out, int32_t alc_form, lagp_timing *timing, void *cuda_stream) {
     lagp_status chk = check_batch_args(X, N, p, Z, XX, M, d, g, n0, n, Nprime, idx_out, mean_out, s2_out);
     if (chk != LAGP_OK) return chk;
-    if (alc_form != LAGP_ALC_EXPLICIT && alc_form != LAGP_ALC_INCREMENTAL)
-        return fail(LAGP_EINVAL, "alc_form must be LAGP_ALC_EXPLICIT or LAGP_ALC_INCREMENTAL (got %d)", alc_form);
+    if (alc_form != LAGP_ALC_EXPLICIT && alc_form != LAGP_ALC_INCREMENTAL && alc_form != LAGP_ALC_EXPLICIT_DFMA)
+        return fail(LAGP_EINVAL,
+                    "alc_form must be LAGP_ALC_EXPLICIT, LAGP_ALC_INCREMENTAL or LAGP_ALC_EXPLICIT_DFMA (got %d)",
+                    alc_form);
     if (alc_form == LAGP_ALC_INCREMENTAL)
         return fail(LAGP_EINVAL, "alc_form LAGP_ALC_INCREMENTAL is not built yet");
     cudaStream_t st = (cudaStream_t)cuda_stream;
@@ -111,8 +113,12 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
     const int ld = (n + 3) & ~3;
     const int Npad = (Nprime + 3) & ~3;
     const int64_t cache_stride = (int64_t)n * Npad + 1024;  // + max tile width (tile overrun)
-    const int alc_bps = lagp::alc_explicit_blocks_per_sm(ld, n, p, Npad);
-    if (alc_bps <= 0) return fail(LAGP_EINVAL, "local-design state does not fit in shared memory (n=%d, Nprime=%d)", n, Nprime);
+    // explicit form: DMMA (FP64 tensor) micro-kernel for n <= 64, DFMA otherwise
+    const bool use_dmma = (alc_form == LAGP_ALC_EXPLICIT) && n <= 64;
+    const int alc_bps = use_dmma ? lagp::alc_explicit_dmma_blocks_per_sm(n, p, Npad)
+                                 : lagp::alc_explicit_blocks_per_sm(ld, n, p, Npad);
+    if (alc_bps <= 0)
+        return fail(LAGP_EINVAL, "local-design state does not fit in shared memory (n=%d, Nprime=%d)", n, Nprime);
     const int alc_grid_max = alc_bps * sms;
     // chunk of locations per NN+ALC round: bounds the pool buffer (chunk × N' int32)
     const int64_t chunk = M < 65536 ? M : 65536;
@@ -159,7 +165,7 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
         a.cache = cache; a.coords = coords;
         a.n_partial = counters;
         int grid = (int)(mc < alc_grid ? mc : alc_grid);
-        LAGP_CUDA(lagp::launch_alc_explicit(a, grid, st));
+        LAGP_CUDA(use_dmma ? lagp::launch_alc_explicit_dmma(a, grid, st) : lagp::launch_alc_explicit(a, grid, st));
         launches++;
         if (timing) {
             LAGP_CUDA(cudaEventRecord(ev[3], st));

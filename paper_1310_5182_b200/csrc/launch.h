@@ -36,6 +36,8 @@ struct AlcArgs {
 };
 cudaError_t launch_alc_explicit(const AlcArgs &a, int grid, cudaStream_t st);
 int alc_explicit_blocks_per_sm(int ld, int n, int p, int Npad);
+cudaError_t launch_alc_explicit_dmma(const AlcArgs &a, int grid, cudaStream_t st);
+int alc_explicit_dmma_blocks_per_sm(int n, int p, int Npad);
 
 // diag.cu (rows a3, a4, a5 alone)
 cudaError_t launch_alc_scores(int B, int j, int p, int nc, const double *Xj, const double *Kinv, const double *cands,

@@ -150,13 +150,14 @@ def run_both(torch, dev, lagp, cfg, form="explicit", threads=0):
         ("C1", 5, 60, dict(n0=5, n=60, Nprime=60)),  # n = N' = N: full GP
     ],
 )
-def test_alc_batch_vs_oracle(torch_dev, lagp, name, M, N, over):
+@pytest.mark.parametrize("form", ["explicit", "explicit_dfma"])
+def test_alc_batch_vs_oracle(torch_dev, lagp, name, M, N, over, form):
     torch, dev = torch_dev
     cfg = make_config(name, M=M, N=N, **over)
-    g, o = run_both(torch, dev, lagp, cfg)
+    g, o = run_both(torch, dev, lagp, cfg, form=form)
     p = cfg["X"].shape[1]
     rep = compare(g, o, cfg["n0"], float(np.std(cfg["Z"])), tau_for(p))
-    print(name, rep)
+    print(name, form, rep)
 
 
 def test_full_gp_special_case(torch_dev, lagp):
