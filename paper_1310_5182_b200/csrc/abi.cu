@@ -47,12 +47,22 @@ int num_sms() {
 
 bool finite_pos(double v) { return std::isfinite(v) && v > 0.0; }
 
-// Stream-ordered workspace allocations released in one place.
+// Stream-ordered workspace allocations released in one place. The device's
+// default memory pool keeps freed blocks (release threshold raised once per
+// call, idempotent) so repeated calls do not return the workspace to the OS
+// and re-map it at every synchronisation.
 struct Workspace {
     cudaStream_t st;
     void *ptrs[16];
     int n = 0;
-    explicit Workspace(cudaStream_t s) : st(s) {}
+    explicit Workspace(cudaStream_t s) : st(s) {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = 8ull << 30;  // keep up to 8 GiB cached
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     cudaError_t alloc(void **p, size_t bytes) {
         if (bytes == 0) bytes = 16;
         cudaError_t e = cudaMallocAsync(p, bytes, st);
@@ -102,8 +112,6 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
         return fail(LAGP_EINVAL,
                     "alc_form must be LAGP_ALC_EXPLICIT, LAGP_ALC_INCREMENTAL or LAGP_ALC_EXPLICIT_DFMA (got %d)",
                     alc_form);
-    if (alc_form == LAGP_ALC_INCREMENTAL)
-        return fail(LAGP_EINVAL, "alc_form LAGP_ALC_INCREMENTAL is not built yet");
     cudaStream_t st = (cudaStream_t)cuda_stream;
     lagp_status st_ret = LAGP_OK;
     if (timing) std::memset(timing, 0, sizeof *timing);
@@ -112,11 +120,25 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
     const int sms = num_sms();
     const int ld = (n + 3) & ~3;
     const int Npad = (Nprime + 3) & ~3;
-    const int64_t cache_stride = (int64_t)n * Npad + 1024;  // + max tile width (tile overrun)
+    int64_t cache_stride = (int64_t)n * Npad + 1024;  // + max tile width (tile overrun)
+    const bool incremental = alc_form == LAGP_ALC_INCREMENTAL;
     // explicit form: DMMA (FP64 tensor) micro-kernel for n <= 64, DFMA otherwise
     const bool use_dmma = (alc_form == LAGP_ALC_EXPLICIT) && n <= 64;
-    const int alc_bps = use_dmma ? lagp::alc_explicit_dmma_blocks_per_sm(n, p, Npad)
-                                 : lagp::alc_explicit_blocks_per_sm(ld, n, p, Npad);
+    lagp::IncPlan plan{};
+    int alc_bps = 0;
+    if (incremental) {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        plan = lagp::inc_plan(n, p, Nprime, Npad, (size_t)optin - 2048);
+        if (!plan.ok)
+            return fail(LAGP_EINVAL, "incremental form: Nprime=%d / n=%d exceed this build's limits", Nprime, n);
+        alc_bps = 1;
+        cache_stride = (int64_t)plan.global_entries * Npad + 1024;
+    } else {
+        alc_bps = use_dmma ? lagp::alc_explicit_dmma_blocks_per_sm(n, p, Npad)
+                           : lagp::alc_explicit_blocks_per_sm(ld, n, p, Npad);
+    }
     if (alc_bps <= 0)
         return fail(LAGP_EINVAL, "local-design state does not fit in shared memory (n=%d, Nprime=%d)", n, Nprime);
     const int alc_grid_max = alc_bps * sms;
@@ -136,7 +158,7 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
     int host_counters[2] = {0, 0};
 
     LAGP_CUDA(ws.alloc((void **)&pool, (size_t)chunk * Nprime * sizeof(int32_t)));
-    LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(nn_grid)));
+    LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(nn_grid, N, p, Nprime)));
     LAGP_CUDA(ws.alloc((void **)&cache, (size_t)alc_grid * cache_stride * sizeof(double)));
     LAGP_CUDA(ws.alloc((void **)&coords, (size_t)alc_grid * p * Npad * sizeof(double)));
     LAGP_CUDA(ws.alloc((void **)&counters, 2 * sizeof(int)));
@@ -148,9 +170,8 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
     for (int64_t m0 = 0; m0 < M; m0 += chunk) {
         const int64_t mc = (M - m0) < chunk ? (M - m0) : chunk;
         if (timing) LAGP_CUDA(cudaEventRecord(ev[1], st));
-        LAGP_CUDA(lagp::launch_nn(X, N, p, XX + m0 * p, mc, Nprime, pool, nullptr, nnws,
-                                  lagp::nn_grid(mc, sms), counters + 1, st));
-        launches++;
+        LAGP_CUDA(lagp::launch_nn(X, N, p, XX + m0 * p, mc, Nprime, n0, false, pool, nullptr, nnws,
+                                  lagp::nn_grid(mc, sms), counters + 1, st, m0 > 0, &launches));
         if (timing) LAGP_CUDA(cudaEventRecord(ev[2], st));
         lagp::AlcArgs a;
         a.X = X; a.N = N; a.p = p; a.Z = Z; a.XX = XX + m0 * p; a.M = mc;
@@ -165,7 +186,10 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
         a.cache = cache; a.coords = coords;
         a.n_partial = counters;
         int grid = (int)(mc < alc_grid ? mc : alc_grid);
-        LAGP_CUDA(use_dmma ? lagp::launch_alc_explicit_dmma(a, grid, st) : lagp::launch_alc_explicit(a, grid, st));
+        if (incremental)
+            LAGP_CUDA(lagp::launch_alc_incremental(a, plan, grid, st));
+        else
+            LAGP_CUDA(use_dmma ? lagp::launch_alc_explicit_dmma(a, grid, st) : lagp::launch_alc_explicit(a, grid, st));
         launches++;
         if (timing) {
             LAGP_CUDA(cudaEventRecord(ev[3], st));
@@ -270,10 +294,11 @@ lagp_status laGP_nn_pool(const double *X, int64_t N, int32_t p, const double *XX
         void *nnws = nullptr;
         int *fb = nullptr;
         const int grid = lagp::nn_grid(M, num_sms());
-        LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(grid)));
+        LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(grid, N, p, Nprime)));
         LAGP_CUDA(ws.alloc((void **)&fb, sizeof(int)));
         LAGP_CUDA(cudaMemsetAsync(fb, 0, sizeof(int), st));
-        LAGP_CUDA(lagp::launch_nn(X, N, p, XX, M, Nprime, pool_out, d2_out, nnws, grid, fb, st));
+        LAGP_CUDA(lagp::launch_nn(X, N, p, XX, M, Nprime, Nprime, true, pool_out, d2_out, nnws, grid, fb, st, false,
+                                  nullptr));
     cleanup:;
     }
     cudaError_t e = cudaStreamSynchronize(st);

@@ -7,9 +7,12 @@
 namespace lagp {
 
 // nn.cu (row a1)
-cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64_t M, int Nprime, int32_t *pool,
-                      double *d2, void *ws, int grid, int *fb, cudaStream_t st);
-size_t nn_ws_bytes(int grid);
+// sorted = true: the whole pool ascending by (d^2, index) (laGP_nn_pool); false:
+// pool[0..n0) ascending, the rest of the N' nearest in any order (laGP_alc_batch).
+cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64_t M, int Nprime, int n0, bool sorted,
+                      int32_t *pool, double *d2, void *ws, int grid, int *fb, cudaStream_t st, bool prepared,
+                      int *launches);
+size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime);
 int nn_grid(int64_t M, int num_sms);
 
 // fused local-design kernels (rows a2-a5)
@@ -37,6 +40,19 @@ struct AlcArgs {
 cudaError_t launch_alc_explicit(const AlcArgs &a, int grid, cudaStream_t st);
 int alc_explicit_blocks_per_sm(int ld, int n, int p, int Npad);
 cudaError_t launch_alc_explicit_dmma(const AlcArgs &a, int grid, cudaStream_t st);
+
+// alc_incremental.cu (row f1): where the per-candidate w_c entries live
+struct IncPlan {
+    bool ok;
+    int cpt;             // candidates per thread (1024 threads)
+    int R;               // entries in registers
+    int S;               // entries in shared memory
+    int global_entries;  // entries in the per-CTA HBM slab (A.cache)
+    int wsz;             // doubles of the shared w region (>= S*Npad, >= predict scratch)
+    size_t smem;         // dynamic shared memory bytes
+};
+IncPlan inc_plan(int n, int p, int Nprime, int Npad, size_t smem_optin);
+cudaError_t launch_alc_incremental(const AlcArgs &a, const IncPlan &pl, int grid, cudaStream_t st);
 int alc_explicit_dmma_blocks_per_sm(int n, int p, int Npad);
 
 // diag.cu (rows a3, a4, a5 alone)

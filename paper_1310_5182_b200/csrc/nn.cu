@@ -3,10 +3,12 @@
 // NN candidate restriction P:484-487), exact by the key (d^2, row index) with
 // d^2 accumulated by fma in the order k = 0..p-1 (reading R8).
 //
-// B200 design (DESIGN.md §6.1): a persistent grid of CTAs, each handling NN_Q
+// B200 design (DESIGN.md §5.2): a persistent grid of CTAs, each handling NN_Q
 // queries at a time. One pass streams X through registers (coalesced rows) and
 // evaluates all NN_Q queries per row, so X is read from L2 once per NN_Q
-// queries. Selection is threshold-then-sort: a strided sample of X gives a
+// queries. The pass is a paired-FP32 (FFMA2, sm_100) prefilter on an FP32 copy
+// of X with a rigorous rounding margin; only rows that pass it get the exact
+// FP64 key, which alone decides membership. Selection is threshold-then-sort: a strided sample of X gives a
 // per-query threshold tau at ~1.5 N' expected survivors; the filter pass
 // appends (d^2, i) with d^2 <= tau to a per-query buffer; the buffer is
 // bitonic-sorted in shared memory by (key bits, index) and its first N' rows
@@ -21,7 +23,7 @@
 namespace lagp {
 
 constexpr int NN_THREADS = 256;
-constexpr int NN_Q = 8;
+constexpr int NN_Q = 16;
 constexpr int NN_SAMPLE = 2048;
 constexpr int NN_CAP = 8192;
 constexpr int NN_MAX_ROUNDS = 6;
@@ -30,11 +32,18 @@ struct NNSmem {
     uint64_t key[NN_CAP];
     int32_t idx[NN_CAP];
     double qx[NN_Q][LAGP_PMAX];
+    float nqf[NN_Q][LAGP_PMAX];  // -(query coords) in FP32 for the prefilter
     double tau[NN_Q];
+    float thrf[NN_Q];            // FP32 prefilter threshold: tau + rounding margin, rounded up
+    double qn2[NN_Q];            // ||x_q||^2 (for the margin)
     int cnt[NN_Q];
     int rank[NN_Q];
     int state[NN_Q];  // 0 = active, 1 = done, 2 = fallback
+    int valid[NN_Q];  // survivors with exact d2 <= tau
     unsigned hist[256];
+    unsigned whist[NN_THREADS / 32][256];  // per-warp histograms (sample quantiles)
+    unsigned long long redk[NN_THREADS / 32];
+    int redi[NN_THREADS / 32];
     int scan[NN_THREADS / 32];
     int misc[4];
 };
@@ -87,6 +96,34 @@ __device__ __forceinline__ double row_d2(const double *xr, const double *q, int 
     return acc;
 }
 
+// Warp 0 finds the bin of a 256-bin histogram holding the need-th element
+// (1-based): misc[0] = bin, misc[1] = rank within the bin, misc[2] = bin count.
+__device__ __forceinline__ void warp_pick_bin(const unsigned *hist, int need, int *misc) {
+    const int lane = threadIdx.x & 31;
+    unsigned loc[8], tot = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) { loc[i] = hist[lane * 8 + i]; tot += loc[i]; }
+    unsigned incl = tot;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += y;
+    }
+    const unsigned excl = incl - tot;
+    if (excl < (unsigned)need && incl >= (unsigned)need) {
+        unsigned acc = excl;
+        for (int i = 0; i < 8; i++) {
+            if (acc + loc[i] >= (unsigned)need) {
+                misc[0] = lane * 8 + i;
+                misc[1] = need - (int)acc;
+                misc[2] = (int)loc[i];
+                break;
+            }
+            acc += loc[i];
+        }
+    }
+}
+
 // Exact fallback for one query (index q within the group): radix select of the
 // Nprime-th smallest 64-bit key, then an ordered collection that takes every
 // key below it plus the lowest-index rows equal to it. Leaves s.key/s.idx
@@ -108,16 +145,7 @@ __device__ void nn_exact_select(NNSmem &s, const double *__restrict__ X, int64_t
             if ((k & hmask) == prefix) atomicAdd(&s.hist[(k >> shift) & 255u], 1u);
         }
         __syncthreads();
-        if (tid == 0) {
-            unsigned acc = 0;
-            int b = 0;
-            for (; b < 256; b++) {
-                if (acc + s.hist[b] >= (unsigned)need) break;
-                acc += s.hist[b];
-            }
-            s.misc[0] = b;
-            s.misc[1] = need - (int)acc;
-        }
+        if (tid < 32) warp_pick_bin(s.hist, need, s.misc);
         __syncthreads();
         prefix |= ((uint64_t)s.misc[0]) << shift;
         need = s.misc[1];
@@ -167,108 +195,336 @@ __device__ void nn_exact_select(NNSmem &s, const double *__restrict__ X, int64_t
     __syncthreads();
 }
 
+// FP32 copy of X for the prefilter and B = max_i ||X_i||^2 (as ordered uint64 bits).
+__global__ void nn_prep_kernel(const double *__restrict__ X, int64_t N, int p, float *__restrict__ X32,
+                               unsigned long long *__restrict__ maxn2) {
+    double mx = 0.0;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
+        double n2 = 0.0;
+        for (int k = 0; k < p; k++) {
+            const double v = X[r * p + k];
+            X32[r * p + k] = (float)v;
+            n2 = fma(v, v, n2);
+        }
+        mx = fmax(mx, n2);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxn2, (unsigned long long)__double_as_longlong(mx));
+}
+
+// FP32 row of the prefilter copy (P compile-time, 0 = generic)
+template <int P>
+__device__ __forceinline__ void load_row32(const float *__restrict__ X32, int64_t row, int p, float *xf) {
+    const float *src = X32 + row * (int64_t)(P ? P : p);
+    if (P == 8) {
+        const float4 a = __ldg(reinterpret_cast<const float4 *>(src));
+        const float4 b = __ldg(reinterpret_cast<const float4 *>(src) + 1);
+        xf[0] = a.x; xf[1] = a.y; xf[2] = a.z; xf[3] = a.w;
+        xf[4] = b.x; xf[5] = b.y; xf[6] = b.z; xf[7] = b.w;
+    } else if (P == 4) {
+        const float4 a = __ldg(reinterpret_cast<const float4 *>(src));
+        xf[0] = a.x; xf[1] = a.y; xf[2] = a.z; xf[3] = a.w;
+    } else if (P == 2) {
+        const float2 a = __ldg(reinterpret_cast<const float2 *>(src));
+        xf[0] = a.x; xf[1] = a.y;
+    } else {
+#pragma unroll
+        for (int k = 0; k < (P ? P : LAGP_PMAX); k++)
+            if (P || k < p) xf[k] = __ldg(src + k);
+    }
+}
+
+// paired-FP32 prefilter distance: sum_k (x_k - q_k)^2 with FFMA2 (nq = -q)
+template <int P>
+__device__ __forceinline__ float row_d2f(const float *xf, const float *nq, int p) {
+    constexpr int PP = P ? P : LAGP_PMAX;
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k + 1 < PP; k += 2) {
+        if (P || k + 1 < p) {
+            const float2 d = __fadd2_rn(make_float2(xf[k], xf[k + 1]), make_float2(nq[k], nq[k + 1]));
+            acc = __ffma2_rn(d, d, acc);
+        } else if (!P && k < p) {
+            const float d = xf[k] + nq[k];
+            acc.x = fmaf(d, d, acc.x);
+        }
+    }
+    if (PP & 1) {
+        const int k = PP - 1;
+        if (P || k < p) {
+            const float d = xf[k] + nq[k];
+            acc.x = fmaf(d, d, acc.x);
+        }
+    }
+    return acc.x + acc.y;
+}
+
+// Upper edge of the 16-bit (sign+exponent+7 mantissa bits) bin holding the r-th
+// smallest (1-based) of S non-negative floats, by a two-pass warp radix select.
+// Used only to pick a threshold; an over-estimate just admits a few more rows.
+__device__ float warp_quantile(const float *__restrict__ v, int S, int r, unsigned *hist) {
+    const int lane = threadIdx.x & 31;
+    if (r > S) return INFINITY;
+    unsigned prefix = 0;
+    int need = r;
+    for (int pass = 0; pass < 2; pass++) {
+        const int sh = pass == 0 ? 24 : 16;
+        for (int b = lane; b < 256; b += 32) hist[b] = 0;
+        __syncwarp();
+        for (int t = lane; t < S; t += 32) {
+            const unsigned bits = __float_as_uint(v[t]);
+            if (pass == 0 || (bits >> 24) == prefix) atomicAdd(&hist[(bits >> sh) & 255u], 1u);
+        }
+        __syncwarp();
+        unsigned loc[8], tot = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) { loc[i] = hist[lane * 8 + i]; tot += loc[i]; }
+        unsigned incl = tot;  // inclusive warp scan of per-lane totals
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
+        }
+        const unsigned excl = incl - tot;
+        int bin = -1, below = 0;
+        if (excl < (unsigned)need && incl >= (unsigned)need) {
+            unsigned acc = excl;
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                if (bin < 0 && acc + loc[i] >= (unsigned)need) { bin = lane * 8 + i; below = (int)acc; }
+                acc += loc[i];
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, bin >= 0);
+        const int src = __ffs(m) - 1;
+        bin = __shfl_sync(0xffffffffu, bin, src);
+        below = __shfl_sync(0xffffffffu, below, src);
+        need -= below;
+        prefix = pass == 0 ? (unsigned)bin : ((prefix << 8) | (unsigned)bin);
+        __syncwarp();
+    }
+    return __uint_as_float((prefix << 16) | 0xFFFFu);
+}
+
+// (key, idx) composite order
+__device__ __forceinline__ bool kv_less(unsigned long long ka, int ia, unsigned long long kb, int ib) {
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+// Exact selection of the Nprime smallest (key, idx) of the c survivors held in
+// s.key/s.idx[0..c): radix select of the Nprime-th composite value (8 key
+// digits, then 4 index digits only if the key is tied), then the n0 smallest in
+// ascending order by n0 block-argmin rounds (pool[0..n0) = X_{n0}(x) in NN
+// order), then the rest compacted in any order (positions >= n0 never affect
+// results: every candidate's score and the (Delta, index) argmax are
+// order-independent).
+__device__ void select_pool(NNSmem &s, int c, int Nprime, int n0, int32_t *__restrict__ po) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    unsigned long long kth = 0;
+    int need = Nprime;
+    for (int sh = 56; sh >= 0; sh -= 8) {
+        for (int b = tid; b < 256; b += blockDim.x) s.hist[b] = 0;
+        __syncthreads();
+        const unsigned long long hm = (sh == 56) ? 0ull : (~0ull << (sh + 8));
+        for (int t = tid; t < c; t += blockDim.x)
+            if ((s.key[t] & hm) == kth) atomicAdd(&s.hist[(s.key[t] >> sh) & 255u], 1u);
+        __syncthreads();
+        if (tid < 32) warp_pick_bin(s.hist, need, s.misc);  // misc[2] = elements sharing this prefix
+        __syncthreads();
+        kth |= ((unsigned long long)s.misc[0]) << sh;
+        need = s.misc[1];
+        __syncthreads();
+    }
+    int ith = 0x7fffffff;  // composite tie break on the index
+    if (s.misc[2] > need) {
+        unsigned ip = 0;
+        for (int sh = 24; sh >= 0; sh -= 8) {
+            for (int b = tid; b < 256; b += blockDim.x) s.hist[b] = 0;
+            __syncthreads();
+            const unsigned hm = (sh == 24) ? 0u : (~0u << (sh + 8));
+            for (int t = tid; t < c; t += blockDim.x)
+                if (s.key[t] == kth && ((unsigned)s.idx[t] & hm) == ip)
+                    atomicAdd(&s.hist[((unsigned)s.idx[t] >> sh) & 255u], 1u);
+            __syncthreads();
+            if (tid < 32) warp_pick_bin(s.hist, need, s.misc);
+            __syncthreads();
+            ip |= ((unsigned)s.misc[0]) << sh;
+            need = s.misc[1];
+            __syncthreads();
+        }
+        ith = (int)ip;
+    }
+    // mark members: idx >= 0 in, set bit 31 for non-members / taken ones
+    for (int t = tid; t < c; t += blockDim.x) {
+        const bool in = kv_less(s.key[t], s.idx[t], kth, ith) || (s.key[t] == kth && s.idx[t] == ith);
+        if (!in) s.idx[t] |= (int)0x80000000;
+    }
+    __syncthreads();
+    // n0 smallest in ascending (key, idx) order
+    for (int r = 0; r < n0; r++) {
+        unsigned long long bk = ~0ull;
+        int bi = 0x7fffffff, bt = -1;
+        for (int t = tid; t < c; t += blockDim.x)
+            if (s.idx[t] >= 0 && kv_less(s.key[t], s.idx[t], bk, bi)) { bk = s.key[t]; bi = s.idx[t]; bt = t; }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+            const int ot = __shfl_xor_sync(0xffffffffu, bt, off);
+            if (kv_less(ok, oi, bk, bi)) { bk = ok; bi = oi; bt = ot; }
+        }
+        if (lane == 0) { s.redk[wid] = bk; s.redi[wid] = bi; s.scan[wid] = bt; }
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long k0 = s.redk[0];
+            int i0 = s.redi[0], t0 = s.scan[0];
+            for (int w = 1; w < nw; w++)
+                if (kv_less(s.redk[w], s.redi[w], k0, i0)) { k0 = s.redk[w]; i0 = s.redi[w]; t0 = s.scan[w]; }
+            po[r] = i0;
+            s.idx[t0] |= (int)0x80000000;
+        }
+        __syncthreads();
+    }
+    // the other members, any order
+    if (tid == 0) s.misc[3] = n0;
+    __syncthreads();
+    for (int t = tid; t < c; t += blockDim.x)
+        if (s.idx[t] >= 0) po[atomicAdd(&s.misc[3], 1)] = s.idx[t];
+    __syncthreads();
+}
+
 template <int P>
 __global__ void __launch_bounds__(NN_THREADS)
-nn_pool_kernel(const double *__restrict__ X, int64_t N, int p, const double *__restrict__ XX, int64_t M,
-               int Nprime, int32_t *__restrict__ pool_out, double *__restrict__ d2_out,
-               double *__restrict__ samp_ws, uint64_t *__restrict__ bufk_ws, int32_t *__restrict__ bufi_ws,
-               int *__restrict__ fallback_count) {
+nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, const unsigned long long *maxn2_bits,
+               int64_t N, int p, const double *__restrict__ XX, int64_t M, int Nprime, int n0, int bufcap,
+               int sorted, int32_t *__restrict__ pool_out, double *__restrict__ d2_out, float *__restrict__ samp_ws,
+               uint64_t *__restrict__ bufk_ws, int32_t *__restrict__ bufi_ws, int *__restrict__ fallback_count) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     NNSmem &s = *reinterpret_cast<NNSmem *>(smem_raw);
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
     const int64_t ngroups = (M + NN_Q - 1) / NN_Q;
     const int S = (int)(N < NN_SAMPLE ? N : NN_SAMPLE);
-    double *samp = samp_ws + (size_t)blockIdx.x * NN_Q * NN_SAMPLE;
-    uint64_t *bufk = bufk_ws + (size_t)blockIdx.x * NN_Q * NN_CAP;
-    int32_t *bufi = bufi_ws + (size_t)blockIdx.x * NN_Q * NN_CAP;
+    float *samp = samp_ws + (size_t)blockIdx.x * NN_Q * NN_SAMPLE;
+    uint64_t *bufk = bufk_ws + (size_t)blockIdx.x * NN_Q * bufcap;
+    int32_t *bufi = bufi_ws + (size_t)blockIdx.x * NN_Q * bufcap;
+    const double Bn2 = __longlong_as_double((long long)*maxn2_bits);
+    const double u32 = 5.9604644775390625e-08;  // 2^-24, FP32 unit roundoff
 
     for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
         const int64_t q0 = grp * NN_Q;
         const int nq = (int)((M - q0) < NN_Q ? (M - q0) : NN_Q);
         for (int e = tid; e < NN_Q * LAGP_PMAX; e += blockDim.x) {
             int q = e / LAGP_PMAX, k = e % LAGP_PMAX;
-            s.qx[q][k] = (q < nq && k < p) ? XX[(q0 + q) * p + k] : 0.0;
+            const double v = (q < nq && k < p) ? XX[(q0 + q) * p + k] : 0.0;
+            s.qx[q][k] = v;
+            s.nqf[q][k] = -(float)v;
         }
         __syncthreads();
-
-        // ---- sample phase: sorted strided sample of d^2 per query
-        for (int q = 0; q < nq; q++) {
-            int npow = 1;
-            while (npow < S) npow <<= 1;
-            for (int t = tid; t < npow; t += blockDim.x) {
-                if (t < S) {
-                    int64_t r = (int64_t)t * N / S;
-                    double xr[P ? P : LAGP_PMAX];
-                    load_row<P>(X, r, p, xr);
-                    s.key[t] = d2_key(row_d2<P>(xr, s.qx[q], p));
-                    s.idx[t] = (int)r;
-                } else {
-                    s.key[t] = ~0ull;
-                    s.idx[t] = 0x7fffffff;
-                }
-            }
-            __syncthreads();
-            bitonic_sort(s, npow);
-            for (int t = tid; t < S; t += blockDim.x) samp[q * NN_SAMPLE + t] = __longlong_as_double((long long)s.key[t]);
-            __syncthreads();
-            if (tid == 0) {
-                // target ~1.5 N' survivors (+ a few sample ranks of slack)
-                double want = 1.5 * (double)Nprime * (double)S / (double)N;
-                int r = (int)ceil(want) + 12;
-                if (Nprime >= N || r >= S) r = S;  // tau = +inf: take every row
-                s.rank[q] = r;
-                s.state[q] = 0;
-            }
-            __syncthreads();
+        if (tid < NN_Q) {
+            double n2 = 0.0;
+            for (int k = 0; k < p; k++) n2 = fma(s.qx[tid][k], s.qx[tid][k], n2);
+            s.qn2[tid] = n2;
         }
-        if (tid == 0)
-            for (int q = nq; q < NN_Q; q++) s.state[q] = 1;
+        // ---- sample phase: strided sample of FP32 distances for every query
+        for (int e = tid; e < NN_Q * S; e += blockDim.x) {
+            const int q = e / S, t = e - q * S;
+            const int64_t r = (int64_t)t * N / S;
+            float xf[P ? P : LAGP_PMAX];
+            load_row32<P>(X32, r, p, xf);
+            samp[q * NN_SAMPLE + t] = row_d2f<P>(xf, s.nqf[q], p);
+        }
+        __syncthreads();
+        for (int q = wid; q < NN_Q; q += nw) {
+            // target ~1.5 N' survivors (+ a few sample ranks of slack)
+            int r = (int)ceil(1.5 * (double)Nprime * (double)S / (double)N) + 12;
+            if (Nprime >= N || r > S) r = S + 1;  // tau = +inf: every row
+            const float tq = warp_quantile(samp + q * NN_SAMPLE, S, r, s.whist[wid]);
+            if (lane == 0) {
+                s.rank[q] = r;
+                s.tau[q] = (double)tq;
+                s.state[q] = q < nq ? 0 : 1;
+            }
+        }
         __syncthreads();
 
         // ---- filter rounds
         for (int round = 0; round < NN_MAX_ROUNDS; round++) {
             if (tid < NN_Q && s.state[tid] == 0) {  // only queries still searching
-                int q = tid;
+                const int q = tid;
                 s.cnt[q] = 0;
-                int r = s.rank[q];
-                s.tau[q] = (r >= S) ? INFINITY : samp[q * NN_SAMPLE + r];
+                const double tau = s.tau[q];
+                // FP32 prefilter threshold. With u = 2^-24 and inputs rounded to
+                // FP32, |d2_f32 - d2_exact| <= 8u(||x||^2 + ||X_i||^2) + (p+1)u d2 + O(u^2);
+                // the margin doubles both terms, so every row with exact d2 <= tau passes.
+                const double thr = tau + 16.0 * u32 * (s.qn2[q] + Bn2) + 2.0 * (p + 1) * u32 * tau;
+                s.thrf[q] = isfinite(thr) ? __double2float_ru(thr) : INFINITY;
             }
             __syncthreads();
-            bool any = false;
-            for (int q = 0; q < NN_Q; q++) any |= (s.state[q] == 0);
-            if (!any) break;
+            unsigned act = 0;
+            for (int q = 0; q < NN_Q; q++) act |= (s.state[q] == 0 ? 1u : 0u) << q;
+            if (!act) break;
             for (int64_t r = tid; r < N; r += blockDim.x) {
-                double xr[P ? P : LAGP_PMAX];
-                load_row<P>(X, r, p, xr);
+                float xf[P ? P : LAGP_PMAX];
+                load_row32<P>(X32, r, p, xf);
 #pragma unroll
                 for (int q = 0; q < NN_Q; q++) {
-                    if (s.state[q] != 0) continue;
-                    double d2 = row_d2<P>(xr, s.qx[q], p);
-                    if (d2 <= s.tau[q]) {
+                    if (!((act >> q) & 1u)) continue;
+                    const float d2f = row_d2f<P>(xf, s.nqf[q], p);
+                    if (d2f <= s.thrf[q]) {  // candidate: the exact key is computed densely below
                         int pos = atomicAdd(&s.cnt[q], 1);
-                        if (pos < NN_CAP) {
-                            bufk[q * NN_CAP + pos] = d2_key(d2);
-                            bufi[q * NN_CAP + pos] = (int)r;
-                        }
+                        if (pos < bufcap) bufi[q * bufcap + pos] = (int)r;
                     }
                 }
             }
             __syncthreads();
-            if (tid < NN_Q && s.state[tid] == 0) {
-                int q = tid;
-                int c = s.cnt[q];
-                int r = s.rank[q];
-                if (c >= Nprime && c <= NN_CAP) {
-                    s.state[q] = 1;
+            // dense exact pass over the prefilter survivors: FP64 key, keep d2 <= tau
+            for (int q = 0; q < NN_Q; q++) {
+                if (!((act >> q) & 1u)) continue;
+                const int cf = min(s.cnt[q], bufcap);
+                if (tid == 0) s.misc[3] = 0;
+                __syncthreads();
+                int keep = 0;
+                for (int t = tid; t < cf; t += blockDim.x) {
+                    const int r = bufi[q * bufcap + t];
+                    double xr[P ? P : LAGP_PMAX];
+                    load_row<P>(X, r, p, xr);
+                    const double d2 = row_d2<P>(xr, s.qx[q], p);
+                    const bool ok = d2 <= s.tau[q];
+                    bufk[q * bufcap + t] = ok ? d2_key(d2) : ~0ull;  // ~0 = out (sorts last)
+                    keep += ok;
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) keep += __shfl_xor_sync(0xffffffffu, keep, off);
+                if (lane == 0 && keep) atomicAdd(&s.misc[3], keep);
+                __syncthreads();
+                if (tid == 0) {
+                    s.valid[q] = s.misc[3];           // exact d2 <= tau
+                    s.cnt[q] = s.cnt[q] > bufcap ? bufcap + 1 : cf;  // entries in the buffer (bufcap+1: overflow)
+                }
+                __syncthreads();
+            }
+            // re-pick the rank of the missed queries from their samples
+            for (int q = wid; q < NN_Q; q += nw) {
+                if (s.state[q] != 0) continue;  // warp-uniform
+                const int c = s.cnt[q] > bufcap ? s.cnt[q] : s.valid[q];  // overflow -> too many
+                const int r = s.rank[q];
+                int nr = r, st = 0;
+                if (c >= Nprime && c <= bufcap) {
+                    st = 1;
                 } else if (c < Nprime) {
-                    int nr = (int)ceil((double)(r + 1) * 1.5 * (double)Nprime / (double)(c > 0 ? c : 1)) + 16;
+                    nr = (int)ceil((double)r * 1.5 * (double)Nprime / (double)(c > 0 ? c : 1)) + 16;
                     if (nr <= r) nr = r + 1;
-                    if (nr >= S) nr = S;
-                    if (r >= S) s.state[q] = 2; else s.rank[q] = nr;
-                } else {  // too many survivors
-                    int nr = (int)floor((double)r * 0.7 * (double)NN_CAP / (double)c);
-                    if (r >= S) nr = (int)floor((double)(S - 1) * 0.7 * (double)NN_CAP / (double)c);
-                    if (nr >= r || nr < 0) s.state[q] = 2; else s.rank[q] = nr;
+                    if (r > S) st = 2; else if (nr > S) nr = S + 1;
+                } else {
+                    nr = (int)floor((double)(r > S ? S : r) * 0.7 * (double)bufcap / (double)c);
+                    if (nr >= r || nr < 1) st = 2;
+                }
+                float tq = 0.f;
+                if (st == 0) tq = warp_quantile(samp + q * NN_SAMPLE, S, nr, s.whist[wid]);
+                if (lane == 0) {
+                    s.state[q] = st;
+                    if (st == 0) { s.rank[q] = nr; s.tau[q] = (double)tq; }
                 }
             }
             __syncthreads();
@@ -277,9 +533,10 @@ nn_pool_kernel(const double *__restrict__ X, int64_t N, int p, const double *__r
         if (tid < NN_Q && s.state[tid] == 0) s.state[tid] = 2;
         __syncthreads();
 
-        // ---- per-query sort and output
+        // ---- per-query exact selection and output
         for (int q = 0; q < nq; q++) {
             int c;
+            int32_t *po = pool_out + (q0 + q) * (int64_t)Nprime;
             if (s.state[q] == 2) {
                 if (tid == 0) atomicAdd(fallback_count, 1);
                 nn_exact_select<P>(s, X, N, p, q, Nprime);
@@ -287,48 +544,64 @@ nn_pool_kernel(const double *__restrict__ X, int64_t N, int p, const double *__r
             } else {
                 c = s.cnt[q];
                 for (int t = tid; t < c; t += blockDim.x) {
-                    s.key[t] = bufk[q * NN_CAP + t];
-                    s.idx[t] = bufi[q * NN_CAP + t];
+                    s.key[t] = bufk[q * bufcap + t];
+                    s.idx[t] = bufi[q * bufcap + t];
                 }
             }
-            int npow = 1;
-            while (npow < c) npow <<= 1;
-            for (int t = c + tid; t < npow; t += blockDim.x) {
-                s.key[t] = ~0ull;
-                s.idx[t] = 0x7fffffff;
-            }
             __syncthreads();
-            bitonic_sort(s, npow);
-            int32_t *po = pool_out + (q0 + q) * (int64_t)Nprime;
-            for (int t = tid; t < Nprime; t += blockDim.x) {
-                po[t] = s.idx[t];
-                if (d2_out) d2_out[(q0 + q) * (int64_t)Nprime + t] = __longlong_as_double((long long)s.key[t]);
+            if (sorted) {
+                int npow = 1;
+                while (npow < c) npow <<= 1;
+                for (int t = c + tid; t < npow; t += blockDim.x) {
+                    s.key[t] = ~0ull;
+                    s.idx[t] = 0x7fffffff;
+                }
+                __syncthreads();
+                bitonic_sort(s, npow);
+                for (int t = tid; t < Nprime; t += blockDim.x) {
+                    po[t] = s.idx[t];
+                    if (d2_out) d2_out[(q0 + q) * (int64_t)Nprime + t] = __longlong_as_double((long long)s.key[t]);
+                }
+                __syncthreads();
+            } else {
+                select_pool(s, c, Nprime, n0, po);
             }
-            __syncthreads();
         }
     }
 }
 
 size_t nn_smem_bytes() { return sizeof(NNSmem); }
 
-// Host launcher. Workspace is allocated by the caller (abi.cu) via nn_ws_bytes.
-size_t nn_ws_bytes(int grid) {
-    return (size_t)grid * NN_Q * (NN_SAMPLE * sizeof(double) + NN_CAP * (sizeof(uint64_t) + sizeof(int32_t))) + 256;
+// per-query global survivor buffer: enough for ~1.5 N' plus sampling noise
+static int nn_bufcap(int Nprime) {
+    int c = 3 * Nprime;
+    if (c < 2048) c = 2048;
+    if (c > NN_CAP) c = NN_CAP;
+    return c;
+}
+
+// Workspace layout: [maxn2 bits (256 B)] [X32: N*p floats] [sample] [survivor keys] [survivor idx]
+size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime) {
+    const size_t bc = (size_t)nn_bufcap(Nprime);
+    return 256 + (((size_t)N * p * sizeof(float) + 255) & ~(size_t)255) +
+           (size_t)grid * NN_Q * (NN_SAMPLE * sizeof(float) + bc * (sizeof(uint64_t) + sizeof(int32_t))) + 256;
 }
 
 template <int P>
-static cudaError_t launch_nn_t(const double *X, int64_t N, int p, const double *XX, int64_t M, int Nprime,
-                               int32_t *pool, double *d2, void *ws, int grid, int *fb, cudaStream_t st) {
+static cudaError_t launch_nn_t(const double *X, const float *X32, const unsigned long long *mx, int64_t N, int p,
+                               const double *XX, int64_t M, int Nprime, int n0, int sorted, int32_t *pool, double *d2,
+                               char *w, int grid, int *fb, cudaStream_t st) {
     size_t smem = sizeof(NNSmem);
     cudaError_t e = cudaFuncSetAttribute(nn_pool_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    char *w = (char *)ws;
-    double *samp = (double *)w;
-    w += (size_t)grid * NN_Q * NN_SAMPLE * sizeof(double);
+    const int bc = nn_bufcap(Nprime);
+    float *samp = (float *)w;
+    w += (size_t)grid * NN_Q * NN_SAMPLE * sizeof(float);
     uint64_t *bk = (uint64_t *)w;
-    w += (size_t)grid * NN_Q * NN_CAP * sizeof(uint64_t);
+    w += (size_t)grid * NN_Q * bc * sizeof(uint64_t);
     int32_t *bi = (int32_t *)w;
-    nn_pool_kernel<P><<<grid, NN_THREADS, smem, st>>>(X, N, p, XX, M, Nprime, pool, d2, samp, bk, bi, fb);
+    nn_pool_kernel<P><<<grid, NN_THREADS, smem, st>>>(X, X32, mx, N, p, XX, M, Nprime, n0, bc, sorted, pool, d2, samp,
+                                                      bk, bi, fb);
     return cudaGetLastError();
 }
 
@@ -338,15 +611,33 @@ int nn_grid(int64_t M, int num_sms) {
     return (int)(groups < g ? (groups > 0 ? groups : 1) : g);
 }
 
-cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64_t M, int Nprime, int32_t *pool,
-                      double *d2, void *ws, int grid, int *fb, cudaStream_t st) {
+// Two launches: the FP32 copy / max row norm (prep), then the pool kernel.
+// With prepared = true the prep results already in `ws` are reused (chunked calls).
+cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64_t M, int Nprime, int n0, bool sorted,
+                      int32_t *pool, double *d2, void *ws, int grid, int *fb, cudaStream_t st, bool prepared,
+                      int *launches) {
+    char *w = (char *)ws;
+    unsigned long long *mx = (unsigned long long *)w;
+    float *X32 = (float *)(w + 256);
+    char *rest = w + 256 + (((size_t)N * p * sizeof(float) + 255) & ~(size_t)255);
+    if (!prepared) {
+        cudaError_t e = cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st);
+        if (e != cudaSuccess) return e;
+        int blocks = (int)((N + 255) / 256);
+        if (blocks > 4096) blocks = 4096;
+        nn_prep_kernel<<<blocks, 256, 0, st>>>(X, N, p, X32, mx);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        if (launches) (*launches)++;
+    }
+    if (launches) (*launches)++;
     switch (p) {
-        case 1: return launch_nn_t<1>(X, N, p, XX, M, Nprime, pool, d2, ws, grid, fb, st);
-        case 2: return launch_nn_t<2>(X, N, p, XX, M, Nprime, pool, d2, ws, grid, fb, st);
-        case 3: return launch_nn_t<3>(X, N, p, XX, M, Nprime, pool, d2, ws, grid, fb, st);
-        case 4: return launch_nn_t<4>(X, N, p, XX, M, Nprime, pool, d2, ws, grid, fb, st);
-        case 8: return launch_nn_t<8>(X, N, p, XX, M, Nprime, pool, d2, ws, grid, fb, st);
-        default: return launch_nn_t<0>(X, N, p, XX, M, Nprime, pool, d2, ws, grid, fb, st);
+        case 1: return launch_nn_t<1>(X, X32, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 2: return launch_nn_t<2>(X, X32, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 3: return launch_nn_t<3>(X, X32, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 4: return launch_nn_t<4>(X, X32, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 8: return launch_nn_t<8>(X, X32, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        default: return launch_nn_t<0>(X, X32, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
     }
 }
 

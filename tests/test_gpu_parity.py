@@ -150,7 +150,7 @@ def run_both(torch, dev, lagp, cfg, form="explicit", threads=0):
         ("C1", 5, 60, dict(n0=5, n=60, Nprime=60)),  # n = N' = N: full GP
     ],
 )
-@pytest.mark.parametrize("form", ["explicit", "explicit_dfma"])
+@pytest.mark.parametrize("form", ["explicit", "explicit_dfma", "incremental"])
 def test_alc_batch_vs_oracle(torch_dev, lagp, name, M, N, over, form):
     torch, dev = torch_dev
     cfg = make_config(name, M=M, N=N, **over)
@@ -160,7 +160,11 @@ def test_alc_batch_vs_oracle(torch_dev, lagp, name, M, N, over, form):
     print(name, form, rep)
 
 
-def test_full_gp_special_case(torch_dev, lagp):
+FORMS = ["explicit", "explicit_dfma", "incremental"]
+
+
+@pytest.mark.parametrize("form", FORMS)
+def test_full_gp_special_case(torch_dev, lagp, form):
     """n = N' = N: the local design is all of X; prediction equals Eq (1)-(2)."""
     torch, dev = torch_dev
     rng = np.random.default_rng(5)
@@ -168,7 +172,7 @@ def test_full_gp_special_case(torch_dev, lagp):
     Z = np.sin(3 * X[:, 0]) + X[:, 1]
     XX = rng.random((6, 2))
     d, g = 0.1, 1e-4
-    r = lagp.alc_batch(T(torch, dev, X), T(torch, dev, Z), T(torch, dev, XX), d, g, 3, 40, 40)
+    r = lagp.alc_batch(T(torch, dev, X), T(torch, dev, Z), T(torch, dev, XX), d, g, 3, 40, 40, form=form)
     K = np.exp(-((X[:, None] - X[None]) ** 2).sum(-1) / d) + g * np.eye(40)
     for i in range(6):
         assert sorted(r["idx"][i].cpu().tolist()) == list(range(40))
@@ -179,42 +183,57 @@ def test_full_gp_special_case(torch_dev, lagp):
         assert abs(r["s2"][i].item() - s2) <= 1e-7 * s2
 
 
-def test_exhausted_and_sentinel(torch_dev, lagp):
+@pytest.mark.parametrize("form", FORMS)
+def test_exhausted_and_sentinel(torch_dev, lagp, form):
     torch, dev = torch_dev
     X = np.array([[0.5, 0.5]] * 3 + [[0.9, 0.9]])
     Z = np.array([1.0, 1.0, 1.0, 2.0])
     XX = np.array([[0.4, 0.5]])
     cfg = dict(X=X, Z=Z, XX=XX, d=0.1, g=0.0, n0=1, n=3, Nprime=3)
-    g, o = run_both(torch, dev, lagp, cfg)
+    g, o = run_both(torch, dev, lagp, cfg, form=form)
     assert g["idx"].tolist() == o["idx"].tolist() == [[0, -1, -1]]
     assert g["flags"][0] & lagp.FLAG_EXHAUSTED and g["flags"][0] & lagp.FLAG_SENTINEL
     assert abs(g["mean"][0] - o["mean"][0]) < 1e-14 and abs(g["s2"][0] - o["s2"][0]) < 1e-14
     assert np.isnan(g["var"][0])
 
 
-def test_exact_tie_lowest_index(torch_dev, lagp):
+@pytest.mark.parametrize("form", FORMS)
+def test_exact_tie_lowest_index(torch_dev, lagp, form):
     torch, dev = torch_dev
     X = np.array([[0.0], [0.1], [-0.1], [0.2], [-0.2]])
     Z = X[:, 0].copy()
     cfg = dict(X=X, Z=Z, XX=np.array([[0.0]]), d=0.05, g=1e-4, n0=1, n=3, Nprime=5)
-    g, o = run_both(torch, dev, lagp, cfg)
+    g, o = run_both(torch, dev, lagp, cfg, form=form)
     assert g["idx"][0, :2].tolist() == [0, 1]
     assert g["flags"][0] & lagp.FLAG_NEAR_TIE
     assert g["gaps"][0, 0] == 0.0
 
 
-def test_determinism_and_chunk_composition(torch_dev, lagp):
+@pytest.mark.parametrize("form", FORMS)
+def test_determinism_and_chunk_composition(torch_dev, lagp, form):
     torch, dev = torch_dev
     cfg = make_config("C2", M=300, N=20000)
     X, Z, XX = (T(torch, dev, cfg[k]) for k in ("X", "Z", "XX"))
     args = (cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"])
-    a = lagp.alc_batch(X, Z, XX, *args)
-    b = lagp.alc_batch(X, Z, XX, *args)
-    c1 = lagp.alc_batch(X, Z, XX[:113], *args)
-    c2 = lagp.alc_batch(X, Z, XX[113:], *args)
+    a = lagp.alc_batch(X, Z, XX, *args, form=form)
+    b = lagp.alc_batch(X, Z, XX, *args, form=form)
+    c1 = lagp.alc_batch(X, Z, XX[:113], *args, form=form)
+    c2 = lagp.alc_batch(X, Z, XX[113:], *args, form=form)
     for k in ("idx", "mean", "s2", "var", "flags"):
         assert torch.equal(a[k], b[k]), k
         assert torch.equal(a[k], torch.cat([c1[k], c2[k]])), k
+
+
+def test_forms_agree(torch_dev, lagp):
+    """Explicit (DMMA), explicit (DFMA) and incremental forms select the same
+    designs on the C1 locations (all three within the parity rules)."""
+    torch, dev = torch_dev
+    cfg = make_config("C1")
+    X, Z, XX = (T(torch, dev, cfg[k]) for k in ("X", "Z", "XX"))
+    args = (cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"])
+    res = {f: lagp.alc_batch(X, Z, XX, *args, form=f) for f in FORMS}
+    same = [(res[f]["idx"] == res["incremental"]["idx"]).all(1).float().mean().item() for f in FORMS]
+    assert min(same) >= 0.97, same
 
 
 def test_host_entry_point_matches_device(torch_dev, lagp):
@@ -227,18 +246,19 @@ def test_host_entry_point_matches_device(torch_dev, lagp):
     assert np.array_equal(h["mean"], d["mean"].cpu().numpy())
 
 
-def test_full_size_C2_sampled(torch_dev, lagp):
+@pytest.mark.parametrize("form", FORMS)
+def test_full_size_C2_sampled(torch_dev, lagp, form):
     """The bench configuration (C2: N=1e5, M=1e4) in the bench's launch
     configuration, checked on a seeded sample of 48 locations."""
     torch, dev = torch_dev
     cfg = make_config("C2")
     r = lagp.alc_batch(T(torch, dev, cfg["X"]), T(torch, dev, cfg["Z"]), T(torch, dev, cfg["XX"]), cfg["d"], cfg["g"],
-                       cfg["n0"], cfg["n"], cfg["Nprime"], gaps=True)
+                       cfg["n0"], cfg["n"], cfg["Nprime"], gaps=True, form=form)
     sel = np.sort(np.random.default_rng(7).choice(cfg["XX"].shape[0], 48, replace=False))
     g = {k: v.cpu().numpy()[sel] for k, v in r.items() if hasattr(v, "cpu")}
     o = oracle.alc_batch(cfg["X"], cfg["Z"], cfg["XX"][sel], cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"])
     compare(g, o, cfg["n0"], float(np.std(cfg["Z"])), tau_for(8))
-    # properties at every location: flags clean, s2 > 0, indices distinct and in range
+    # properties at every location: indices distinct and in range, s2 > 0
     idx = r["idx"].cpu().numpy()
     assert (idx >= 0).all() and (idx < cfg["X"].shape[0]).all()
     srt = np.sort(idx, axis=1)
