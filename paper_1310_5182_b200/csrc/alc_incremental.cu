@@ -13,14 +13,18 @@
 //   e_c = K(x_c, x*) - w_{c*}^T w_c          (= Cov_j(f(x_c), f(x*)))
 //   w_c[j] = e_c / rho,  s_c -= (e_c/rho)^2,  cov_c -= (cov_{c*}/rho) (e_c/rho).
 // The initial NN design X_{n0} enters by the same append, forced in NN order.
-// The prediction (a5) is the fresh Cholesky of K_n, as in the explicit form.
+//
+// a5 from the same factor (L_n is a Cholesky factor of K_n = C(X_n) + eta I,
+// built column by column): with z = L^{-1} h and y~ = L^{-1} Y (one new entry
+// per append, y~_j = (y* - w_{c*}^T y~)/rho),
+//   mean = z^T y~,  psi = ||y~||^2,  s2 = psi (1 + eta - ||z||^2) / n   (Eq 1-2).
 //
 // B200 mapping: one CTA of 1024 threads per location (persistent grid, one CTA
 // per SM), one pool candidate per thread when N' <= 1024. The candidate's state
-// (x_c, kappa_c, s_c, cov_c and the first R entries of w_c) lives in registers,
-// entries [R, R+S) in shared memory (entry-major, conflict-free), the rest in an
-// HBM slab — so for the C1–C4 shapes the whole local state is on-chip and each
-// step is one pass over the candidates: one exp, one j-term dot, one argmax.
+// (x_c, s_c, cov_c and the first R entries of w_c) lives in registers, entries
+// [R, R+S) in shared memory (entry-major, conflict-free), the rest in an HBM
+// slab — so for the C1–C4 shapes almost all of the local state is on-chip and
+// each step is one pass over the candidates: one exp, one j-term dot, one argmax.
 #include <cuda_runtime.h>
 
 #include "block_ops.cuh"
@@ -40,31 +44,29 @@ constexpr int INC_THREADS = 1024;
 struct IncShared {
     double xstar[LAGP_PMAX];
     double xq[LAGP_PMAX];
-    double rho, znew, kapstar;
-    int cstar;
+    double rho, znew, ystar;
     uint32_t fl;
 };
 
-// Generic part: w entries [R, R+S) in smem (wsm[a - R][c]), [R+S, n) in the HBM slab.
+// smem (doubles): wsm S*Npad | wstar n4 | ytil n4 | zv n4 | red 160
+__host__ __device__ inline int inc_n4(int n) { return (n + 3) & ~3; }
+
 template <int R, int P, int CPT>
 __global__ void __launch_bounds__(INC_THREADS, 1)
-alc_incremental_kernel(AlcArgs A, int S, int wsz) {
+alc_incremental_kernel(AlcArgs A, int S) {
     extern __shared__ __align__(16) double sm[];
     const int n = A.n, Np = A.Nprime, Npad = A.Npad, n0 = A.n0;
     const int p = P ? P : A.p;
-    // smem: wsm S*Npad | wstar n | Xj n*p (r4) | yv n | hv n | red 160 ; predict scratch aliases wsm
     double *wsm = sm;
-    double *wstar = wsm + wsz;  // wsz >= S*Npad and >= the predict scratch (aliases wsm)
-    double *Xj = wstar + ((n + 3) & ~3);
-    double *yv = Xj + ((n * p + 3) & ~3);
-    double *hv = yv + ((n + 3) & ~3);
-    double *red = hv + ((n + 3) & ~3);
+    double *wstar = wsm + (size_t)S * Npad;
+    double *ytil = wstar + inc_n4(n);
+    double *zv = ytil + inc_n4(n);
+    double *red = zv + inc_n4(n);
     __shared__ IncShared sh;
 
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     double *gw = A.cache + (size_t)blockIdx.x * A.cache_stride;  // entries >= R+S: gw[(a-R-S)*Npad + c]
-    const double *coordsg = A.coords + (size_t)blockIdx.x * p * Npad;
-    double *coordsw = A.coords + (size_t)blockIdx.x * p * Npad;
+    double *coords = A.coords + (size_t)blockIdx.x * p * Npad;   // generic-p path only
     const double rth = A.rtheta, eta = A.eta;
     const int G = n - n0;
     const int RS = R + S;
@@ -103,7 +105,7 @@ alc_incremental_kernel(AlcArgs A, int S, int wsz) {
             } else if (valid[q]) {
                 for (int k = 0; k < p; k++) {
                     const double v = A.X[(int64_t)gidx[q] * p + k];
-                    coordsw[k * Npad + c] = v;
+                    coords[k * Npad + c] = v;
                     double diff = __dsub_rn(v, sh.xq[k]);
                     d2 = __fma_rn(diff, diff, d2);
                 }
@@ -115,8 +117,7 @@ alc_incremental_kernel(AlcArgs A, int S, int wsz) {
         }
         __syncthreads();
 
-        int j = 0;           // current design size
-        bool done = false;   // exhausted
+        int j = 0;  // current design size
         for (; j < n; j++) {
             int cstar;
             if (j < n0) {
@@ -138,12 +139,11 @@ alc_incremental_kernel(AlcArgs A, int S, int wsz) {
                         }
                     }
                 }
-                if (sentinel) atomicOr(&sh.fl, (uint32_t)LAGP_FLAG_SENTINEL);
-                if (nonfinite) atomicOr(&sh.fl, (uint32_t)LAGP_FLAG_NONFINITE);
+                if (__any_sync(0xffffffffu, sentinel) && lane == 0) atomicOr(&sh.fl, (uint32_t)LAGP_FLAG_SENTINEL);
+                if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(&sh.fl, (uint32_t)LAGP_FLAG_NONFINITE);
                 best = block_top2(best, red);
                 if (best.pos < 0) {
                     if (tid == 0) sh.fl |= LAGP_FLAG_EXHAUSTED;
-                    done = true;
                     break;
                 }
                 cstar = best.pos;
@@ -154,7 +154,7 @@ alc_incremental_kernel(AlcArgs A, int S, int wsz) {
                     idx[j] = best.i1;
                 }
             }
-            // ---- a4 on the factor: publish w_{c*}, x*, rho, z_new
+            // ---- a4 on the factor: publish w_{c*}, x*, rho, z_new, y*
             const int owner = cstar % INC_THREADS, oq = cstar / INC_THREADS;
             if (tid == owner) {
 #pragma unroll
@@ -170,23 +170,44 @@ alc_incremental_kernel(AlcArgs A, int S, int wsz) {
                         const double rho = sqrt(s[q]);
                         sh.rho = rho;
                         sh.znew = cov[q] / rho;
+                        sh.ystar = A.Z[gidx[q]];
                         chosen[q] = true;
                         if (!(s[q] > 0.0)) atomicOr(&sh.fl, (uint32_t)LAGP_FLAG_NONFINITE);
                     }
                 }
             }
-            if (!P && tid < p) sh.xstar[tid] = coordsg[tid * Npad + cstar];
+            if (!P && tid < p) sh.xstar[tid] = coords[tid * Npad + cstar];
             for (int a = R + tid; a < j; a += blockDim.x)
                 wstar[a] = (a < RS) ? wsm[(size_t)(a - R) * Npad + cstar] : gw[(size_t)(a - RS) * Npad + cstar];
             __syncthreads();
-            if (tid < p) Xj[j * p + tid] = sh.xstar[tid];
-            if (tid == 0) hv[j] = corr_from_d2(sqdist_fma(sh.xstar, sh.xq, p), rth);  // kappa_* (same bits as init)
             const double rrho = 1.0 / sh.rho, znew = sh.znew;
+            if (wid == 0) {  // a5 state: y~_j = (y* - w*^T y~) / rho, z_j = z_new
+                double acc = 0.0;
+                for (int a = lane; a < j; a += 32) acc = fma(wstar[a], ytil[a], acc);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                if (lane == 0) {
+                    ytil[j] = (sh.ystar - acc) * rrho;
+                    zv[j] = znew;
+                }
+            }
             // ---- every candidate: new entry of w_c, downdates of s_c and cov_c
 #pragma unroll
             for (int q = 0; q < CPT; q++) {
                 const int c = tid + q * INC_THREADS;
                 if (!valid[q]) continue;
+                // issue the HBM-slab loads first (independent, latency overlapped)
+                double acc2 = 0.0, acc3 = 0.0;
+                for (int a = RS; a < j; a += 4) {
+                    const double g0 = gw[(size_t)(a - RS) * Npad + c];
+                    const double g1 = a + 1 < j ? gw[(size_t)(a + 1 - RS) * Npad + c] : 0.0;
+                    const double g2 = a + 2 < j ? gw[(size_t)(a + 2 - RS) * Npad + c] : 0.0;
+                    const double g3 = a + 3 < j ? gw[(size_t)(a + 3 - RS) * Npad + c] : 0.0;
+                    acc2 = fma(wstar[a], g0, acc2);
+                    acc3 = fma(a + 1 < j ? wstar[a + 1] : 0.0, g1, acc3);
+                    acc2 = fma(a + 2 < j ? wstar[a + 2] : 0.0, g2, acc2);
+                    acc3 = fma(a + 3 < j ? wstar[a + 3] : 0.0, g3, acc3);
+                }
                 double d2 = 0.0;
                 if (P) {
 #pragma unroll
@@ -196,11 +217,10 @@ alc_incremental_kernel(AlcArgs A, int S, int wsz) {
                     }
                 } else {
                     for (int k = 0; k < p; k++) {
-                        double diff = __dsub_rn(coordsg[k * Npad + c], sh.xstar[k]);
+                        double diff = __dsub_rn(coords[k * Npad + c], sh.xstar[k]);
                         d2 = __fma_rn(diff, diff, d2);
                     }
                 }
-                double e = corr_from_d2(d2, rth);
                 double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
                 for (int a = 0; a < R; a += 2) {  // R even; wstar[a >= j] = 0, wr[a >= j] = 0
@@ -209,14 +229,18 @@ alc_incremental_kernel(AlcArgs A, int S, int wsz) {
                     acc1 = fma(ws.y, wr[q][a + 1], acc1);
                 }
                 const int jr = j < RS ? j : RS;
-                for (int a = R; a < jr; a++) acc0 = fma(wstar[a], wsm[(size_t)(a - R) * Npad + c], acc0);
-                for (int a = RS; a < j; a++) acc1 = fma(wstar[a], gw[(size_t)(a - RS) * Npad + c], acc1);
-                e -= acc0 + acc1;
+                int a = R;
+                for (; a + 1 < jr; a += 2) {
+                    acc0 = fma(wstar[a], wsm[(size_t)(a - R) * Npad + c], acc0);
+                    acc1 = fma(wstar[a + 1], wsm[(size_t)(a + 1 - R) * Npad + c], acc1);
+                }
+                if (a < jr) acc0 = fma(wstar[a], wsm[(size_t)(a - R) * Npad + c], acc0);
+                const double e = corr_from_d2(d2, rth) - ((acc0 + acc1) + (acc2 + acc3));
                 const double wn = e * rrho;
                 if (j < R) {
 #pragma unroll
-                    for (int a = 0; a < R; a++)
-                        if (a == j) wr[q][a] = wn;
+                    for (int b = 0; b < R; b++)
+                        if (b == j) wr[q][b] = wn;
                 } else if (j < RS) {
                     wsm[(size_t)(j - R) * Npad + c] = wn;
                 } else {
@@ -225,26 +249,35 @@ alc_incremental_kernel(AlcArgs A, int S, int wsz) {
                 s[q] = fma(-wn, wn, s[q]);
                 cov[q] = fma(-znew, wn, cov[q]);
             }
-            __syncthreads();  // wstar / sh reused next step
+            __syncthreads();  // wstar / sh / ytil reused next step
         }
-        (void)done;
 
-        // ---- a5: predict on D_j (fresh Cholesky; scratch aliases the smem w entries)
-        for (int t = tid; t < j; t += blockDim.x) yv[t] = A.Z[idx[t]];
+        // ---- a5: mean = z^T y~, psi = ||y~||^2, s2 = psi (1 + eta - ||z||^2) / j
         __syncthreads();
-        double mu, sc, vr;
-        const int ldp = (j + 1) | 1;
-        double *Ksc = wsm;  // needs j*ldp + 2*ldp doubles (checked on the host)
-        bool ok = block_predict(Ksc, ldp, j, p, Xj, yv, hv, rth, eta, Ksc + (size_t)j * ldp,
-                                Ksc + (size_t)j * ldp + ldp, red, &mu, &sc, &vr);
-        if (tid == 0) {
-            uint32_t f = sh.fl;
-            if (!ok || !isfinite(mu) || !isfinite(sc)) f |= LAGP_FLAG_NONFINITE;
-            A.mean[xi] = mu;
-            A.s2[xi] = sc;
-            if (A.var) A.var[xi] = vr;
-            if (A.flags) A.flags[xi] = f;
-            if (f & (LAGP_FLAG_EXHAUSTED | LAGP_FLAG_NONFINITE)) atomicAdd(A.n_partial, 1);
+        if (wid == 0) {
+            double mu = 0.0, psi = 0.0, zz = 0.0;
+            for (int a = lane; a < j; a += 32) {
+                mu = fma(zv[a], ytil[a], mu);
+                psi = fma(ytil[a], ytil[a], psi);
+                zz = fma(zv[a], zv[a], zz);
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                mu += __shfl_xor_sync(0xffffffffu, mu, off);
+                psi += __shfl_xor_sync(0xffffffffu, psi, off);
+                zz += __shfl_xor_sync(0xffffffffu, zz, off);
+            }
+            if (lane == 0) {
+                const double sc = psi * (1.0 + eta - zz) / (double)j;
+                const double vr = j > 2 ? sc * (double)j / (double)(j - 2) : __longlong_as_double(0x7ff8000000000000LL);
+                uint32_t f = sh.fl;
+                if (!isfinite(mu) || !isfinite(sc)) f |= LAGP_FLAG_NONFINITE;
+                A.mean[xi] = mu;
+                A.s2[xi] = sc;
+                if (A.var) A.var[xi] = vr;
+                if (A.flags) A.flags[xi] = f;
+                if (f & (LAGP_FLAG_EXHAUSTED | LAGP_FLAG_NONFINITE)) atomicAdd(A.n_partial, 1);
+            }
         }
         __syncthreads();
     }
@@ -252,11 +285,11 @@ alc_incremental_kernel(AlcArgs A, int S, int wsz) {
 
 // ---------------------------------------------------------------- host side
 template <int R, int P, int CPT>
-static cudaError_t inc_launch_t(const AlcArgs &a, int S, int wsz, int grid, size_t smem, cudaStream_t st) {
+static cudaError_t inc_launch_t(const AlcArgs &a, int S, int grid, size_t smem, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(alc_incremental_kernel<R, P, CPT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    alc_incremental_kernel<R, P, CPT><<<grid, INC_THREADS, smem, st>>>(a, S, wsz);
+    alc_incremental_kernel<R, P, CPT><<<grid, INC_THREADS, smem, st>>>(a, S);
     return cudaGetLastError();
 }
 
@@ -271,22 +304,20 @@ static int inc_R(int p, int cpt) {
 IncPlan inc_plan(int n, int p, int Nprime, int Npad, size_t smem_optin) {
     IncPlan pl{};
     pl.cpt = (Nprime + INC_THREADS - 1) / INC_THREADS;
-    if (pl.cpt > 8) { pl.ok = false; return pl; }
+    if (pl.cpt > 8) {
+        pl.ok = false;
+        return pl;
+    }
     pl.R = inc_R(p, pl.cpt);
-    const size_t fixed = ((size_t)((n + 3) & ~3) * 3 + ((n * p + 3) & ~3) + 160) * sizeof(double);
-    const int ldp = (n + 1) | 1;
-    const size_t predict_need = ((size_t)n * ldp + 2 * ldp) * sizeof(double);
+    const size_t fixed = ((size_t)inc_n4(n) * 3 + 160) * sizeof(double);
     size_t avail = smem_optin > fixed + 1024 ? smem_optin - fixed - 1024 : 0;
     int S = (int)(avail / ((size_t)Npad * sizeof(double)));
     const int need = n - pl.R > 0 ? n - pl.R : 0;
     if (S > need) S = need;
     if (S < 0) S = 0;
-    size_t wbytes = (size_t)S * Npad * sizeof(double);
-    if (wbytes < predict_need) wbytes = predict_need;
     pl.S = S;
-    wbytes = (wbytes + 31) & ~(size_t)31;
-    pl.wsz = (int)(wbytes / sizeof(double));
-    pl.smem = wbytes + fixed;
+    pl.wsz = S * Npad;
+    pl.smem = (size_t)S * Npad * sizeof(double) + fixed;
     pl.ok = pl.smem <= smem_optin;
     pl.global_entries = n - pl.R - S > 0 ? n - pl.R - S : 0;
     return pl;
@@ -294,14 +325,14 @@ IncPlan inc_plan(int n, int p, int Nprime, int Npad, size_t smem_optin) {
 
 cudaError_t launch_alc_incremental(const AlcArgs &a, const IncPlan &pl, int grid, cudaStream_t st) {
     const int p = a.p;
-#define INC_DISPATCH_P(R_, CPT_)                                                                  \
-    switch (p) {                                                                                  \
-        case 1: return inc_launch_t<R_, 1, CPT_>(a, pl.S, pl.wsz, grid, pl.smem, st);                    \
-        case 2: return inc_launch_t<R_, 2, CPT_>(a, pl.S, pl.wsz, grid, pl.smem, st);                    \
-        case 3: return inc_launch_t<R_, 3, CPT_>(a, pl.S, pl.wsz, grid, pl.smem, st);                    \
-        case 4: return inc_launch_t<R_, 4, CPT_>(a, pl.S, pl.wsz, grid, pl.smem, st);                    \
-        case 8: return inc_launch_t<R_, 8, CPT_>(a, pl.S, pl.wsz, grid, pl.smem, st);                    \
-        default: return inc_launch_t<0, 0, CPT_>(a, pl.S, pl.wsz, grid, pl.smem, st);                    \
+#define INC_DISPATCH_P(R_, CPT_)                                                     \
+    switch (p) {                                                                     \
+        case 1: return inc_launch_t<R_, 1, CPT_>(a, pl.S, grid, pl.smem, st);        \
+        case 2: return inc_launch_t<R_, 2, CPT_>(a, pl.S, grid, pl.smem, st);        \
+        case 3: return inc_launch_t<R_, 3, CPT_>(a, pl.S, grid, pl.smem, st);        \
+        case 4: return inc_launch_t<R_, 4, CPT_>(a, pl.S, grid, pl.smem, st);        \
+        case 8: return inc_launch_t<R_, 8, CPT_>(a, pl.S, grid, pl.smem, st);        \
+        default: return inc_launch_t<0, 0, CPT_>(a, pl.S, grid, pl.smem, st);        \
     }
     if (pl.cpt == 1) {
         if (p == 8 && pl.R == INC_R8) { INC_DISPATCH_P(INC_R8, 1) }

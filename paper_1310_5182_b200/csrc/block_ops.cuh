@@ -7,7 +7,7 @@
 
 namespace lagp {
 
-// Sum over the CTA (blockDim.x multiple of 32, <= 1024). `scratch` >= 32 doubles.
+// Sum over the CTA (blockDim.x multiple of 32, <= 1024). `scratch` >= 33 doubles.
 // Deterministic: fixed shuffle tree, then warp partials summed in warp order.
 __device__ __forceinline__ double block_sum(double v, double *scratch) {
 #pragma unroll
@@ -16,15 +16,21 @@ __device__ __forceinline__ double block_sum(double v, double *scratch) {
     __syncthreads();
     if (lane == 0) scratch[wid] = v;
     __syncthreads();
-    double s = 0.0;
-    const int nw = blockDim.x >> 5;
-    for (int w = 0; w < nw; w++) s += scratch[w];
+    if (wid == 0) {  // second level: warp 0 over the warp partials (fixed tree)
+        const int nw = blockDim.x >> 5;
+        double s = lane < nw ? scratch[lane] : 0.0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) scratch[32] = s;
+    }
+    __syncthreads();
+    const double s = scratch[32];
     __syncthreads();
     return s;
 }
 
 // Block-wide merge of per-thread Top2 records; every thread receives the result.
-__device__ __forceinline__ Top2 block_top2(Top2 t, double *scratch /* >= 4*32 doubles */) {
+__device__ __forceinline__ Top2 block_top2(Top2 t, double *scratch /* >= 132 doubles */) {
     warp_merge_top2(t);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     __syncthreads();
@@ -35,12 +41,30 @@ __device__ __forceinline__ Top2 block_top2(Top2 t, double *scratch /* >= 4*32 do
         scratch[4 * wid + 3] = int_bits_to_double(t.pos);
     }
     __syncthreads();
+    if (wid == 0) {  // second level: warp 0 merges the warp results (fixed tree)
+        const int nw = blockDim.x >> 5;
+        Top2 r;
+        r.init();
+        if (lane < nw) {
+            r.d1 = scratch[4 * lane + 0];
+            r.d2 = scratch[4 * lane + 1];
+            r.i1 = double_bits_to_int(scratch[4 * lane + 2]);
+            r.pos = double_bits_to_int(scratch[4 * lane + 3]);
+        }
+        warp_merge_top2(r);
+        if (lane == 0) {
+            scratch[128] = r.d1;
+            scratch[129] = r.d2;
+            scratch[130] = int_bits_to_double(r.i1);
+            scratch[131] = int_bits_to_double(r.pos);
+        }
+    }
+    __syncthreads();
     Top2 r;
-    r.init();
-    const int nw = blockDim.x >> 5;
-    for (int w = 0; w < nw; w++)
-        r.merge(scratch[4 * w + 0], double_bits_to_int(scratch[4 * w + 2]),
-                double_bits_to_int(scratch[4 * w + 3]), scratch[4 * w + 1]);
+    r.d1 = scratch[128];
+    r.d2 = scratch[129];
+    r.i1 = double_bits_to_int(scratch[130]);
+    r.pos = double_bits_to_int(scratch[131]);
     __syncthreads();
     return r;
 }
