@@ -48,7 +48,7 @@ struct IncShared {
     uint32_t fl;
 };
 
-// smem (doubles): wsm S*Npad | wstar n4 | ytil n4 | zv n4 | red 160
+// smem (doubles): wsm S*Npad | wstar n4 | ytil n4 | zv n4 | zc Npad | red 160
 __host__ __device__ inline int inc_n4(int n) { return (n + 3) & ~3; }
 
 template <int R, int P, int CPT>
@@ -61,7 +61,8 @@ alc_incremental_kernel(AlcArgs A, int S) {
     double *wstar = wsm + (size_t)S * Npad;
     double *ytil = wstar + inc_n4(n);
     double *zv = ytil + inc_n4(n);
-    double *red = zv + inc_n4(n);
+    double *zc = zv + inc_n4(n);  // Z of the pool candidates (y* without an HBM round trip)
+    double *red = zc + Npad;
     __shared__ IncShared sh;
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -112,6 +113,7 @@ alc_incremental_kernel(AlcArgs A, int S) {
             }
             s[q] = 1.0 + eta;
             cov[q] = valid[q] ? corr_from_d2(d2, rth) : 0.0;  // kappa_c (z is empty at j = 0)
+            if (valid[q]) zc[c] = A.Z[gidx[q]];
 #pragma unroll
             for (int a = 0; a < (R > 0 ? R : 1); a++) wr[q][a] = 0.0;
         }
@@ -124,8 +126,8 @@ alc_incremental_kernel(AlcArgs A, int S) {
                 cstar = j;  // forced NN append (a2), pool order = NN order
             } else {
                 // ---- a3: argmax of Delta_c = cov_c^2 / s_c over valid, unchosen candidates
-                Top2 best;
-                best.init();
+                double bd1 = -1.0, bd2 = 0.0;  // bd1 < 0: no candidate
+                int bi = -1, bp = -1;
                 bool sentinel = false, nonfinite = false;
 #pragma unroll
                 for (int q = 0; q < CPT; q++) {
@@ -134,15 +136,23 @@ alc_incremental_kernel(AlcArgs A, int S) {
                             sentinel = true;
                         } else {
                             const double dl = cov[q] * cov[q] / s[q];
-                            if (!isfinite(dl)) nonfinite = true;
-                            else best.push(dl, gidx[q], tid + q * INC_THREADS);
+                            if (!isfinite(dl)) {
+                                nonfinite = true;
+                            } else if (dl > bd1 || (dl == bd1 && (unsigned)gidx[q] < (unsigned)bi)) {
+                                bd2 = fmax(bd2, bd1);
+                                bd1 = dl;
+                                bi = gidx[q];
+                                bp = tid + q * INC_THREADS;
+                            } else {
+                                bd2 = fmax(bd2, dl);
+                            }
                         }
                     }
                 }
                 if (__any_sync(0xffffffffu, sentinel) && lane == 0) atomicOr(&sh.fl, (uint32_t)LAGP_FLAG_SENTINEL);
                 if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(&sh.fl, (uint32_t)LAGP_FLAG_NONFINITE);
-                best = block_top2(best, red);
-                if (best.pos < 0) {
+                const ArgTop best = block_argtop(bd1, bi, bd2, bp, red);
+                if (best.i1 < 0) {
                     if (tid == 0) sh.fl |= LAGP_FLAG_EXHAUSTED;
                     break;
                 }
@@ -170,7 +180,7 @@ alc_incremental_kernel(AlcArgs A, int S) {
                         const double rho = sqrt(s[q]);
                         sh.rho = rho;
                         sh.znew = cov[q] / rho;
-                        sh.ystar = A.Z[gidx[q]];
+                        sh.ystar = zc[cstar];
                         chosen[q] = true;
                         if (!(s[q] > 0.0)) atomicOr(&sh.fl, (uint32_t)LAGP_FLAG_NONFINITE);
                     }
@@ -309,7 +319,7 @@ IncPlan inc_plan(int n, int p, int Nprime, int Npad, size_t smem_optin) {
         return pl;
     }
     pl.R = inc_R(p, pl.cpt);
-    const size_t fixed = ((size_t)inc_n4(n) * 3 + 160) * sizeof(double);
+    const size_t fixed = ((size_t)inc_n4(n) * 3 + Npad + 160) * sizeof(double);
     size_t avail = smem_optin > fixed + 1024 ? smem_optin - fixed - 1024 : 0;
     int S = (int)(avail / ((size_t)Npad * sizeof(double)));
     const int need = n - pl.R > 0 ? n - pl.R : 0;

@@ -69,6 +69,79 @@ __device__ __forceinline__ Top2 block_top2(Top2 t, double *scratch /* >= 132 dou
     return r;
 }
 
+// Fast block argmax for non-negative scores: each thread brings its best (d1, i1)
+// and its own second best d2 (d = score >= 0; invalid = no candidate). The warp
+// and block levels use redux.sync max/min on the 64-bit pattern of the doubles
+// (non-negative doubles order like their bits) instead of shuffle trees:
+//   d1 = max score, i1 = lowest global index among exact maxima (R7),
+//   d2 = max of everything else (for the top-2 gap). Every thread gets the result;
+// i1 = INT_MAX when no thread had a candidate. `scratch` >= 100 doubles.
+struct ArgTop {
+    double d1, d2;
+    int i1;   // global index of the winner, -1 if none
+    int pos;  // caller's payload of the winner (pool position)
+};
+__device__ __forceinline__ void warp_argtop(unsigned long long &k1, unsigned &i1, unsigned long long &k2, int &pos) {
+    const unsigned full = 0xffffffffu;
+    const unsigned hi = (unsigned)(k1 >> 32), lo = (unsigned)k1;
+    const unsigned mhi = __reduce_max_sync(full, hi);
+    const unsigned mlo = __reduce_max_sync(full, hi == mhi ? lo : 0u);
+    const bool ismax = (hi == mhi && lo == mlo);
+    const unsigned mi = __reduce_min_sync(full, ismax ? i1 : 0xffffffffu);
+    const bool win = ismax && i1 == mi;
+    const unsigned wb = __ballot_sync(full, win);
+    pos = __shfl_sync(full, pos, wb ? __ffs(wb) - 1 : 0);
+    // second: the winner contributes its own second, everyone else its best
+    const unsigned long long c2 = (win && (__ffs(wb) - 1) == (int)(threadIdx.x & 31)) ? k2 : k1;
+    const unsigned shi = __reduce_max_sync(full, (unsigned)(c2 >> 32));
+    const unsigned slo = __reduce_max_sync(full, (unsigned)(c2 >> 32) == shi ? (unsigned)c2 : 0u);
+    k1 = ((unsigned long long)mhi << 32) | mlo;
+    i1 = mi;
+    k2 = ((unsigned long long)shi << 32) | slo;
+}
+__device__ __forceinline__ ArgTop block_argtop(double d1, int i1, double d2, int pos, double *scratch) {
+    // invalid entries carry key 0 and index 0xffffffff (lose every tie)
+    unsigned long long k1 = (unsigned long long)__double_as_longlong(d1 > 0.0 ? d1 : 0.0);
+    unsigned long long k2 = (unsigned long long)__double_as_longlong(d2 > 0.0 ? d2 : 0.0);
+    unsigned ii = (unsigned)i1;
+    warp_argtop(k1, ii, k2, pos);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long *sk = reinterpret_cast<unsigned long long *>(scratch);
+    __syncthreads();
+    if (lane == 0) {
+        sk[3 * wid + 0] = k1;
+        sk[3 * wid + 1] = ((unsigned long long)(unsigned)pos << 32) | ii;
+        sk[3 * wid + 2] = k2;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        unsigned long long a1 = 0, a2 = 0;
+        unsigned ai = 0xffffffffu;
+        int ap = -1;
+        if (lane < nw) {
+            a1 = sk[3 * lane + 0];
+            ai = (unsigned)sk[3 * lane + 1];
+            ap = (int)(unsigned)(sk[3 * lane + 1] >> 32);
+            a2 = sk[3 * lane + 2];
+        }
+        warp_argtop(a1, ai, a2, ap);
+        if (lane == 0) {
+            sk[96] = a1;
+            sk[97] = ((unsigned long long)(unsigned)ap << 32) | ai;
+            sk[98] = a2;
+        }
+    }
+    __syncthreads();
+    ArgTop r;
+    r.d1 = __longlong_as_double((long long)sk[96]);
+    r.i1 = (int)(unsigned)sk[97];
+    r.pos = (int)(unsigned)(sk[97] >> 32);
+    r.d2 = __longlong_as_double((long long)sk[98]);
+    __syncthreads();
+    return r;
+}
+
 // Partitioned-inverse append (a4; Eq (6)): given the
 // explicit K_j^{-1} in Kinv (leading dimension ld, symmetric), k = k_j(x_new)
 // and kdiag = K(x_new,x_new) + eta, overwrite Kinv with K_{j+1}^{-1}:
