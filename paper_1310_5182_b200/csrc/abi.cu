@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 
 #include "lagp_internal.cuh"
@@ -122,6 +123,10 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
     const int Npad = (Nprime + 3) & ~3;
     int64_t cache_stride = (int64_t)n * Npad + 1024;  // + max tile width (tile overrun)
     const bool incremental = alc_form == LAGP_ALC_INCREMENTAL;
+    // incremental form: the single-CTA kernel by default; LAGP_CLUSTER=1 selects the
+    // 2-CTA cluster variant (measured slower on C2: 27.8 vs 15.1 ms)
+    const char *cl = getenv("LAGP_CLUSTER");
+    const bool use_cluster = incremental && lagp::inc_cluster_supported(n, p, Nprime) && (cl && cl[0] == '1');
     // explicit form: DMMA (FP64 tensor) micro-kernel for n <= 64, DFMA otherwise
     const bool use_dmma = (alc_form == LAGP_ALC_EXPLICIT) && n <= 64;
     lagp::IncPlan plan{};
@@ -186,7 +191,9 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
         a.cache = cache; a.coords = coords;
         a.n_partial = counters;
         int grid = (int)(mc < alc_grid ? mc : alc_grid);
-        if (incremental)
+        if (incremental && use_cluster)
+            LAGP_CUDA(lagp::launch_alc_inc_cluster(a, sms, st));
+        else if (incremental)
             LAGP_CUDA(lagp::launch_alc_incremental(a, plan, grid, st));
         else
             LAGP_CUDA(use_dmma ? lagp::launch_alc_explicit_dmma(a, grid, st) : lagp::launch_alc_explicit(a, grid, st));

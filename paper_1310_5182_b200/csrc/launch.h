@@ -52,6 +52,9 @@ struct IncPlan {
     size_t smem;         // dynamic shared memory bytes
 };
 IncPlan inc_plan(int n, int p, int Nprime, int Npad, size_t smem_optin);
+// alc_incremental_cluster.cu: 2-CTA cluster per location (N' <= 1024, n <= 64, p in {2,3,8})
+bool inc_cluster_supported(int n, int p, int Nprime);
+cudaError_t launch_alc_inc_cluster(const AlcArgs &a, int num_sms, cudaStream_t st);
 cudaError_t launch_alc_incremental(const AlcArgs &a, const IncPlan &pl, int grid, cudaStream_t st);
 int alc_explicit_dmma_blocks_per_sm(int n, int p, int Npad);
 
