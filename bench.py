@@ -179,13 +179,29 @@ def run_reference(args):
     return 0
 
 
+def form_work(form, n0, n, Np, p):
+    """Algorithmic FP64 work per location of a local-design kernel.
+
+    explicit forms: the paper count (N'-j)(2j^2 + 4j) per step j (SURVEY §8d);
+    incremental form: per candidate update at design size j, 2j (w_*^T w_c) +
+    3p (distance) + 8 (new entry, s and cov downdates, Delta) flop, over the
+    N'-j-1 unchosen candidates, for j = 0..n-1 (the NN appends included); the
+    exp per update is not counted (as in §8d)."""
+    if form == "incremental":
+        return float(sum((Np - j - 1) * (2 * j + 3 * p + 8) for j in range(0, n)))
+    return float(alc_paper_flops_per_location(n0, n, Np))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--form", default="explicit", choices=["explicit", "incremental", "explicit_dfma"])
+    ap.add_argument("--form", default="incremental", choices=["explicit", "incremental", "explicit_dfma"],
+                    help="formulation of the headline number")
+    ap.add_argument("--compare", default="explicit",
+                    help="comma list of other forms timed the same way and reported under 'forms' ('' = none)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
@@ -210,45 +226,68 @@ def main():
     XXr_np = np.ascontiguousarray(cfg["XX"][lo:lo + M_rank])
     XX = torch.from_numpy(XXr_np).to(dev)
     n0, n, Np, d, g = cfg["n0"], cfg["n"], cfg["Nprime"], cfg["d"], cfg["g"]
+    p = cfg["X"].shape[1]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+    M_all = M_rank * world
+    nominal, meas = fp64_peak_tflops()
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        lagp.alc_batch(X, Z, XX, d, g, n0, n, Np, form=args.form)
-    torch.cuda.synchronize()
+    def time_form(form, clocks=None):
+        for _ in range(args.warmup):
+            lagp.alc_batch(X, Z, XX, d, g, n0, n, Np, form=form)
+        torch.cuda.synchronize()
+        if clocks:
+            clocks.start()
+        total = alc = nn = 0.0
+        launches = 0
+        res = None
+        for _ in range(args.steps):
+            flush.fill_(1.0)  # L2 flush between timed steps (untimed)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res = lagp.alc_batch(X, Z, XX, d, g, n0, n, Np, form=form, timing=True)
+            e1.record(stream)
+            barrier()
+            total += e0.elapsed_time(e1)
+            alc += res["timing"]["alc_ms"]
+            nn += res["timing"]["nn_ms"]
+            launches += res["timing"]["launches"]
+        clk = clocks.stop() if clocks else None
+        t = torch.tensor([total, alc, nn], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t[0]) / args.steps
+        alc_launch_ms = float(t[1]) / args.steps  # one local-design launch per step (M = 10,000)
+        achieved = M_rank * form_work(form, n0, n, Np, p) / (alc_launch_ms / 1000.0) / 1e12
+        roof = {"bound": "alu", "kernel": {"incremental": "alc_incremental_kernel",
+                                           "explicit": "alc_explicit_dmma_kernel",
+                                           "explicit_dfma": "alc_explicit_kernel"}[form],
+                "achieved": achieved, "peak": nominal, "unit": "TFLOP/s", "frac": achieved / nominal,
+                "traffic": None,
+                "work": ("incremental: (N'-j-1)(2j+3p+8) flop per location-step j=0..n-1, FP64, exp not counted"
+                         if form == "incremental" else
+                         "paper count (N'-j)(2j^2+4j) flop per location-step (SURVEY §8d), FP64"),
+                "peak_basis": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz",
+                "peak_measured_dfma": meas,
+                "kernel_ms_per_launch": alc_launch_ms}
+        return dict(ms_step=ms_step, value=M_all / (ms_step / 1000.0), alc_ms=alc_launch_ms,
+                    nn_ms=float(t[2]) / args.steps, launches=launches, res=res, clk=clk, roofline=roof)
 
-    stream = torch.cuda.current_stream(dev)
-    clocks = ClockSampler(local)
-    clocks.start()
-    total_ms = 0.0
-    alc_ms = nn_ms = 0.0
-    launches = 0
-    res = None
-    for _ in range(args.steps):
-        flush.fill_(1.0)  # L2 flush between timed steps (untimed)
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        res = lagp.alc_batch(X, Z, XX, d, g, n0, n, Np, form=args.form, timing=True)
-        e1.record(stream)
-        barrier()
-        total_ms += e0.elapsed_time(e1)
-        alc_ms += res["timing"]["alc_ms"]
-        nn_ms += res["timing"]["nn_ms"]
-        launches += res["timing"]["launches"]
-    clk = clocks.stop()
-    t = torch.tensor([total_ms, alc_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, alc_max = float(t[0]), float(t[1])
-    ms_step = total_ms / args.steps
-    M_all = M_rank * world
-    value = M_all / (ms_step / 1000.0)
+    head = time_form(args.form, ClockSampler(local))
+    others = {}
+    for f in [f for f in args.compare.split(",") if f and f != args.form]:
+        o = time_form(f)
+        others[f] = {"ms_per_step": o["ms_step"], "value": o["value"], "unit": UNIT,
+                     "phase_ms_per_step": {"nn": o["nn_ms"], "local_design": o["alc_ms"]},
+                     "roofline": o["roofline"]}
+    ms_step, value, res = head["ms_step"], head["value"], head["res"]
     evals = alc_evals_per_location(n0, n, Np)
 
     # ---- e2e: the host-buffer public entry point, copies inside the timed region
@@ -281,18 +320,15 @@ def main():
             dist.destroy_process_group()
         return 0
 
-    # ---- roofline of the dominant kernel (the fused ALC local-design kernel)
-    nominal, meas = fp64_peak_tflops()
-    alc_launch_ms = alc_max / args.steps  # one ALC launch per step at M = 10,000
-    flops_launch = M_rank * alc_paper_flops_per_location(n0, n, Np)
-    achieved = flops_launch / (alc_launch_ms / 1000.0) / 1e12
-    traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(f"alc_{args.form}")
+            tr = json.load(open(tp))
+            head["roofline"]["traffic"] = tr.get(args.form)
+            for f in others:
+                others[f]["roofline"]["traffic"] = tr.get(f)
         except Exception:
-            traffic = None
+            pass
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -302,15 +338,12 @@ def main():
                    "alc_form": args.form, "l2": "flushed (256 MiB write) before every timed step",
                    "parallelism": f"dp{world} (XX sharded, X/Z replicated)"},
         "alc_evals_per_sec": M_all * evals / (ms_step / 1000.0),
-        "phase_ms_per_step": {"nn": nn_ms / args.steps, "alc_loop_and_predict": alc_ms / args.steps},
-        "roofline": {"bound": "alu", "kernel": f"alc_{args.form}_kernel", "achieved": achieved,
-                     "peak": nominal, "unit": "TFLOP/s", "frac": achieved / nominal, "traffic": traffic,
-                     "work": "paper-count (N'-j)(2j^2+4j) flop per location-step (SURVEY §8d), FP64",
-                     "peak_basis": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz",
-                     "peak_measured_dfma": meas},
+        "phase_ms_per_step": {"nn": head["nn_ms"], "local_design": head["alc_ms"]},
+        "roofline": head["roofline"],
+        "forms": others,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": launches,
-        "clocks": clk,
+        "gpu_launches": head["launches"],
+        "clocks": head["clk"],
         "status": int(res["status"]),
     }
     if world == 1 and not args.no_cpu_baseline:

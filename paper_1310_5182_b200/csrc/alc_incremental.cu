@@ -44,7 +44,7 @@ constexpr int INC_THREADS = 1024;
 struct IncShared {
     double xstar[LAGP_PMAX];
     double xq[LAGP_PMAX];
-    double rho, znew, ystar;
+    double rho, rrho, znew, ystar;
     uint32_t fl;
 };
 
@@ -179,6 +179,7 @@ alc_incremental_kernel(AlcArgs A, int S) {
                         }
                         const double rho = sqrt(s[q]);
                         sh.rho = rho;
+                        sh.rrho = 1.0 / rho;
                         sh.znew = cov[q] / rho;
                         sh.ystar = zc[cstar];
                         chosen[q] = true;
@@ -190,7 +191,7 @@ alc_incremental_kernel(AlcArgs A, int S) {
             for (int a = R + tid; a < j; a += blockDim.x)
                 wstar[a] = (a < RS) ? wsm[(size_t)(a - R) * Npad + cstar] : gw[(size_t)(a - RS) * Npad + cstar];
             __syncthreads();
-            const double rrho = 1.0 / sh.rho, znew = sh.znew;
+            const double rrho = sh.rrho, znew = sh.znew;
             if (wid == 0) {  // a5 state: y~_j = (y* - w*^T y~) / rho, z_j = z_new
                 double acc = 0.0;
                 for (int a = lane; a < j; a += 32) acc = fma(wstar[a], ytil[a], acc);
@@ -239,12 +240,18 @@ alc_incremental_kernel(AlcArgs A, int S) {
                     acc1 = fma(ws.y, wr[q][a + 1], acc1);
                 }
                 const int jr = j < RS ? j : RS;
+                const double *wp = wsm + c;  // column of this candidate, entry a at wp[(a - R) * Npad]
                 int a = R;
-                for (; a + 1 < jr; a += 2) {
-                    acc0 = fma(wstar[a], wsm[(size_t)(a - R) * Npad + c], acc0);
-                    acc1 = fma(wstar[a + 1], wsm[(size_t)(a + 1 - R) * Npad + c], acc1);
+                for (; a + 3 < jr; a += 4) {  // R even -> a even: wstar pairs are 16-byte aligned
+                    const double2 s01 = *reinterpret_cast<const double2 *>(wstar + a);
+                    const double2 s23 = *reinterpret_cast<const double2 *>(wstar + a + 2);
+                    const double *q0 = wp + (size_t)(a - R) * Npad;
+                    acc0 = fma(s01.x, q0[0], acc0);
+                    acc1 = fma(s01.y, q0[Npad], acc1);
+                    acc0 = fma(s23.x, q0[2 * Npad], acc0);
+                    acc1 = fma(s23.y, q0[3 * Npad], acc1);
                 }
-                if (a < jr) acc0 = fma(wstar[a], wsm[(size_t)(a - R) * Npad + c], acc0);
+                for (; a < jr; a++) acc0 = fma(wstar[a], wp[(size_t)(a - R) * Npad], acc0);
                 const double e = corr_from_d2(d2, rth) - ((acc0 + acc1) + (acc2 + acc3));
                 const double wn = e * rrho;
                 if (j < R) {
