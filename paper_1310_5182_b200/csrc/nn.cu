@@ -404,8 +404,17 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
     NNSmem &s = *reinterpret_cast<NNSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
     const int64_t ngroups = (M + NN_Q - 1) / NN_Q;
-    const int S = (int)(N < NN_SAMPLE ? N : NN_SAMPLE);
-    float *samp = samp_ws + (size_t)blockIdx.x * NN_Q * NN_SAMPLE;
+    // sample sizes and target ranks (see the threshold phase)
+    const int S1 = (int)(N < 1024 ? N : 1024);
+    int64_t s2 = (int64_t)64 * N / (Nprime > 0 ? Nprime : 1);
+    if (s2 < S1) s2 = S1;
+    if (s2 > 65536) s2 = 65536;
+    if (s2 > N) s2 = N;
+    const int S2 = (int)s2;
+    const int r2 = (int)ceil(1.5 * (double)Nprime * (double)S2 / (double)N) + 12;
+    int r1 = (int)ceil(4.0 * (double)r2 * (double)S1 / (double)S2) + 4;
+    if (Nprime >= N) r1 = S1 + 1;
+    (void)samp_ws;
     uint64_t *bufk = bufk_ws + (size_t)blockIdx.x * NN_Q * bufcap;
     int32_t *bufi = bufi_ws + (size_t)blockIdx.x * NN_Q * bufcap;
     const double Bn2 = __longlong_as_double((long long)*maxn2_bits);
@@ -426,27 +435,66 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
             for (int k = 0; k < p; k++) n2 = fma(s.qx[tid][k], s.qx[tid][k], n2);
             s.qn2[tid] = n2;
         }
-        // ---- sample phase: strided sample of FP32 distances for every query
-        for (int e = tid; e < NN_Q * S; e += blockDim.x) {
-            const int q = e / S, t = e - q * S;
-            const int64_t r = (int64_t)t * N / S;
-            float xf[P ? P : LAGP_PMAX];
-            load_row32<P>(X32, r, p, xf);
-            samp[q * NN_SAMPLE + t] = row_d2f<P>(xf, s.nqf[q], p);
-        }
-        __syncthreads();
-        for (int q = wid; q < NN_Q; q += nw) {
-            // target ~1.5 N' survivors (+ a few sample ranks of slack)
-            int r = (int)ceil(1.5 * (double)Nprime * (double)S / (double)N) + 12;
-            if (Nprime >= N || r > S) r = S + 1;  // tau = +inf: every row
-            const float tq = warp_quantile(samp + q * NN_SAMPLE, S, r, s.whist[wid]);
-            if (lane == 0) {
-                s.rank[q] = r;
-                s.tau[q] = (double)tq;
-                s.state[q] = q < nq ? 0 : 1;
+        // ---- threshold phase, two-level sampling (all 16 queries per row load).
+        // T1: S1 <= 1024 strided rows; tau1 at a generous rank (about 4x the final
+        //     target, so it bounds the T2 order statistic with margin).
+        // T2: S2 = min(N, 64 N / N') strided rows; the T2 distances below tau1 are
+        //     listed (~4 r2 per query) and tau = their r2-th smallest, where r2 puts
+        //     ~1.5 N' expected survivors under tau (relative spread ~1/sqrt(r2) = 10 %).
+        {
+            float *t1 = reinterpret_cast<float *>(s.key);  // NN_Q x 1024 floats (64 KB)
+            for (int e = tid; e < NN_Q * S1; e += blockDim.x) {
+                const int q = e / S1, t = e - q * S1;
+                const int64_t r = (int64_t)t * N / S1;
+                float xf[P ? P : LAGP_PMAX];
+                load_row32<P>(X32, r, p, xf);
+                t1[q * 1024 + t] = row_d2f<P>(xf, s.nqf[q], p);
+            }
+            __syncthreads();
+            for (int q = wid; q < NN_Q; q += nw) {
+                const float tq = (r1 > S1) ? INFINITY : warp_quantile(t1 + q * 1024, S1, r1, s.whist[wid]);
+                if (lane == 0) {
+                    s.tau[q] = (double)tq;
+                    s.state[q] = q < nq ? 0 : 1;
+                    s.cnt[q] = 0;
+                }
+            }
+            __syncthreads();
+            if (S2 > S1 && r2 <= S2) {
+                float *lst = reinterpret_cast<float *>(bufk);  // per query bufcap floats
+                for (int64_t t = tid; t < S2; t += blockDim.x) {
+                    const int64_t r = t * N / S2;
+                    float xf[P ? P : LAGP_PMAX];
+                    load_row32<P>(X32, r, p, xf);
+#pragma unroll
+                    for (int q = 0; q < NN_Q; q++) {
+                        const float d2f = row_d2f<P>(xf, s.nqf[q], p);
+                        if (d2f <= (float)s.tau[q]) {
+                            const int pos = atomicAdd(&s.cnt[q], 1);
+                            if (pos < bufcap) lst[(size_t)q * bufcap + pos] = d2f;
+                        }
+                    }
+                }
+                __syncthreads();
+                for (int q = wid; q < NN_Q; q += nw) {
+                    const int c2 = s.cnt[q];
+                    if (c2 >= r2 && c2 <= bufcap) {  // else keep tau1; the filter rounds adapt it
+                        const float tq = warp_quantile(lst + (size_t)q * bufcap, c2, r2, s.whist[wid]);
+                        if (lane == 0) s.tau[q] = (double)tq;
+                    }
+                }
+                __syncthreads();
+            } else if (r2 > S2) {
+                if (tid < NN_Q) s.tau[tid] = INFINITY;  // N' close to N: every row
+                __syncthreads();
+            } else {  // S2 == S1: T1 already has the target resolution
+                for (int q = wid; q < NN_Q; q += nw) {
+                    const float tq = warp_quantile(t1 + q * 1024, S1, r2 <= S1 ? r2 : S1, s.whist[wid]);
+                    if (lane == 0) s.tau[q] = (double)tq;
+                }
+                __syncthreads();
             }
         }
-        __syncthreads();
 
         // ---- filter rounds
         for (int round = 0; round < NN_MAX_ROUNDS; round++) {
@@ -504,27 +552,22 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 }
                 __syncthreads();
             }
-            // re-pick the rank of the missed queries from their samples
-            for (int q = wid; q < NN_Q; q += nw) {
-                if (s.state[q] != 0) continue;  // warp-uniform
+            // missed queries: rescale tau (the count of rows inside the d^2 <= tau ball
+            // grows like tau^(p/2)), aiming at ~1.5 N' survivors
+            if (tid < NN_Q && s.state[tid] == 0) {
+                const int q = tid;
                 const int c = s.cnt[q] > bufcap ? s.cnt[q] : s.valid[q];  // overflow -> too many
-                const int r = s.rank[q];
-                int nr = r, st = 0;
+                const double tau = s.tau[q];
                 if (c >= Nprime && c <= bufcap) {
-                    st = 1;
-                } else if (c < Nprime) {
-                    nr = (int)ceil((double)r * 1.5 * (double)Nprime / (double)(c > 0 ? c : 1)) + 16;
-                    if (nr <= r) nr = r + 1;
-                    if (r > S) st = 2; else if (nr > S) nr = S + 1;
+                    s.state[q] = 1;
+                } else if (!isfinite(tau) || tau <= 0.0) {
+                    s.state[q] = 2;  // cannot rescale (massive ties at 0, or already +inf)
                 } else {
-                    nr = (int)floor((double)(r > S ? S : r) * 0.7 * (double)bufcap / (double)c);
-                    if (nr >= r || nr < 1) st = 2;
-                }
-                float tq = 0.f;
-                if (st == 0) tq = warp_quantile(samp + q * NN_SAMPLE, S, nr, s.whist[wid]);
-                if (lane == 0) {
-                    s.state[q] = st;
-                    if (st == 0) { s.rank[q] = nr; s.tau[q] = (double)tq; }
+                    const double target = c < Nprime ? 1.5 * Nprime : 0.7 * bufcap;
+                    double f = pow(target / (double)(c > 0 ? c : 1), 2.0 / (double)p);
+                    if (c < Nprime && f < 1.05) f = 1.05;
+                    if (c > bufcap && f > 0.95) f = 0.95;
+                    s.tau[q] = tau * f;
                 }
             }
             __syncthreads();
