@@ -32,7 +32,9 @@ struct NNSmem {
     uint64_t key[NN_CAP];
     int32_t idx[NN_CAP];
     double qx[NN_Q][LAGP_PMAX];
-    float nqf[NN_Q][LAGP_PMAX];  // -(query coords) in FP32 for the prefilter
+    float nqf[NN_Q][LAGP_PMAX];  // -(query coords) in FP32 for the sampling distances
+    float qf[NN_Q][LAGP_PMAX];   // query coords in FP32 for the dot-form prefilter
+    float qn2f[NN_Q];            // ||q~||^2 in FP32
     double tau[NN_Q];
     float thrf[NN_Q];            // FP32 prefilter threshold: tau + rounding margin, rounded up
     double qn2[NN_Q];            // ||x_q||^2 (for the margin)
@@ -197,15 +199,19 @@ __device__ void nn_exact_select(NNSmem &s, const double *__restrict__ X, int64_t
 
 // FP32 copy of X for the prefilter and B = max_i ||X_i||^2 (as ordered uint64 bits).
 __global__ void nn_prep_kernel(const double *__restrict__ X, int64_t N, int p, float *__restrict__ X32,
-                               unsigned long long *__restrict__ maxn2) {
+                               float *__restrict__ rn2f, unsigned long long *__restrict__ maxn2) {
     double mx = 0.0;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
         double n2 = 0.0;
+        float f2 = 0.f;
         for (int k = 0; k < p; k++) {
             const double v = X[r * p + k];
-            X32[r * p + k] = (float)v;
+            const float vf = (float)v;
+            X32[r * p + k] = vf;
+            f2 = fmaf(vf, vf, f2);
             n2 = fma(v, v, n2);
         }
+        rn2f[r] = f2;
         mx = fmax(mx, n2);
     }
 #pragma unroll
@@ -394,9 +400,27 @@ __device__ void select_pool(NNSmem &s, int c, int Nprime, int n0, int32_t *__res
     __syncthreads();
 }
 
+// paired-FP32 dot product x~ . q~ (FFMA2)
+template <int P>
+__device__ __forceinline__ float row_dotf(const float *xf, const float *qf, int p) {
+    constexpr int PP = P ? P : LAGP_PMAX;
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k + 1 < PP; k += 2) {
+        if (P || k + 1 < p) acc = __ffma2_rn(make_float2(xf[k], xf[k + 1]), make_float2(qf[k], qf[k + 1]), acc);
+        else if (!P && k < p) acc.x = fmaf(xf[k], qf[k], acc.x);
+    }
+    if (PP & 1) {
+        const int k = PP - 1;
+        if (P || k < p) acc.x = fmaf(xf[k], qf[k], acc.x);
+    }
+    return acc.x + acc.y;
+}
+
 template <int P>
 __global__ void __launch_bounds__(NN_THREADS)
-nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, const unsigned long long *maxn2_bits,
+nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, const float *__restrict__ rn2f,
+               const unsigned long long *maxn2_bits,
                int64_t N, int p, const double *__restrict__ XX, int64_t M, int Nprime, int n0, int bufcap,
                int sorted, int32_t *__restrict__ pool_out, double *__restrict__ d2_out, float *__restrict__ samp_ws,
                uint64_t *__restrict__ bufk_ws, int32_t *__restrict__ bufi_ws, int *__restrict__ fallback_count) {
@@ -428,12 +452,16 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
             const double v = (q < nq && k < p) ? XX[(q0 + q) * p + k] : 0.0;
             s.qx[q][k] = v;
             s.nqf[q][k] = -(float)v;
+            s.qf[q][k] = (float)v;
         }
         __syncthreads();
         if (tid < NN_Q) {
             double n2 = 0.0;
             for (int k = 0; k < p; k++) n2 = fma(s.qx[tid][k], s.qx[tid][k], n2);
             s.qn2[tid] = n2;
+            float f2 = 0.f;
+            for (int k = 0; k < p; k++) f2 = fmaf(s.qf[tid][k], s.qf[tid][k], f2);
+            s.qn2f[tid] = f2;
         }
         // ---- threshold phase, two-level sampling (all 16 queries per row load).
         // T1: S1 <= 1024 strided rows; tau1 at a generous rank (about 4x the final
@@ -502,26 +530,49 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 const int q = tid;
                 s.cnt[q] = 0;
                 const double tau = s.tau[q];
-                // FP32 prefilter threshold. With u = 2^-24 and inputs rounded to
-                // FP32, |d2_f32 - d2_exact| <= 8u(||x||^2 + ||X_i||^2) + (p+1)u d2 + O(u^2);
-                // the margin doubles both terms, so every row with exact d2 <= tau passes.
-                const double thr = tau + 16.0 * u32 * (s.qn2[q] + Bn2) + 2.0 * (p + 1) * u32 * tau;
+                // FP32 prefilter threshold for the dot form d2 ~ ||x~||^2 + ||q~||^2 - 2 x~.q~
+                // (x~, q~ the FP32-rounded inputs, u = 2^-24): rounding the inputs moves d2 by
+                // <= 4u(||x||^2 + ||q||^2) and the FP32 evaluation by <= 2(p+3)u(||x||^2 + ||q||^2)
+                // (first order), i.e. <= (2p+10)u(||x||^2 + ||q||^2); the margin doubles it, so
+                // every row with exact d2 <= tau passes and the FP64 key alone decides.
+                const double thr = tau + (4.0 * p + 20.0) * u32 * (s.qn2[q] + Bn2);
                 s.thrf[q] = isfinite(thr) ? __double2float_ru(thr) : INFINITY;
             }
             __syncthreads();
             unsigned act = 0;
             for (int q = 0; q < NN_Q; q++) act |= (s.state[q] == 0 ? 1u : 0u) << q;
             if (!act) break;
-            for (int64_t r = tid; r < N; r += blockDim.x) {
-                float xf[P ? P : LAGP_PMAX];
-                load_row32<P>(X32, r, p, xf);
+            // 4 rows per thread per iteration: each query's coordinates are loaded
+            // from shared memory once per 4 rows
+            for (int64_t base = tid; base < N; base += 4 * (int64_t)blockDim.x) {
+                float xf[4][P ? P : LAGP_PMAX];
+                float rn[4];
 #pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int64_t r = base + u * (int64_t)blockDim.x;
+                    if (r < N) {
+                        load_row32<P>(X32, r, p, xf[u]);
+                        rn[u] = __ldg(rn2f + r);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < (P ? P : LAGP_PMAX); k++) xf[u][k] = 0.f;
+                        rn[u] = __int_as_float(0x7fc00000);  // NaN: never <= thr, even thr = +inf
+                    }
+                }
+#pragma unroll 1
                 for (int q = 0; q < NN_Q; q++) {
                     if (!((act >> q) & 1u)) continue;
-                    const float d2f = row_d2f<P>(xf, s.nqf[q], p);
-                    if (d2f <= s.thrf[q]) {  // candidate: the exact key is computed densely below
-                        int pos = atomicAdd(&s.cnt[q], 1);
-                        if (pos < bufcap) bufi[q * bufcap + pos] = (int)r;
+                    float qv[P ? P : LAGP_PMAX];
+#pragma unroll
+                    for (int k = 0; k < (P ? P : LAGP_PMAX); k++) qv[k] = s.qf[q][k];
+                    const float qn = s.qn2f[q], thr = s.thrf[q];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const float d2f = fmaf(-2.f, row_dotf<P>(xf[u], qv, p), qn + rn[u]);
+                        if (d2f <= thr) {  // candidate: the exact key is computed densely below
+                            const int pos = atomicAdd(&s.cnt[q], 1);
+                            if (pos < bufcap) bufi[q * bufcap + pos] = (int)(base + u * (int64_t)blockDim.x);
+                        }
                     }
                 }
             }
@@ -626,12 +677,13 @@ static int nn_bufcap(int Nprime) {
 // Workspace layout: [maxn2 bits (256 B)] [X32: N*p floats] [sample] [survivor keys] [survivor idx]
 size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime) {
     const size_t bc = (size_t)nn_bufcap(Nprime);
-    return 256 + (((size_t)N * p * sizeof(float) + 255) & ~(size_t)255) +
+    return 256 + (((size_t)N * p * sizeof(float) + 255) & ~(size_t)255) + (((size_t)N * sizeof(float) + 255) & ~(size_t)255) +
            (size_t)grid * NN_Q * (NN_SAMPLE * sizeof(float) + bc * (sizeof(uint64_t) + sizeof(int32_t))) + 256;
 }
 
 template <int P>
-static cudaError_t launch_nn_t(const double *X, const float *X32, const unsigned long long *mx, int64_t N, int p,
+static cudaError_t launch_nn_t(const double *X, const float *X32, const float *rn2f, const unsigned long long *mx,
+                               int64_t N, int p,
                                const double *XX, int64_t M, int Nprime, int n0, int sorted, int32_t *pool, double *d2,
                                char *w, int grid, int *fb, cudaStream_t st) {
     size_t smem = sizeof(NNSmem);
@@ -643,7 +695,7 @@ static cudaError_t launch_nn_t(const double *X, const float *X32, const unsigned
     uint64_t *bk = (uint64_t *)w;
     w += (size_t)grid * NN_Q * bc * sizeof(uint64_t);
     int32_t *bi = (int32_t *)w;
-    nn_pool_kernel<P><<<grid, NN_THREADS, smem, st>>>(X, X32, mx, N, p, XX, M, Nprime, n0, bc, sorted, pool, d2, samp,
+    nn_pool_kernel<P><<<grid, NN_THREADS, smem, st>>>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, bc, sorted, pool, d2, samp,
                                                       bk, bi, fb);
     return cudaGetLastError();
 }
@@ -662,25 +714,26 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
     char *w = (char *)ws;
     unsigned long long *mx = (unsigned long long *)w;
     float *X32 = (float *)(w + 256);
-    char *rest = w + 256 + (((size_t)N * p * sizeof(float) + 255) & ~(size_t)255);
+    float *rn2f = (float *)(w + 256 + (((size_t)N * p * sizeof(float) + 255) & ~(size_t)255));
+    char *rest = (char *)rn2f + (((size_t)N * sizeof(float) + 255) & ~(size_t)255);
     if (!prepared) {
         cudaError_t e = cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st);
         if (e != cudaSuccess) return e;
         int blocks = (int)((N + 255) / 256);
         if (blocks > 4096) blocks = 4096;
-        nn_prep_kernel<<<blocks, 256, 0, st>>>(X, N, p, X32, mx);
+        nn_prep_kernel<<<blocks, 256, 0, st>>>(X, N, p, X32, rn2f, mx);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         if (launches) (*launches)++;
     }
     if (launches) (*launches)++;
     switch (p) {
-        case 1: return launch_nn_t<1>(X, X32, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        case 2: return launch_nn_t<2>(X, X32, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        case 3: return launch_nn_t<3>(X, X32, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        case 4: return launch_nn_t<4>(X, X32, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        case 8: return launch_nn_t<8>(X, X32, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        default: return launch_nn_t<0>(X, X32, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 1: return launch_nn_t<1>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 2: return launch_nn_t<2>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 3: return launch_nn_t<3>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 4: return launch_nn_t<4>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 8: return launch_nn_t<8>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        default: return launch_nn_t<0>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
     }
 }
 
