@@ -538,13 +538,16 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 const double thr = tau + (4.0 * p + 20.0) * u32 * (s.qn2[q] + Bn2);
                 s.thrf[q] = isfinite(thr) ? __double2float_ru(thr) : INFINITY;
             }
+            if (tid < NN_Q && s.state[tid] != 0) s.thrf[tid] = __int_as_float(0x7fc00000);  // NaN: inactive
             __syncthreads();
             unsigned act = 0;
             for (int q = 0; q < NN_Q; q++) act |= (s.state[q] == 0 ? 1u : 0u) << q;
             if (!act) break;
             // 4 rows per thread per iteration: each query's coordinates are loaded
             // from shared memory once per 4 rows
-            for (int64_t base = tid; base < N; base += 4 * (int64_t)blockDim.x) {
+            // (the loop bound is warp-uniform: the ballots below need whole warps)
+            for (int64_t wbase = tid - lane; wbase < N; wbase += 4 * (int64_t)blockDim.x) {
+                const int64_t base = wbase + lane;
                 float xf[4][P ? P : LAGP_PMAX];
                 float rn[4];
 #pragma unroll
@@ -560,18 +563,28 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                     }
                 }
 #pragma unroll 1
-                for (int q = 0; q < NN_Q; q++) {
-                    if (!((act >> q) & 1u)) continue;
+                for (int q = 0; q < NN_Q; q++) {  // inactive queries have thr = NaN: no candidates
                     float qv[P ? P : LAGP_PMAX];
 #pragma unroll
                     for (int k = 0; k < (P ? P : LAGP_PMAX); k++) qv[k] = s.qf[q][k];
                     const float qn = s.qn2f[q], thr = s.thrf[q];
+                    bool hit[4];
 #pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const float d2f = fmaf(-2.f, row_dotf<P>(xf[u], qv, p), qn + rn[u]);
-                        if (d2f <= thr) {  // candidate: the exact key is computed densely below
-                            const int pos = atomicAdd(&s.cnt[q], 1);
-                            if (pos < bufcap) bufi[q * bufcap + pos] = (int)(base + u * (int64_t)blockDim.x);
+                    for (int u = 0; u < 4; u++) hit[u] = fmaf(-2.f, row_dotf<P>(xf[u], qv, p), qn + rn[u]) <= thr;
+                    // warp-aggregated append: one uniform test per (row block, query)
+                    if (__any_sync(0xffffffffu, hit[0] | hit[1] | hit[2] | hit[3])) {
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const unsigned m = __ballot_sync(0xffffffffu, hit[u]);
+                            if (m) {
+                                int basepos = 0;
+                                if (lane == 0) basepos = atomicAdd(&s.cnt[q], __popc(m));
+                                basepos = __shfl_sync(0xffffffffu, basepos, 0);
+                                if (hit[u]) {
+                                    const int pos = basepos + __popc(m & ((1u << lane) - 1u));
+                                    if (pos < bufcap) bufi[q * bufcap + pos] = (int)(base + u * (int64_t)blockDim.x);
+                                }
+                            }
                         }
                     }
                 }
