@@ -136,7 +136,7 @@ def make_config(name: str, M: int | None = None, N: int | None = None, **over) -
         X = lhs(Nd, p, r["seedX"])
         # an LHS of size M is not a prefix of an LHS of size M' > M; always draw
         # the full-size predictive LHS and slice, so test subsets match the bench.
-        XX = lhs(r["M"], p, r["seedXX"])[:Mx]
+        XX = lhs(max(r["M"], Mx), p, r["seedXX"])[:Mx]
         Z = borehole(X)
     elif r["kind"] == "lgbb":
         X = lgbb_design(jitter_seed=r["seedX"])

@@ -117,6 +117,7 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
     lagp_status st_ret = LAGP_OK;
     if (timing) std::memset(timing, 0, sizeof *timing);
     if (M == 0) return LAGP_OK;
+    cudaGetLastError();  // this library's (static) runtime state only: start from a clean error slot
 
     const int sms = num_sms();
     const int ld = (n + 3) & ~3;
@@ -165,7 +166,8 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
     LAGP_CUDA(ws.alloc((void **)&pool, (size_t)chunk * Nprime * sizeof(int32_t)));
     LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(nn_grid, N, p, Nprime)));
     LAGP_CUDA(ws.alloc((void **)&cache, (size_t)alc_grid * cache_stride * sizeof(double)));
-    LAGP_CUDA(ws.alloc((void **)&coords, (size_t)alc_grid * p * Npad * sizeof(double)));
+    // per-CTA slab: pool coordinates [p][Npad] (+ kappa and chosen flags for the DFMA kernel)
+    LAGP_CUDA(ws.alloc((void **)&coords, (size_t)alc_grid * (p + 2) * Npad * sizeof(double)));
     LAGP_CUDA(ws.alloc((void **)&counters, 2 * sizeof(int)));
     LAGP_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int), st));
     if (timing)

@@ -41,9 +41,13 @@ __device__ __forceinline__ int kp(int a, int b, int ld) {
     return ((a >> 1) & 1) * (ld * ld / 2) + ((b * (ld >> 2) + (a >> 2)) << 1) + (a & 1);
 }
 
-// smem carve-up (doubles): Kp ld*ld | tile 2*ALC_TILE | Xj n*p | h,w,ks,us,yv 5*ld | kap Npad | red 160 | chosen Npad bytes
+// smem carve-up (doubles): Kp ld*ld | tile 2*ALC_TILE | Xj n*p | h,w,ks,us,yv 5*ld | red 160.
+// kappa_c and the chosen mask live in the per-CTA global slab after the pool
+// coordinates (read once per candidate per step in the epilogue), so the
+// shared-memory footprint does not grow with N' (n = 128 needs 128 KB for K^{-1}).
 __host__ __device__ inline size_t alc_smem_bytes(int ld, int n, int p, int Npad) {
-    return ((size_t)ld * ld + 2 * ALC_TILE + (size_t)((n * p + 3) & ~3) + 5 * (size_t)ld + Npad + 160) * sizeof(double) + Npad;
+    (void)Npad;
+    return ((size_t)ld * ld + 2 * ALC_TILE + (size_t)((n * p + 3) & ~3) + 5 * (size_t)ld + 160) * sizeof(double);
 }
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
@@ -112,15 +116,15 @@ alc_explicit_kernel(AlcArgs A) {
     double *ks = w + ld;
     double *us = ks + ld;
     double *yv = us + ld;
-    double *kap = yv + ld;
-    double *red = kap + Npad;  // 160 doubles of reduction scratch
-    unsigned char *chosen = reinterpret_cast<unsigned char *>(red + 160);
+    double *red = yv + ld;  // 160 doubles of reduction scratch
     __shared__ double xq[LAGP_PMAX];
     __shared__ uint32_t fl_s;
 
     const int tid = threadIdx.x;
     double *cache = A.cache + (size_t)blockIdx.x * A.cache_stride;
-    double *coords = A.coords + (size_t)blockIdx.x * p * Npad;
+    double *coords = A.coords + (size_t)blockIdx.x * (p + 2) * Npad;  // [p][Npad] coords | kap | chosen
+    double *kap = coords + (size_t)p * Npad;
+    unsigned char *chosen = reinterpret_cast<unsigned char *>(kap + Npad);
     const double rth = A.rtheta, eta = A.eta;
     const int G = n - A.n0;
 
@@ -131,7 +135,7 @@ alc_explicit_kernel(AlcArgs A) {
         if (tid == 0) fl_s = 0;
         for (int e = tid; e < ld * ld; e += blockDim.x) Kp[e] = 0.0;
         __syncthreads();
-        // ---- gather the pool (SoA coords in the slab), kappa_c and the chosen mask in smem
+        // ---- gather the pool (SoA coords), kappa_c and the chosen mask into the CTA's slab
         for (int c = tid; c < Np; c += blockDim.x) {
             const double *xr = A.X + (int64_t)pool[c] * p;
             for (int k = 0; k < p; k++) coords[k * Npad + c] = xr[k];
@@ -338,10 +342,14 @@ cudaError_t launch_alc_explicit(const AlcArgs &a, int grid, cudaStream_t st) {
 int alc_explicit_blocks_per_sm(int ld, int n, int p, int Npad) {
     int nb = 0;
     size_t smem = alc_smem_bytes(ld, n, p, Npad);
-    if (cudaFuncSetAttribute(alc_explicit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(alc_explicit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();  // do not leave a sticky error for the next launch check
         return 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, alc_explicit_kernel, ALC_THREADS, smem) != cudaSuccess)
+    }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, alc_explicit_kernel, ALC_THREADS, smem) != cudaSuccess) {
+        cudaGetLastError();
         nb = 0;
+    }
     return nb;
 }
 

@@ -313,10 +313,14 @@ int alc_explicit_dmma_blocks_per_sm(int n, int p, int Npad) {
     int nb = 0;
     size_t smem = dm_smem_bytes(n, p, Npad);
     if (cudaFuncSetAttribute(alc_explicit_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
+        cudaSuccess) {
+        cudaGetLastError();  // do not leave a sticky error for the next launch check
         return 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, alc_explicit_dmma_kernel, DM_THREADS, smem) != cudaSuccess)
+    }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, alc_explicit_dmma_kernel, DM_THREADS, smem) != cudaSuccess) {
+        cudaGetLastError();
         nb = 0;
+    }
     return nb;
 }
 

@@ -50,7 +50,14 @@ for p in [int(x) for x in a.ps.split(",")]:
             for form in a.forms.split(","):
                 # calibrate M
                 M = 64
-                r = lagp.alc_batch(X, Z, XXall[:M], *args, form=form, timing=True)
+                try:
+                    r = lagp.alc_batch(X, Z, XXall[:M], *args, form=form, timing=True)
+                except lagp.LagpError as ex:  # outside this build's limits: record, continue
+                    line = json.dumps(dict(p=p, n=n, Nprime=Np, form=form, unsupported=str(ex)))
+                    print(line, flush=True)
+                    if out:
+                        out.write(line + "\n")
+                    continue
                 while r["timing"]["alc_ms"] < a.target_ms / 2 and M < 32768:
                     M = min(32768, M * 2 if r["timing"]["alc_ms"] > 0 else M * 4)
                     r = lagp.alc_batch(X, Z, XXall[:M], *args, form=form, timing=True)
