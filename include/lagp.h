@@ -33,6 +33,8 @@ extern "C" {
 #define LAGP_ABI_VERSION 1
 #define LAGP_NMAX 128  /* largest local design size n supported (Fig 4 uses n <= 512: NEXT f4) */
 #define LAGP_PMAX 16   /* largest input dimension p */
+#define LAGP_NPRIME_MAX 65536 /* largest candidate pool N' (laGP_alc_batch; the incremental
+                                 form takes N' <= 8192, laGP_nn_pool's sorted output N' <= 8192) */
 
 typedef enum {
     LAGP_OK = 0,      /* every location reached size n                                   */
@@ -94,7 +96,8 @@ typedef struct {
  *   X [N×p], Z [N]          design and responses (zero-mean GP, Z used raw, R14)
  *   XX [M×p]                predictive locations (this shard); M may be 0
  *   d  (theta > 0, finite)  lengthscale;  g (eta >= 0, finite) nugget
- *   1 <= n0 <= n <= Nprime <= N,  n <= LAGP_NMAX,  1 <= p <= LAGP_PMAX
+ *   1 <= n0 <= n <= Nprime <= N,  n <= LAGP_NMAX,  1 <= p <= LAGP_PMAX,
+ *   Nprime <= LAGP_NPRIME_MAX (<= 8192 for LAGP_ALC_INCREMENTAL)
  *   idx_out  [M×n] int32    first n0 = NN order, then greedy order; -1 tail if exhausted
  *   mean_out [M], s2_out [M]
  *   var_out  [M]   nullable

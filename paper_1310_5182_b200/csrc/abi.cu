@@ -89,7 +89,8 @@ lagp_status check_batch_args(const double *X, int64_t N, int32_t p, const double
     if (n > LAGP_NMAX) return fail(LAGP_EINVAL, "n must be <= LAGP_NMAX=%d (got %d)", LAGP_NMAX, n);
     if (Nprime < n) return fail(LAGP_EINVAL, "Nprime must be >= n (got Nprime=%d, n=%d)", Nprime, n);
     if (Nprime > N) return fail(LAGP_EINVAL, "Nprime must be <= N (got Nprime=%d, N=%lld)", Nprime, (long long)N);
-    if (Nprime > 8192) return fail(LAGP_EINVAL, "Nprime must be <= 8192 in this build (got %d)", Nprime);
+    if (Nprime > LAGP_NPRIME_MAX)
+        return fail(LAGP_EINVAL, "Nprime must be <= LAGP_NPRIME_MAX=%d (got %d)", LAGP_NPRIME_MAX, Nprime);
     if (!X || !Z) return fail(LAGP_EINVAL, "X and Z must be non-NULL");
     if (M > 0 && (!XX || !idx_out || !mean_out || !s2_out))
         return fail(LAGP_EINVAL, "XX, idx_out, mean_out and s2_out must be non-NULL when M > 0");
@@ -149,8 +150,11 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
         return fail(LAGP_EINVAL, "local-design state does not fit in shared memory (n=%d, Nprime=%d)", n, Nprime);
     const int alc_grid_max = alc_bps * sms;
     // chunk of locations per NN+ALC round: bounds the pool buffer (chunk × N' int32)
-    const int64_t chunk = M < 65536 ? M : 65536;
-    const int nn_grid = lagp::nn_grid(chunk, sms);
+    // (at most 65,536 locations and a ~1 GiB pool buffer per chunk)
+    int64_t chunk = M < 65536 ? M : 65536;
+    const int64_t chunk_pool = ((int64_t)1 << 28) / Nprime;
+    if (chunk > chunk_pool) chunk = chunk_pool > 1 ? chunk_pool : 1;
+    const int nn_grid = lagp::nn_grid(chunk, sms, Nprime);
     const int alc_grid = (int)(chunk < alc_grid_max ? chunk : alc_grid_max);
 
     Workspace ws(st);
@@ -164,7 +168,7 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
     int host_counters[2] = {0, 0};
 
     LAGP_CUDA(ws.alloc((void **)&pool, (size_t)chunk * Nprime * sizeof(int32_t)));
-    LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(nn_grid, N, p, Nprime)));
+    LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(nn_grid, N, p, Nprime, false)));
     LAGP_CUDA(ws.alloc((void **)&cache, (size_t)alc_grid * cache_stride * sizeof(double)));
     // per-CTA slab: pool coordinates [p][Npad] (+ kappa and chosen flags for the DFMA kernel)
     LAGP_CUDA(ws.alloc((void **)&coords, (size_t)alc_grid * (p + 2) * Npad * sizeof(double)));
@@ -178,7 +182,7 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
         const int64_t mc = (M - m0) < chunk ? (M - m0) : chunk;
         if (timing) LAGP_CUDA(cudaEventRecord(ev[1], st));
         LAGP_CUDA(lagp::launch_nn(X, N, p, XX + m0 * p, mc, Nprime, n0, false, pool, nullptr, nnws,
-                                  lagp::nn_grid(mc, sms), counters + 1, st, m0 > 0, &launches));
+                                  lagp::nn_grid(mc, sms, Nprime), counters + 1, st, m0 > 0, &launches));
         if (timing) LAGP_CUDA(cudaEventRecord(ev[2], st));
         lagp::AlcArgs a;
         a.X = X; a.N = N; a.p = p; a.Z = Z; a.XX = XX + m0 * p; a.M = mc;
@@ -302,8 +306,8 @@ lagp_status laGP_nn_pool(const double *X, int64_t N, int32_t p, const double *XX
         Workspace ws(st);
         void *nnws = nullptr;
         int *fb = nullptr;
-        const int grid = lagp::nn_grid(M, num_sms());
-        LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(grid, N, p, Nprime)));
+        const int grid = lagp::nn_grid(M, num_sms(), Nprime);
+        LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(grid, N, p, Nprime, true)));
         LAGP_CUDA(ws.alloc((void **)&fb, sizeof(int)));
         LAGP_CUDA(cudaMemsetAsync(fb, 0, sizeof(int), st));
         LAGP_CUDA(lagp::launch_nn(X, N, p, XX, M, Nprime, Nprime, true, pool_out, d2_out, nnws, grid, fb, st, false,

@@ -33,12 +33,12 @@ __host__ __device__ inline int dm_kl(int n) {
 }
 __host__ __device__ inline int dm_kr(int n) { return (n + 7) & ~7; }
 __host__ __device__ inline int dm_vl(int n) { return dm_kr(n) > dm_kl(n) ? dm_kr(n) : dm_kl(n); }
-// smem (doubles): K kr*kl | tiles 2*kr*TL | Xj r4(n*p) | h,w,ks,us,yv 5*kl | kap Npad | red 160 | chosen Npad bytes
+// smem (doubles): K kr*kl | tiles 2*kr*TL | Xj r4(n*p) | h,w,ks,us,yv 5*vl | red 160
 __host__ __device__ inline size_t dm_smem_bytes(int n, int p, int Npad) {
     const int kl = dm_kl(n), kr = dm_kr(n);
-    return ((size_t)kr * kl + 2 * (size_t)kr * DM_TL + (size_t)((n * p + 3) & ~3) + 5 * (size_t)dm_vl(n) + Npad + 160) *
-               sizeof(double) +
-           Npad;
+    (void)Npad;  // kappa_c / chosen live in the CTA's global slab: smem does not grow with N'
+    return ((size_t)kr * kl + 2 * (size_t)kr * DM_TL + (size_t)((n * p + 3) & ~3) + 5 * (size_t)dm_vl(n) + 160) *
+           sizeof(double);
 }
 
 __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
@@ -103,16 +103,16 @@ alc_explicit_dmma_kernel(AlcArgs A) {
     double *ks = w + vl;
     double *us = ks + vl;
     double *yv = us + vl;
-    double *kap = yv + vl;
-    double *red = kap + Npad;
-    unsigned char *chosen = reinterpret_cast<unsigned char *>(red + 160);
+    double *red = yv + vl;
     __shared__ double xq[LAGP_PMAX];
     __shared__ uint32_t fl_s;
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int g = lane >> 2, kq = lane & 3;
     double *cache = A.cache + (size_t)blockIdx.x * A.cache_stride;
-    double *coords = A.coords + (size_t)blockIdx.x * p * Npad;
+    double *coords = A.coords + (size_t)blockIdx.x * (p + 2) * Npad;  // [p][Npad] coords | kap | chosen
+    double *kap = coords + (size_t)p * Npad;
+    unsigned char *chosen = reinterpret_cast<unsigned char *>(kap + Npad);
     const double rth = A.rtheta, eta = A.eta;
     const int G = n - A.n0;
 

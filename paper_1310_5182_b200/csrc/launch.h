@@ -12,8 +12,8 @@ namespace lagp {
 cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64_t M, int Nprime, int n0, bool sorted,
                       int32_t *pool, double *d2, void *ws, int grid, int *fb, cudaStream_t st, bool prepared,
                       int *launches);
-size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime);
-int nn_grid(int64_t M, int num_sms);
+size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime, bool sorted);
+int nn_grid(int64_t M, int num_sms, int Nprime);
 
 // fused local-design kernels (rows a2-a5)
 struct AlcArgs {

@@ -128,11 +128,11 @@ __device__ __forceinline__ void warp_pick_bin(const unsigned *hist, int need, in
 
 // Exact fallback for one query (index q within the group): radix select of the
 // Nprime-th smallest 64-bit key, then an ordered collection that takes every
-// key below it plus the lowest-index rows equal to it. Leaves s.key/s.idx
-// holding exactly Nprime entries (unsorted).
+// key below it plus the lowest-index rows equal to it. Leaves ok/oi (global
+// buffers of the query) holding exactly Nprime entries (unsorted).
 template <int P>
-__device__ void nn_exact_select(NNSmem &s, const double *__restrict__ X, int64_t N, int p, int q,
-                                int Nprime) {
+__device__ void nn_exact_select(NNSmem &s, const double *__restrict__ X, int64_t N, int p, int q, int Nprime,
+                                uint64_t *ok, int32_t *oi) {
     const int tid = threadIdx.x;
     uint64_t prefix = 0;
     int need = Nprime;  // rank (1-based) of the target within the current prefix bucket
@@ -171,8 +171,8 @@ __device__ void nn_exact_select(NNSmem &s, const double *__restrict__ X, int64_t
         bool eq = (r < N) && k == tau;
         if (lt) {
             int pos = atomicAdd(&s.misc[2], 1);
-            s.key[pos] = k;
-            s.idx[pos] = (int)r;
+            ok[pos] = k;
+            oi[pos] = (int)r;
         }
         unsigned bal = __ballot_sync(0xffffffffu, eq);
         if (lane == 0) s.scan[wid] = __popc(bal);
@@ -182,8 +182,8 @@ __device__ void nn_exact_select(NNSmem &s, const double *__restrict__ X, int64_t
         int rk = before + __popc(bal & ((1u << lane) - 1u));
         if (eq && rk < need) {
             int pos = (Nprime - need) + rk;
-            s.key[pos] = k;
-            s.idx[pos] = (int)r;
+            ok[pos] = k;
+            oi[pos] = (int)r;
         }
         __syncthreads();
         if (tid == 0) {
@@ -325,7 +325,9 @@ __device__ __forceinline__ bool kv_less(unsigned long long ka, int ia, unsigned 
 // order), then the rest compacted in any order (positions >= n0 never affect
 // results: every candidate's score and the (Delta, index) argmax are
 // order-independent).
-__device__ void select_pool(NNSmem &s, int c, int Nprime, int n0, int32_t *__restrict__ po) {
+// K/I may be shared or global memory (large pools select in the global buffers).
+__device__ void select_pool(NNSmem &s, uint64_t *K, int32_t *I, int c, int Nprime, int n0,
+                            int32_t *__restrict__ po) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
     unsigned long long kth = 0;
     int need = Nprime;
@@ -334,7 +336,7 @@ __device__ void select_pool(NNSmem &s, int c, int Nprime, int n0, int32_t *__res
         __syncthreads();
         const unsigned long long hm = (sh == 56) ? 0ull : (~0ull << (sh + 8));
         for (int t = tid; t < c; t += blockDim.x)
-            if ((s.key[t] & hm) == kth) atomicAdd(&s.hist[(s.key[t] >> sh) & 255u], 1u);
+            if ((K[t] & hm) == kth) atomicAdd(&s.hist[(K[t] >> sh) & 255u], 1u);
         __syncthreads();
         if (tid < 32) warp_pick_bin(s.hist, need, s.misc);  // misc[2] = elements sharing this prefix
         __syncthreads();
@@ -350,8 +352,7 @@ __device__ void select_pool(NNSmem &s, int c, int Nprime, int n0, int32_t *__res
             __syncthreads();
             const unsigned hm = (sh == 24) ? 0u : (~0u << (sh + 8));
             for (int t = tid; t < c; t += blockDim.x)
-                if (s.key[t] == kth && ((unsigned)s.idx[t] & hm) == ip)
-                    atomicAdd(&s.hist[((unsigned)s.idx[t] >> sh) & 255u], 1u);
+                if (K[t] == kth && ((unsigned)I[t] & hm) == ip) atomicAdd(&s.hist[((unsigned)I[t] >> sh) & 255u], 1u);
             __syncthreads();
             if (tid < 32) warp_pick_bin(s.hist, need, s.misc);
             __syncthreads();
@@ -363,8 +364,8 @@ __device__ void select_pool(NNSmem &s, int c, int Nprime, int n0, int32_t *__res
     }
     // mark members: idx >= 0 in, set bit 31 for non-members / taken ones
     for (int t = tid; t < c; t += blockDim.x) {
-        const bool in = kv_less(s.key[t], s.idx[t], kth, ith) || (s.key[t] == kth && s.idx[t] == ith);
-        if (!in) s.idx[t] |= (int)0x80000000;
+        const bool in = kv_less(K[t], I[t], kth, ith) || (K[t] == kth && I[t] == ith);
+        if (!in) I[t] |= (int)0x80000000;
     }
     __syncthreads();
     // n0 smallest in ascending (key, idx) order
@@ -372,7 +373,7 @@ __device__ void select_pool(NNSmem &s, int c, int Nprime, int n0, int32_t *__res
         unsigned long long bk = ~0ull;
         int bi = 0x7fffffff, bt = -1;
         for (int t = tid; t < c; t += blockDim.x)
-            if (s.idx[t] >= 0 && kv_less(s.key[t], s.idx[t], bk, bi)) { bk = s.key[t]; bi = s.idx[t]; bt = t; }
+            if (I[t] >= 0 && kv_less(K[t], I[t], bk, bi)) { bk = K[t]; bi = I[t]; bt = t; }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, off);
@@ -388,7 +389,7 @@ __device__ void select_pool(NNSmem &s, int c, int Nprime, int n0, int32_t *__res
             for (int w = 1; w < nw; w++)
                 if (kv_less(s.redk[w], s.redi[w], k0, i0)) { k0 = s.redk[w]; i0 = s.redi[w]; t0 = s.scan[w]; }
             po[r] = i0;
-            s.idx[t0] |= (int)0x80000000;
+            I[t0] |= (int)0x80000000;
         }
         __syncthreads();
     }
@@ -396,7 +397,7 @@ __device__ void select_pool(NNSmem &s, int c, int Nprime, int n0, int32_t *__res
     if (tid == 0) s.misc[3] = n0;
     __syncthreads();
     for (int t = tid; t < c; t += blockDim.x)
-        if (s.idx[t] >= 0) po[atomicAdd(&s.misc[3], 1)] = s.idx[t];
+        if (I[t] >= 0) po[atomicAdd(&s.misc[3], 1)] = I[t];
     __syncthreads();
 }
 
@@ -644,19 +645,21 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
         for (int q = 0; q < nq; q++) {
             int c;
             int32_t *po = pool_out + (q0 + q) * (int64_t)Nprime;
+            uint64_t *qk = bufk + (size_t)q * bufcap;
+            int32_t *qi = bufi + (size_t)q * bufcap;
             if (s.state[q] == 2) {
                 if (tid == 0) atomicAdd(fallback_count, 1);
-                nn_exact_select<P>(s, X, N, p, q, Nprime);
+                nn_exact_select<P>(s, X, N, p, q, Nprime, qk, qi);
                 c = Nprime;
             } else {
                 c = s.cnt[q];
-                for (int t = tid; t < c; t += blockDim.x) {
-                    s.key[t] = bufk[q * bufcap + t];
-                    s.idx[t] = bufi[q * bufcap + t];
-                }
             }
             __syncthreads();
-            if (sorted) {
+            if (sorted) {  // c <= NN_CAP here (bufcap is capped for the sorted output)
+                for (int t = tid; t < c; t += blockDim.x) {
+                    s.key[t] = qk[t];
+                    s.idx[t] = qi[t];
+                }
                 int npow = 1;
                 while (npow < c) npow <<= 1;
                 for (int t = c + tid; t < npow; t += blockDim.x) {
@@ -671,7 +674,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 }
                 __syncthreads();
             } else {
-                select_pool(s, c, Nprime, n0, po);
+                select_pool(s, qk, qi, c, Nprime, n0, po);  // in the query's global buffer
             }
         }
     }
@@ -680,16 +683,17 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
 size_t nn_smem_bytes() { return sizeof(NNSmem); }
 
 // per-query global survivor buffer: enough for ~1.5 N' plus sampling noise
-static int nn_bufcap(int Nprime) {
+// (capped at the shared-memory sort capacity when the sorted pool is requested)
+static int nn_bufcap(int Nprime, bool sorted) {
     int c = 3 * Nprime;
     if (c < 2048) c = 2048;
-    if (c > NN_CAP) c = NN_CAP;
+    if (sorted && c > NN_CAP) c = NN_CAP;
     return c;
 }
 
 // Workspace layout: [maxn2 bits (256 B)] [X32: N*p floats] [sample] [survivor keys] [survivor idx]
-size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime) {
-    const size_t bc = (size_t)nn_bufcap(Nprime);
+size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime, bool sorted) {
+    const size_t bc = (size_t)nn_bufcap(Nprime, sorted);
     return 256 + (((size_t)N * p * sizeof(float) + 255) & ~(size_t)255) + (((size_t)N * sizeof(float) + 255) & ~(size_t)255) +
            (size_t)grid * NN_Q * (NN_SAMPLE * sizeof(float) + bc * (sizeof(uint64_t) + sizeof(int32_t))) + 256;
 }
@@ -702,7 +706,7 @@ static cudaError_t launch_nn_t(const double *X, const float *X32, const float *r
     size_t smem = sizeof(NNSmem);
     cudaError_t e = cudaFuncSetAttribute(nn_pool_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int bc = nn_bufcap(Nprime);
+    const int bc = nn_bufcap(Nprime, sorted != 0);
     float *samp = (float *)w;
     w += (size_t)grid * NN_Q * NN_SAMPLE * sizeof(float);
     uint64_t *bk = (uint64_t *)w;
@@ -713,9 +717,13 @@ static cudaError_t launch_nn_t(const double *X, const float *X32, const float *r
     return cudaGetLastError();
 }
 
-int nn_grid(int64_t M, int num_sms) {
+int nn_grid(int64_t M, int num_sms, int Nprime) {
     int64_t groups = (M + NN_Q - 1) / NN_Q;
     int64_t g = 2LL * num_sms;  // 2 CTAs/SM fit (~110 KB smem each)
+    // keep the survivor buffers under ~2 GiB for large pools
+    const int64_t per_cta = (int64_t)NN_Q * nn_bufcap(Nprime, false) * 12;
+    const int64_t gmax = ((int64_t)2 << 30) / per_cta;
+    if (g > gmax) g = gmax > 1 ? gmax : 1;
     return (int)(groups < g ? (groups > 0 ? groups : 1) : g);
 }
 

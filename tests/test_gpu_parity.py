@@ -163,6 +163,24 @@ def test_alc_batch_vs_oracle(torch_dev, lagp, name, M, N, over, form):
 FORMS = ["explicit", "explicit_dfma", "incremental"]
 
 
+@pytest.mark.parametrize("form", ["explicit", "explicit_dfma"])
+def test_large_pool_explicit(torch_dev, lagp, form):
+    """N' > 8192 (C5's large pools): NN selection in the global survivor buffers
+    and the explicit forms with kappa/chosen in the global slab."""
+    torch, dev = torch_dev
+    cfg = make_config("C5_2d", M=3, Nprime=12000, n=20)
+    g, o = run_both(torch, dev, lagp, cfg, form=form)
+    compare(g, o, cfg["n0"], float(np.std(cfg["Z"])), tau_for(2))
+
+
+def test_incremental_rejects_large_pool(torch_dev, lagp):
+    torch, dev = torch_dev
+    cfg = make_config("C5_2d", M=2, Nprime=9000, n=20)
+    with pytest.raises(lagp.LagpError, match="incremental"):
+        lagp.alc_batch(T(torch, dev, cfg["X"]), T(torch, dev, cfg["Z"]), T(torch, dev, cfg["XX"]), cfg["d"], cfg["g"],
+                       cfg["n0"], cfg["n"], cfg["Nprime"], form="incremental")
+
+
 @pytest.mark.parametrize("form", FORMS)
 def test_full_gp_special_case(torch_dev, lagp, form):
     """n = N' = N: the local design is all of X; prediction equals Eq (1)-(2)."""
