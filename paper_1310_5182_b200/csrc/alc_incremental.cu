@@ -44,12 +44,12 @@ constexpr int INC_THREADS = 1024;
 struct IncShared {
     double xstar[LAGP_PMAX];
     double xq[LAGP_PMAX];
-    double rho, rrho, znew, ystar;
-    uint32_t fl;
+    double rrho, znew, ystar;
 };
 
-// smem (doubles): wsm S*Npad | wstar n4 | ytil n4 | zv n4 | zc Npad | red 160
+// smem (doubles): wsm S*Npad | wst 2*n4 | ytil n4 | zv n4 | zc Npad | red 200
 __host__ __device__ inline int inc_n4(int n) { return (n + 3) & ~3; }
+__host__ __device__ inline int inc_wl(int n, int R) { return inc_n4(n > R ? n : R); }
 
 template <int R, int P, int CPT>
 __global__ void __launch_bounds__(INC_THREADS, 1)
@@ -57,13 +57,16 @@ alc_incremental_kernel(AlcArgs A, int S) {
     extern __shared__ __align__(16) double sm[];
     const int n = A.n, Np = A.Nprime, Npad = A.Npad, n0 = A.n0;
     const int p = P ? P : A.p;
-    double *wsm = sm;
-    double *wstar = wsm + (size_t)S * Npad;
-    double *ytil = wstar + inc_n4(n);
-    double *zv = ytil + inc_n4(n);
-    double *zc = zv + inc_n4(n);  // Z of the pool candidates (y* without an HBM round trip)
-    double *red = zc + Npad;
-    __shared__ IncShared sh;
+    const int n4 = inc_n4(n);
+    double *wsm = sm;                        // S x Npad: entries [R, R+S) of every w_c
+    const int wl = inc_wl(n, R);             // publish slot length: covers n and R entries
+    double *wst = wsm + (size_t)S * Npad;    // 2 x wl: the winner's register entries (by step parity)
+    double *ytil = wst + 2 * wl;
+    double *zv = ytil + n4;
+    double *zc = zv + n4;                    // Z of the pool candidates (y* without an HBM round trip)
+    double *red = zc + Npad;                 // 200 doubles: double-buffered argmax scratch
+    __shared__ IncShared sh[2];              // publish slots by step parity
+    __shared__ uint32_t fl;
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     double *gw = A.cache + (size_t)blockIdx.x * A.cache_stride;  // entries >= R+S: gw[(a-R-S)*Npad + c]
@@ -75,9 +78,9 @@ alc_incremental_kernel(AlcArgs A, int S) {
     for (int64_t xi = blockIdx.x; xi < A.M; xi += gridDim.x) {
         const int32_t *pool = A.pool + xi * (int64_t)Np;
         int32_t *idx = A.idx_out + xi * (int64_t)n;
-        if (tid < p) sh.xq[tid] = A.XX[xi * p + tid];
-        if (tid == 0) sh.fl = 0;
-        for (int t = tid; t < n; t += blockDim.x) wstar[t] = 0.0;
+        if (tid < p) sh[0].xq[tid] = A.XX[xi * p + tid];
+        if (tid == 0) fl = 0;
+        for (int t = tid; t < 2 * wl; t += blockDim.x) wst[t] = 0.0;
         if (A.gap_out)
             for (int t = tid; t < G; t += blockDim.x) A.gap_out[xi * G + t] = __longlong_as_double(0x7ff8000000000000LL);
         for (int t = tid; t < n; t += blockDim.x) idx[t] = (t < n0) ? pool[t] : -1;
@@ -100,14 +103,14 @@ alc_incremental_kernel(AlcArgs A, int S) {
 #pragma unroll
                 for (int k = 0; k < (P ? P : 1); k++) {
                     xc[q][k] = valid[q] ? A.X[(int64_t)gidx[q] * p + k] : 0.0;
-                    double diff = __dsub_rn(xc[q][k], sh.xq[k]);
+                    double diff = __dsub_rn(xc[q][k], sh[0].xq[k]);
                     d2 = __fma_rn(diff, diff, d2);
                 }
             } else if (valid[q]) {
                 for (int k = 0; k < p; k++) {
                     const double v = A.X[(int64_t)gidx[q] * p + k];
                     coords[k * Npad + c] = v;
-                    double diff = __dsub_rn(v, sh.xq[k]);
+                    double diff = __dsub_rn(v, sh[0].xq[k]);
                     d2 = __fma_rn(diff, diff, d2);
                 }
             }
@@ -119,8 +122,12 @@ alc_incremental_kernel(AlcArgs A, int S) {
         }
         __syncthreads();
 
+        // Three barriers per step: two in the argmax, one after the publish. The
+        // publish slots and the argmax scratch alternate by step parity, so a slot
+        // is rewritten only after every thread has passed the next step's barriers.
         int j = 0;  // current design size
         for (; j < n; j++) {
+            const int par = j & 1;
             int cstar;
             if (j < n0) {
                 cstar = j;  // forced NN append (a2), pool order = NN order
@@ -149,56 +156,60 @@ alc_incremental_kernel(AlcArgs A, int S) {
                         }
                     }
                 }
-                if (__any_sync(0xffffffffu, sentinel) && lane == 0) atomicOr(&sh.fl, (uint32_t)LAGP_FLAG_SENTINEL);
-                if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(&sh.fl, (uint32_t)LAGP_FLAG_NONFINITE);
-                const ArgTop best = block_argtop(bd1, bi, bd2, bp, red);
+                if (__any_sync(0xffffffffu, sentinel) && lane == 0) atomicOr(&fl, (uint32_t)LAGP_FLAG_SENTINEL);
+                if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(&fl, (uint32_t)LAGP_FLAG_NONFINITE);
+                const ArgTop best = block_argtop_db(bd1, bi, bd2, bp, red, par);
                 if (best.i1 < 0) {
-                    if (tid == 0) sh.fl |= LAGP_FLAG_EXHAUSTED;
+                    if (tid == 0) fl |= LAGP_FLAG_EXHAUSTED;
                     break;
                 }
                 cstar = best.pos;
                 if (tid == 0) {
                     const double gap = top2_gap(best.d1, best.d2);
-                    if (!(best.d1 > 0.0) || gap < kTieGap) sh.fl |= LAGP_FLAG_NEAR_TIE;
+                    if (!(best.d1 > 0.0) || gap < kTieGap) fl |= LAGP_FLAG_NEAR_TIE;
                     if (A.gap_out) A.gap_out[xi * G + (j - n0)] = gap;
                     idx[j] = best.i1;
                 }
             }
-            // ---- a4 on the factor: publish w_{c*}, x*, rho, z_new, y*
+            // ---- a4 on the factor: the owner publishes its register entries, x*, 1/rho,
+            // z_new, y*; the winner's shared/HBM entries are read in place by everyone
+            IncShared &pb = sh[par];
+            double *ws = wst + par * wl;
             const int owner = cstar % INC_THREADS, oq = cstar / INC_THREADS;
             if (tid == owner) {
 #pragma unroll
                 for (int q = 0; q < CPT; q++) {
                     if (q == oq) {
 #pragma unroll
-                        for (int a = 0; a < R; a++)
-                            if (a < j) wstar[a] = wr[q][a];
+                        for (int a = 0; a < R; a++) ws[a] = (a < j) ? wr[q][a] : 0.0;
                         if (P) {
 #pragma unroll
-                            for (int k = 0; k < (P ? P : 1); k++) sh.xstar[k] = xc[q][k];
+                            for (int k = 0; k < (P ? P : 1); k++) pb.xstar[k] = xc[q][k];
                         }
                         const double rho = sqrt(s[q]);
-                        sh.rho = rho;
-                        sh.rrho = 1.0 / rho;
-                        sh.znew = cov[q] / rho;
-                        sh.ystar = zc[cstar];
+                        pb.rrho = 1.0 / rho;
+                        pb.znew = cov[q] / rho;
+                        pb.ystar = zc[cstar];
                         chosen[q] = true;
-                        if (!(s[q] > 0.0)) atomicOr(&sh.fl, (uint32_t)LAGP_FLAG_NONFINITE);
+                        if (!(s[q] > 0.0)) atomicOr(&fl, (uint32_t)LAGP_FLAG_NONFINITE);
                     }
                 }
             }
-            if (!P && tid < p) sh.xstar[tid] = coords[tid * Npad + cstar];
-            for (int a = R + tid; a < j; a += blockDim.x)
-                wstar[a] = (a < RS) ? wsm[(size_t)(a - R) * Npad + cstar] : gw[(size_t)(a - RS) * Npad + cstar];
+            if (!P && tid < p) pb.xstar[tid] = coords[tid * Npad + cstar];
             __syncthreads();
-            const double rrho = sh.rrho, znew = sh.znew;
+            const double rrho = pb.rrho, znew = pb.znew;
+            const double *wcs = wsm + cstar;  // winner's column, entry a at wcs[(a - R) * Npad]
+            const double *wcg = gw + cstar;   // ... and in the slab, entry a at wcg[(a - RS) * Npad]
             if (wid == 0) {  // a5 state: y~_j = (y* - w*^T y~) / rho, z_j = z_new
                 double acc = 0.0;
-                for (int a = lane; a < j; a += 32) acc = fma(wstar[a], ytil[a], acc);
+                for (int a = lane; a < j; a += 32) {
+                    const double wa = a < R ? ws[a] : (a < RS ? wcs[(size_t)(a - R) * Npad] : wcg[(size_t)(a - RS) * Npad]);
+                    acc = fma(wa, ytil[a], acc);
+                }
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
                 if (lane == 0) {
-                    ytil[j] = (sh.ystar - acc) * rrho;
+                    ytil[j] = (pb.ystar - acc) * rrho;
                     zv[j] = znew;
                 }
             }
@@ -207,51 +218,48 @@ alc_incremental_kernel(AlcArgs A, int S) {
             for (int q = 0; q < CPT; q++) {
                 const int c = tid + q * INC_THREADS;
                 if (!valid[q]) continue;
-                // issue the HBM-slab loads first (independent, latency overlapped)
+                // HBM-slab entries first (independent loads, latency overlapped)
                 double acc2 = 0.0, acc3 = 0.0;
-                for (int a = RS; a < j; a += 4) {
+                for (int a = RS; a < j; a += 2) {
+                    const bool two = a + 1 < j;
                     const double g0 = gw[(size_t)(a - RS) * Npad + c];
-                    const double g1 = a + 1 < j ? gw[(size_t)(a + 1 - RS) * Npad + c] : 0.0;
-                    const double g2 = a + 2 < j ? gw[(size_t)(a + 2 - RS) * Npad + c] : 0.0;
-                    const double g3 = a + 3 < j ? gw[(size_t)(a + 3 - RS) * Npad + c] : 0.0;
-                    acc2 = fma(wstar[a], g0, acc2);
-                    acc3 = fma(a + 1 < j ? wstar[a + 1] : 0.0, g1, acc3);
-                    acc2 = fma(a + 2 < j ? wstar[a + 2] : 0.0, g2, acc2);
-                    acc3 = fma(a + 3 < j ? wstar[a + 3] : 0.0, g3, acc3);
+                    const double g1 = two ? gw[(size_t)(a + 1 - RS) * Npad + c] : 0.0;
+                    const double h0 = wcg[(size_t)(a - RS) * Npad];
+                    const double h1 = two ? wcg[(size_t)(a + 1 - RS) * Npad] : 0.0;
+                    acc2 = fma(h0, g0, acc2);
+                    acc3 = fma(h1, g1, acc3);
                 }
                 double d2 = 0.0;
                 if (P) {
 #pragma unroll
                     for (int k = 0; k < (P ? P : 1); k++) {
-                        double diff = __dsub_rn(xc[q][k], sh.xstar[k]);
+                        double diff = __dsub_rn(xc[q][k], pb.xstar[k]);
                         d2 = __fma_rn(diff, diff, d2);
                     }
                 } else {
                     for (int k = 0; k < p; k++) {
-                        double diff = __dsub_rn(coords[k * Npad + c], sh.xstar[k]);
+                        double diff = __dsub_rn(coords[k * Npad + c], pb.xstar[k]);
                         d2 = __fma_rn(diff, diff, d2);
                     }
                 }
                 double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
-                for (int a = 0; a < R; a += 2) {  // R even; wstar[a >= j] = 0, wr[a >= j] = 0
-                    const double2 ws = reinterpret_cast<const double2 *>(wstar)[a >> 1];
-                    acc0 = fma(ws.x, wr[q][a], acc0);
-                    acc1 = fma(ws.y, wr[q][a + 1], acc1);
+                for (int a = 0; a < R; a += 2) {  // R even; ws[a >= j] = 0 and wr[a >= j] = 0
+                    const double2 w2 = reinterpret_cast<const double2 *>(ws)[a >> 1];
+                    acc0 = fma(w2.x, wr[q][a], acc0);
+                    acc1 = fma(w2.y, wr[q][a + 1], acc1);
                 }
                 const int jr = j < RS ? j : RS;
-                const double *wp = wsm + c;  // column of this candidate, entry a at wp[(a - R) * Npad]
+                const double *wp = wsm + c;  // this candidate's column
                 int a = R;
-                for (; a + 3 < jr; a += 4) {  // R even -> a even: wstar pairs are 16-byte aligned
-                    const double2 s01 = *reinterpret_cast<const double2 *>(wstar + a);
-                    const double2 s23 = *reinterpret_cast<const double2 *>(wstar + a + 2);
-                    const double *q0 = wp + (size_t)(a - R) * Npad;
-                    acc0 = fma(s01.x, q0[0], acc0);
-                    acc1 = fma(s01.y, q0[Npad], acc1);
-                    acc0 = fma(s23.x, q0[2 * Npad], acc0);
-                    acc1 = fma(s23.y, q0[3 * Npad], acc1);
+                for (; a + 3 < jr; a += 4) {
+                    const size_t o = (size_t)(a - R) * Npad;
+                    acc0 = fma(wcs[o], wp[o], acc0);
+                    acc1 = fma(wcs[o + Npad], wp[o + Npad], acc1);
+                    acc0 = fma(wcs[o + 2 * Npad], wp[o + 2 * Npad], acc0);
+                    acc1 = fma(wcs[o + 3 * Npad], wp[o + 3 * Npad], acc1);
                 }
-                for (; a < jr; a++) acc0 = fma(wstar[a], wp[(size_t)(a - R) * Npad], acc0);
+                for (; a < jr; a++) acc0 = fma(wcs[(size_t)(a - R) * Npad], wp[(size_t)(a - R) * Npad], acc0);
                 const double e = corr_from_d2(d2, rth) - ((acc0 + acc1) + (acc2 + acc3));
                 const double wn = e * rrho;
                 if (j < R) {
@@ -266,7 +274,6 @@ alc_incremental_kernel(AlcArgs A, int S) {
                 s[q] = fma(-wn, wn, s[q]);
                 cov[q] = fma(-znew, wn, cov[q]);
             }
-            __syncthreads();  // wstar / sh / ytil reused next step
         }
 
         // ---- a5: mean = z^T y~, psi = ||y~||^2, s2 = psi (1 + eta - ||z||^2) / j
@@ -287,7 +294,7 @@ alc_incremental_kernel(AlcArgs A, int S) {
             if (lane == 0) {
                 const double sc = psi * (1.0 + eta - zz) / (double)j;
                 const double vr = j > 2 ? sc * (double)j / (double)(j - 2) : __longlong_as_double(0x7ff8000000000000LL);
-                uint32_t f = sh.fl;
+                uint32_t f = fl;
                 if (!isfinite(mu) || !isfinite(sc)) f |= LAGP_FLAG_NONFINITE;
                 A.mean[xi] = mu;
                 A.s2[xi] = sc;
@@ -326,7 +333,7 @@ IncPlan inc_plan(int n, int p, int Nprime, int Npad, size_t smem_optin) {
         return pl;
     }
     pl.R = inc_R(p, pl.cpt);
-    const size_t fixed = ((size_t)inc_n4(n) * 3 + Npad + 160) * sizeof(double);
+    const size_t fixed = ((size_t)inc_n4(n) * 2 + 2 * (size_t)inc_wl(n, pl.R) + Npad + 200) * sizeof(double);
     size_t avail = smem_optin > fixed + 1024 ? smem_optin - fixed - 1024 : 0;
     int S = (int)(avail / ((size_t)Npad * sizeof(double)));
     const int need = n - pl.R > 0 ? n - pl.R : 0;

@@ -142,6 +142,51 @@ __device__ __forceinline__ ArgTop block_argtop(double d1, int i1, double d2, int
     return r;
 }
 
+// block_argtop with the scratch double-buffered by `parity` (alternate calls
+// must alternate parity) and no trailing barrier: two __syncthreads instead of
+// three. `scratch` >= 200 doubles. Safe when at least one other barrier
+// separates two calls with the same parity.
+__device__ __forceinline__ ArgTop block_argtop_db(double d1, int i1, double d2, int pos, double *scratch,
+                                                  int parity) {
+    unsigned long long k1 = (unsigned long long)__double_as_longlong(d1 > 0.0 ? d1 : 0.0);
+    unsigned long long k2 = (unsigned long long)__double_as_longlong(d2 > 0.0 ? d2 : 0.0);
+    unsigned ii = (unsigned)i1;
+    warp_argtop(k1, ii, k2, pos);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long *sk = reinterpret_cast<unsigned long long *>(scratch) + parity * 100;
+    if (lane == 0) {
+        sk[3 * wid + 0] = k1;
+        sk[3 * wid + 1] = ((unsigned long long)(unsigned)pos << 32) | ii;
+        sk[3 * wid + 2] = k2;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        unsigned long long a1 = 0, a2 = 0;
+        unsigned ai = 0xffffffffu;
+        int ap = -1;
+        if (lane < nw) {
+            a1 = sk[3 * lane + 0];
+            ai = (unsigned)sk[3 * lane + 1];
+            ap = (int)(unsigned)(sk[3 * lane + 1] >> 32);
+            a2 = sk[3 * lane + 2];
+        }
+        warp_argtop(a1, ai, a2, ap);
+        if (lane == 0) {
+            sk[96] = a1;
+            sk[97] = ((unsigned long long)(unsigned)ap << 32) | ai;
+            sk[98] = a2;
+        }
+    }
+    __syncthreads();
+    ArgTop r;
+    r.d1 = __longlong_as_double((long long)sk[96]);
+    r.i1 = (int)(unsigned)sk[97];
+    r.pos = (int)(unsigned)(sk[97] >> 32);
+    r.d2 = __longlong_as_double((long long)sk[98]);
+    return r;
+}
+
 // Partitioned-inverse append (a4; Eq (6)): given the
 // explicit K_j^{-1} in Kinv (leading dimension ld, symmetric), k = k_j(x_new)
 // and kdiag = K(x_new,x_new) + eta, overwrite Kinv with K_{j+1}^{-1}:
