@@ -84,6 +84,9 @@ alc_incremental_kernel(AlcArgs A, int S) {
         if (A.gap_out)
             for (int t = tid; t < G; t += blockDim.x) A.gap_out[xi * G + t] = __longlong_as_double(0x7ff8000000000000LL);
         for (int t = tid; t < n; t += blockDim.x) idx[t] = (t < n0) ? pool[t] : -1;
+        // shared entries not yet appended read as 0, so the dot below runs in
+        // whole groups of 4 (S is a multiple of 4)
+        for (int t = tid; t < S * Npad; t += blockDim.x) wsm[t] = 0.0;
         __syncthreads();
 
         // ---- per-candidate state
@@ -203,7 +206,7 @@ alc_incremental_kernel(AlcArgs A, int S) {
             if (wid == 0) {  // a5 state: y~_j = (y* - w*^T y~) / rho, z_j = z_new
                 double acc = 0.0;
                 for (int a = lane; a < j; a += 32) {
-                    const double wa = a < R ? ws[a] : (a < RS ? wcs[(size_t)(a - R) * Npad] : wcg[(size_t)(a - RS) * Npad]);
+                    const double wa = a < R ? ws[a] : (a < RS ? wcs[(a - R) * Npad] : wcg[(a - RS) * Npad]);
                     acc = fma(wa, ytil[a], acc);
                 }
 #pragma unroll
@@ -222,10 +225,10 @@ alc_incremental_kernel(AlcArgs A, int S) {
                 double acc2 = 0.0, acc3 = 0.0;
                 for (int a = RS; a < j; a += 2) {
                     const bool two = a + 1 < j;
-                    const double g0 = gw[(size_t)(a - RS) * Npad + c];
-                    const double g1 = two ? gw[(size_t)(a + 1 - RS) * Npad + c] : 0.0;
-                    const double h0 = wcg[(size_t)(a - RS) * Npad];
-                    const double h1 = two ? wcg[(size_t)(a + 1 - RS) * Npad] : 0.0;
+                    const double g0 = gw[(a - RS) * Npad + c];
+                    const double g1 = two ? gw[(a + 1 - RS) * Npad + c] : 0.0;
+                    const double h0 = wcg[(a - RS) * Npad];
+                    const double h1 = two ? wcg[(a + 1 - RS) * Npad] : 0.0;
                     acc2 = fma(h0, g0, acc2);
                     acc3 = fma(h1, g1, acc3);
                 }
@@ -249,27 +252,29 @@ alc_incremental_kernel(AlcArgs A, int S) {
                     acc0 = fma(w2.x, wr[q][a], acc0);
                     acc1 = fma(w2.y, wr[q][a + 1], acc1);
                 }
-                const int jr = j < RS ? j : RS;
+                // shared entries [R, min(j, R+S)) rounded up to 4: rows >= j are still 0 in
+                // every column read here (the winner's included: chosen columns are frozen)
+                const int e4 = (j < RS ? j - R + 3 : S) & ~3;
                 const double *wp = wsm + c;  // this candidate's column
-                int a = R;
-                for (; a + 3 < jr; a += 4) {
-                    const size_t o = (size_t)(a - R) * Npad;
+                for (int o = 0; o < e4 * Npad; o += 4 * Npad) {  // shared offsets fit 32 bits
                     acc0 = fma(wcs[o], wp[o], acc0);
                     acc1 = fma(wcs[o + Npad], wp[o + Npad], acc1);
                     acc0 = fma(wcs[o + 2 * Npad], wp[o + 2 * Npad], acc0);
                     acc1 = fma(wcs[o + 3 * Npad], wp[o + 3 * Npad], acc1);
                 }
-                for (; a < jr; a++) acc0 = fma(wcs[(size_t)(a - R) * Npad], wp[(size_t)(a - R) * Npad], acc0);
                 const double e = corr_from_d2(d2, rth) - ((acc0 + acc1) + (acc2 + acc3));
                 const double wn = e * rrho;
                 if (j < R) {
 #pragma unroll
                     for (int b = 0; b < R; b++)
                         if (b == j) wr[q][b] = wn;
+                } else if (chosen[q]) {
+                    // a chosen column is never read after its own step: keep its rows >= j
+                    // at 0 so the padded dot above sees no write from this step
                 } else if (j < RS) {
-                    wsm[(size_t)(j - R) * Npad + c] = wn;
+                    wsm[(j - R) * Npad + c] = wn;
                 } else {
-                    gw[(size_t)(j - RS) * Npad + c] = wn;
+                    gw[(j - RS) * Npad + c] = wn;
                 }
                 s[q] = fma(-wn, wn, s[q]);
                 cov[q] = fma(-znew, wn, cov[q]);
@@ -337,7 +342,8 @@ IncPlan inc_plan(int n, int p, int Nprime, int Npad, size_t smem_optin) {
     size_t avail = smem_optin > fixed + 1024 ? smem_optin - fixed - 1024 : 0;
     int S = (int)(avail / ((size_t)Npad * sizeof(double)));
     const int need = n - pl.R > 0 ? n - pl.R : 0;
-    if (S > need) S = need;
+    if (S > inc_n4(need)) S = inc_n4(need);
+    S &= ~3;  // the shared dot runs in groups of 4 entries
     if (S < 0) S = 0;
     pl.S = S;
     pl.wsz = S * Npad;

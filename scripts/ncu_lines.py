@@ -1,6 +1,6 @@
 """Attribute ncu per-SASS stall samples to source lines (run here, no GPU).
 
-    python scripts/ncu_lines.py <report.ncu-rep> <cubin-basename-in-lib> <kernel-substring> [top]
+    python scripts/ncu_lines.py <report.ncu-rep> <cubin-basename-in-lib> <kernel-substring> [top] [inst]
 
 The cubin is extracted from paper_1310_5182_b200/liblagp_b200.so (cuobjdump
 -xelf) and disassembled with nvdisasm -g (line info); the profile's SASS rows
@@ -17,6 +17,7 @@ import tempfile
 
 rep, cub, kname = sys.argv[1], sys.argv[2], sys.argv[3]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 25
+by_inst = len(sys.argv) > 5 and sys.argv[5] == "inst"  # rank by warp instructions executed
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.join(ROOT, "paper_1310_5182_b200", "liblagp_b200.so")], cwd=tmp,
@@ -40,6 +41,7 @@ hdr = next(r for r in rows if r and r[0] == "Address")
 data = rows[rows.index(hdr) + 1:]
 iA, iW = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)")
 iX = hdr.index("L1 Wavefronts Shared Excessive")
+iI = hdr.index("Instructions Executed")
 base = int(data[0][iA], 16)
 agg = collections.Counter()
 exc = collections.Counter()
@@ -49,7 +51,7 @@ for r in data:
     except ValueError:
         continue
     key = lines.get(off, ("?", 0))
-    agg[key] += int(r[iW] or 0)
+    agg[key] += int(r[iI] or 0) if by_inst else int(r[iW] or 0)
     exc[key] += int(r[iX] or 0)
 tot = sum(agg.values()) or 1
 src = {}
