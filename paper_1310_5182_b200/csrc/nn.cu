@@ -48,6 +48,8 @@ struct NNSmem {
     int redi[NN_THREADS / 32];
     int scan[NN_THREADS / 32];
     int misc[4];
+    unsigned long long n0k[LAGP_NMAX];  // the n0 nearest (select_pool)
+    int n0i[LAGP_NMAX];
 };
 
 __device__ __forceinline__ bool key_less(uint64_t ka, int ia, uint64_t kb, int ib) {
@@ -318,86 +320,143 @@ __device__ __forceinline__ bool kv_less(unsigned long long ka, int ia, unsigned 
     return ka < kb || (ka == kb && ia < ib);
 }
 
-// Exact selection of the Nprime smallest (key, idx) of the c survivors held in
-// s.key/s.idx[0..c): radix select of the Nprime-th composite value (8 key
-// digits, then 4 index digits only if the key is tied), then the n0 smallest in
-// ascending order by n0 block-argmin rounds (pool[0..n0) = X_{n0}(x) in NN
-// order), then the rest compacted in any order (positions >= n0 never affect
-// results: every candidate's score and the (Delta, index) argmax are
-// order-independent).
-// K/I may be shared or global memory (large pools select in the global buffers).
-__device__ void select_pool(NNSmem &s, uint64_t *K, int32_t *I, int c, int Nprime, int n0,
-                            int32_t *__restrict__ po) {
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-    unsigned long long kth = 0;
-    int need = Nprime;
-    for (int sh = 56; sh >= 0; sh -= 8) {
+// Radix select over the live entries of K/I[0..c) (K != ~0): the composite
+// (kth, ith) of the rank-th smallest (key, idx) (1-based), so that an entry is
+// among the `rank` smallest iff (K, I) <= (kth, ith). The digits start below the
+// bits shared by every live key (kmin/kmax), 8 bits at a time, and stop as soon
+// as the bucket holding the target is taken whole (then ith = INT_MAX and kth
+// has all lower bits set); only a fully tied key goes on to index digits.
+// Histogram increments are aggregated per warp (match.any): the leading digits
+// of nearby d^2 values collide heavily.
+__device__ void radix_select_kv(NNSmem &s, const uint64_t *K, const int32_t *I, int c, int rank, uint64_t kmin,
+                                uint64_t kmax, unsigned long long &kth_out, int &ith_out) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint64_t diff = kmin ^ kmax;
+    int sh = diff ? 64 - __clzll((long long)diff) : 0;  // bits [sh, 64) are common to all live keys
+    unsigned long long prefix = sh >= 64 ? 0ull : (kmin & (~0ull << sh));
+    int need = rank, cnt = c;
+    bool whole = false;
+    while (sh > 0) {
+        const int w = sh >= 8 ? 8 : sh;
+        const int lo = sh - w;
         for (int b = tid; b < 256; b += blockDim.x) s.hist[b] = 0;
         __syncthreads();
-        const unsigned long long hm = (sh == 56) ? 0ull : (~0ull << (sh + 8));
-        for (int t = tid; t < c; t += blockDim.x)
-            if ((K[t] & hm) == kth) atomicAdd(&s.hist[(K[t] >> sh) & 255u], 1u);
+        const unsigned long long hm = sh >= 64 ? 0ull : (~0ull << sh);
+        for (int base = tid - lane; base < c; base += blockDim.x) {
+            const int t = base + lane;
+            const unsigned long long k = t < c ? K[t] : ~0ull;
+            const bool live = k != ~0ull && (k & hm) == prefix;
+            const unsigned bin = live ? (unsigned)((k >> lo) & ((1u << w) - 1u)) : 0x100u;
+            const unsigned m = __match_any_sync(0xffffffffu, bin);
+            if (live && (__ffs(m) - 1) == lane) atomicAdd(&s.hist[bin], (unsigned)__popc(m));
+        }
         __syncthreads();
-        if (tid < 32) warp_pick_bin(s.hist, need, s.misc);  // misc[2] = elements sharing this prefix
+        if (tid < 32) warp_pick_bin(s.hist, need, s.misc);
         __syncthreads();
-        kth |= ((unsigned long long)s.misc[0]) << sh;
+        prefix |= ((unsigned long long)s.misc[0]) << lo;
         need = s.misc[1];
+        cnt = s.misc[2];
+        sh = lo;
         __syncthreads();
+        if (cnt == need) {  // the whole bucket is in
+            whole = true;
+            break;
+        }
     }
-    int ith = 0x7fffffff;  // composite tie break on the index
-    if (s.misc[2] > need) {
+    int ith = 0x7fffffff;
+    if (whole) {
+        prefix |= sh > 0 ? ((1ull << sh) - 1ull) : 0ull;
+    } else if (cnt > need) {  // the target key is tied: select on the index
         unsigned ip = 0;
-        for (int sh = 24; sh >= 0; sh -= 8) {
+        for (int ish = 24; ish >= 0; ish -= 8) {
             for (int b = tid; b < 256; b += blockDim.x) s.hist[b] = 0;
             __syncthreads();
-            const unsigned hm = (sh == 24) ? 0u : (~0u << (sh + 8));
+            const unsigned hmi = (ish == 24) ? 0u : (~0u << (ish + 8));
             for (int t = tid; t < c; t += blockDim.x)
-                if (K[t] == kth && ((unsigned)I[t] & hm) == ip) atomicAdd(&s.hist[((unsigned)I[t] >> sh) & 255u], 1u);
+                if (K[t] == prefix && ((unsigned)I[t] & hmi) == ip) atomicAdd(&s.hist[((unsigned)I[t] >> ish) & 255u], 1u);
             __syncthreads();
             if (tid < 32) warp_pick_bin(s.hist, need, s.misc);
             __syncthreads();
-            ip |= ((unsigned)s.misc[0]) << sh;
+            ip |= ((unsigned)s.misc[0]) << ish;
             need = s.misc[1];
             __syncthreads();
         }
         ith = (int)ip;
     }
-    // mark members: idx >= 0 in, set bit 31 for non-members / taken ones
+    kth_out = prefix;
+    ith_out = ith;
+}
+
+// Exact selection of the Nprime smallest (key, idx) of the c survivors held in
+// K/I[0..c) (entries with K = ~0 are dead): one radix select for rank Nprime
+// (membership) and one for rank n0, whose n0 members are ranked by counting and
+// written first (pool[0..n0) = X_{n0}(x) in NN order); the rest of the members
+// follow in any order (positions >= n0 never affect results: every candidate's
+// score and the (Delta, index) argmax are order-independent).
+// K/I may be shared or global memory (large pools select in the global buffers).
+__device__ void select_pool(NNSmem &s, uint64_t *K, int32_t *I, int c, int Nprime, int n0,
+                            int32_t *__restrict__ po) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    // range of the live keys
+    unsigned long long kmin = ~0ull, kmax = 0ull;
     for (int t = tid; t < c; t += blockDim.x) {
-        const bool in = kv_less(K[t], I[t], kth, ith) || (K[t] == kth && I[t] == ith);
-        if (!in) I[t] |= (int)0x80000000;
+        const unsigned long long k = K[t];
+        if (k != ~0ull) {
+            kmin = k < kmin ? k : kmin;
+            kmax = k > kmax ? k : kmax;
+        }
     }
-    __syncthreads();
-    // n0 smallest in ascending (key, idx) order
-    for (int r = 0; r < n0; r++) {
-        unsigned long long bk = ~0ull;
-        int bi = 0x7fffffff, bt = -1;
-        for (int t = tid; t < c; t += blockDim.x)
-            if (I[t] >= 0 && kv_less(K[t], I[t], bk, bi)) { bk = K[t]; bi = I[t]; bt = t; }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, off);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-            const int ot = __shfl_xor_sync(0xffffffffu, bt, off);
-            if (kv_less(ok, oi, bk, bi)) { bk = ok; bi = oi; bt = ot; }
-        }
-        if (lane == 0) { s.redk[wid] = bk; s.redi[wid] = bi; s.scan[wid] = bt; }
-        __syncthreads();
-        if (tid == 0) {
-            unsigned long long k0 = s.redk[0];
-            int i0 = s.redi[0], t0 = s.scan[0];
-            for (int w = 1; w < nw; w++)
-                if (kv_less(s.redk[w], s.redi[w], k0, i0)) { k0 = s.redk[w]; i0 = s.redi[w]; t0 = s.scan[w]; }
-            po[r] = i0;
-            I[t0] |= (int)0x80000000;
-        }
-        __syncthreads();
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmin, off);
+        const unsigned long long b = __shfl_xor_sync(0xffffffffu, kmax, off);
+        kmin = a < kmin ? a : kmin;
+        kmax = b > kmax ? b : kmax;
     }
-    // the other members, any order
-    if (tid == 0) s.misc[3] = n0;
+    if (lane == 0) { s.redk[wid] = kmin; s.redi[wid] = (int)(kmax >> 32); s.scan[wid] = (int)(unsigned)kmax; }
     __syncthreads();
-    for (int t = tid; t < c; t += blockDim.x)
-        if (I[t] >= 0) po[atomicAdd(&s.misc[3], 1)] = I[t];
+    kmin = ~0ull;
+    kmax = 0ull;
+    for (int w = 0; w < nw; w++) {
+        const unsigned long long a = s.redk[w];
+        const unsigned long long b = ((unsigned long long)(unsigned)s.redi[w] << 32) | (unsigned)s.scan[w];
+        kmin = a < kmin ? a : kmin;
+        kmax = b > kmax ? b : kmax;
+    }
+    __syncthreads();
+    unsigned long long kth, k0th;
+    int ith, i0th;
+    radix_select_kv(s, K, I, c, Nprime, kmin, kmax, kth, ith);
+    if (n0 > 0) {
+        radix_select_kv(s, K, I, c, n0, kmin, kmax, k0th, i0th);
+    } else {
+        k0th = 0ull;
+        i0th = -1;  // no entry is <= (0, -1)
+    }
+    if (tid == 0) { s.misc[2] = 0; s.misc[3] = n0; }
+    __syncthreads();
+    // the n0 nearest to shared memory (exactly n0: the composite order is total);
+    // the other members straight to the pool
+    for (int t = tid; t < c; t += blockDim.x) {
+        const unsigned long long k = K[t];
+        const int i = I[t];
+        if (k == ~0ull) continue;
+        if (kv_less(k, i, k0th, i0th) || (k == k0th && i == i0th)) {
+            const int pos = atomicAdd(&s.misc[2], 1);
+            s.n0k[pos] = k;
+            s.n0i[pos] = i;
+        } else if (kv_less(k, i, kth, ith) || (k == kth && i == ith)) {
+            po[atomicAdd(&s.misc[3], 1)] = i;
+        }
+    }
+    __syncthreads();
+    for (int a = tid; a < n0; a += blockDim.x) {  // rank by counting
+        const unsigned long long k = s.n0k[a];
+        const int i = s.n0i[a];
+        int r = 0;
+        for (int b = 0; b < n0; b++) r += kv_less(s.n0k[b], s.n0i[b], k, i) ? 1 : 0;
+        po[r] = i;
+    }
     __syncthreads();
 }
 
