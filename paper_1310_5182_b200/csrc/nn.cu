@@ -24,7 +24,6 @@ namespace lagp {
 
 constexpr int NN_THREADS = 256;
 constexpr int NN_Q = 16;
-constexpr int NN_SAMPLE = 2048;
 constexpr int NN_CAP = 8192;
 constexpr int NN_MAX_ROUNDS = 6;
 
@@ -50,6 +49,8 @@ struct NNSmem {
     int misc[4];
     unsigned long long n0k[LAGP_NMAX];  // the n0 nearest (select_pool)
     int n0i[LAGP_NMAX];
+    int wcnt[NN_THREADS / 32][NN_Q];    // filter appends per (warp segment, query)
+    int ovf[NN_Q];                      // a warp segment overflowed
 };
 
 __device__ __forceinline__ bool key_less(uint64_t ka, int ia, uint64_t kb, int ib) {
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(NN_THREADS)
 nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, const float *__restrict__ rn2f,
                const unsigned long long *maxn2_bits,
                int64_t N, int p, const double *__restrict__ XX, int64_t M, int Nprime, int n0, int bufcap,
-               int sorted, int32_t *__restrict__ pool_out, double *__restrict__ d2_out, float *__restrict__ samp_ws,
+               int sorted, int32_t *__restrict__ pool_out, double *__restrict__ d2_out, int32_t *__restrict__ bufc_ws,
                uint64_t *__restrict__ bufk_ws, int32_t *__restrict__ bufi_ws, int *__restrict__ fallback_count) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     NNSmem &s = *reinterpret_cast<NNSmem *>(smem_raw);
@@ -498,9 +499,12 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
     const int r2 = (int)ceil(1.5 * (double)Nprime * (double)S2 / (double)N) + 12;
     int r1 = (int)ceil(4.0 * (double)r2 * (double)S1 / (double)S2) + 4;
     if (Nprime >= N) r1 = S1 + 1;
-    (void)samp_ws;
+    // per query: bufi = filter survivors in NN_THREADS/32 warp segments of segcap rows;
+    // bufk/bufc = the exact survivors (key, row), compacted
     uint64_t *bufk = bufk_ws + (size_t)blockIdx.x * NN_Q * bufcap;
     int32_t *bufi = bufi_ws + (size_t)blockIdx.x * NN_Q * bufcap;
+    int32_t *bufc = bufc_ws + (size_t)blockIdx.x * NN_Q * bufcap;
+    const int segcap = bufcap / nw;
     const double Bn2 = __longlong_as_double((long long)*maxn2_bits);
     const double u32 = 5.9604644775390625e-08;  // 2^-24, FP32 unit roundoff
 
@@ -557,9 +561,14 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
 #pragma unroll
                     for (int q = 0; q < NN_Q; q++) {
                         const float d2f = row_d2f<P>(xf, s.nqf[q], p);
-                        if (d2f <= (float)s.tau[q]) {
-                            const int pos = atomicAdd(&s.cnt[q], 1);
-                            if (pos < bufcap) lst[(size_t)q * bufcap + pos] = d2f;
+                        const bool hit = d2f <= (float)s.tau[q];
+                        const unsigned m = __ballot_sync(__activemask(), hit);
+                        if (m) {  // one shared atomic per warp and query
+                            const int leader = __ffs(m) - 1;
+                            int pos = 0;
+                            if (lane == leader) pos = atomicAdd(&s.cnt[q], __popc(m));
+                            pos = __shfl_sync(__activemask(), pos, leader) + __popc(m & ((1u << lane) - 1u));
+                            if (hit && pos < bufcap) lst[(size_t)q * bufcap + pos] = d2f;
                         }
                     }
                 }
@@ -586,6 +595,8 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
 
         // ---- filter rounds
         for (int round = 0; round < NN_MAX_ROUNDS; round++) {
+            for (int e = tid; e < nw * NN_Q; e += blockDim.x) (&s.wcnt[0][0])[e] = 0;
+            if (tid < NN_Q) s.ovf[tid] = 0;
             if (tid < NN_Q && s.state[tid] == 0) {  // only queries still searching
                 const int q = tid;
                 s.cnt[q] = 0;
@@ -631,48 +642,72 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                     bool hit[4];
 #pragma unroll
                     for (int u = 0; u < 4; u++) hit[u] = fmaf(-2.f, row_dotf<P>(xf[u], qv, p), qn + rn[u]) <= thr;
-                    // warp-aggregated append: one uniform test per (row block, query)
+                    // append to this warp's own segment of the query's buffer: the warp
+                    // owns its counter, so positions come from ballots alone (no atomics)
                     if (__any_sync(0xffffffffu, hit[0] | hit[1] | hit[2] | hit[3])) {
+                        int wc = s.wcnt[wid][q];
+                        const unsigned lt = (1u << lane) - 1u;
+                        int32_t *seg = bufi + q * bufcap + wid * segcap;
 #pragma unroll
                         for (int u = 0; u < 4; u++) {
                             const unsigned m = __ballot_sync(0xffffffffu, hit[u]);
-                            if (m) {
-                                int basepos = 0;
-                                if (lane == 0) basepos = atomicAdd(&s.cnt[q], __popc(m));
-                                basepos = __shfl_sync(0xffffffffu, basepos, 0);
-                                if (hit[u]) {
-                                    const int pos = basepos + __popc(m & ((1u << lane) - 1u));
-                                    if (pos < bufcap) bufi[q * bufcap + pos] = (int)(base + u * (int64_t)blockDim.x);
-                                }
-                            }
+                            const int pos = wc + __popc(m & lt);
+                            if (hit[u] && pos < segcap) seg[pos] = (int)(base + u * (int64_t)blockDim.x);
+                            wc += __popc(m);
                         }
+                        __syncwarp();
+                        if (lane == 0) {
+                            s.wcnt[wid][q] = wc;
+                            if (wc > segcap) s.ovf[q] = 1;
+                        }
+                        __syncwarp();
                     }
                 }
             }
             __syncthreads();
-            // dense exact pass over the prefilter survivors: FP64 key, keep d2 <= tau
+            // dense exact pass over the prefilter survivors (the warp segments read as
+            // one range): FP64 key, keep d2 <= tau, compacted into bufk/bufc
             for (int q = 0; q < NN_Q; q++) {
                 if (!((act >> q) & 1u)) continue;
-                const int cf = min(s.cnt[q], bufcap);
+                if (s.ovf[q]) {  // too many survivors: rescale below
+                    __syncthreads();
+                    if (tid == 0) { s.cnt[q] = bufcap + 1; s.valid[q] = 0; }
+                    __syncthreads();
+                    continue;
+                }
+                int tot = 0;
+                for (int w = 0; w < nw; w++) tot += s.wcnt[w][q];
                 if (tid == 0) s.misc[3] = 0;
                 __syncthreads();
-                int keep = 0;
-                for (int t = tid; t < cf; t += blockDim.x) {
-                    const int r = bufi[q * bufcap + t];
-                    double xr[P ? P : LAGP_PMAX];
-                    load_row<P>(X, r, p, xr);
-                    const double d2 = row_d2<P>(xr, s.qx[q], p);
-                    const bool ok = d2 <= s.tau[q];
-                    bufk[q * bufcap + t] = ok ? d2_key(d2) : ~0ull;  // ~0 = out (sorts last)
-                    keep += ok;
+                for (int tb = tid - lane; tb < tot; tb += blockDim.x) {  // warp-uniform bound
+                    const int t = tb + lane;
+                    bool ok = false;
+                    int r = 0;
+                    double d2 = 0.0;
+                    if (t < tot) {
+                        int w = 0, off = t;
+                        while (off >= s.wcnt[w][q]) { off -= s.wcnt[w][q]; w++; }
+                        r = bufi[q * bufcap + w * segcap + off];
+                        double xr[P ? P : LAGP_PMAX];
+                        load_row<P>(X, r, p, xr);
+                        d2 = row_d2<P>(xr, s.qx[q], p);
+                        ok = d2 <= s.tau[q];
+                    }
+                    const unsigned m = __ballot_sync(0xffffffffu, ok);
+                    if (m) {
+                        int pos = 0;
+                        if (lane == 0) pos = atomicAdd(&s.misc[3], __popc(m));
+                        pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(m & ((1u << lane) - 1u));
+                        if (ok) {
+                            bufk[q * bufcap + pos] = d2_key(d2);
+                            bufc[q * bufcap + pos] = r;
+                        }
+                    }
                 }
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) keep += __shfl_xor_sync(0xffffffffu, keep, off);
-                if (lane == 0 && keep) atomicAdd(&s.misc[3], keep);
                 __syncthreads();
                 if (tid == 0) {
-                    s.valid[q] = s.misc[3];           // exact d2 <= tau
-                    s.cnt[q] = s.cnt[q] > bufcap ? bufcap + 1 : cf;  // entries in the buffer (bufcap+1: overflow)
+                    s.valid[q] = s.misc[3];  // exact d2 <= tau, all of them in bufk/bufc
+                    s.cnt[q] = s.misc[3];
                 }
                 __syncthreads();
             }
@@ -705,7 +740,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
             int c;
             int32_t *po = pool_out + (q0 + q) * (int64_t)Nprime;
             uint64_t *qk = bufk + (size_t)q * bufcap;
-            int32_t *qi = bufi + (size_t)q * bufcap;
+            int32_t *qi = bufc + (size_t)q * bufcap;
             if (s.state[q] == 2) {
                 if (tid == 0) atomicAdd(fallback_count, 1);
                 nn_exact_select<P>(s, X, N, p, q, Nprime, qk, qi);
@@ -750,11 +785,12 @@ static int nn_bufcap(int Nprime, bool sorted) {
     return c;
 }
 
-// Workspace layout: [maxn2 bits (256 B)] [X32: N*p floats] [sample] [survivor keys] [survivor idx]
+// Workspace layout: [maxn2 bits (256 B)] [X32: N*p floats] [rn2f: N floats]
+// [compacted rows] [survivor keys] [filter rows], the last three bufcap per query
 size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime, bool sorted) {
     const size_t bc = (size_t)nn_bufcap(Nprime, sorted);
     return 256 + (((size_t)N * p * sizeof(float) + 255) & ~(size_t)255) + (((size_t)N * sizeof(float) + 255) & ~(size_t)255) +
-           (size_t)grid * NN_Q * (NN_SAMPLE * sizeof(float) + bc * (sizeof(uint64_t) + sizeof(int32_t))) + 256;
+           (size_t)grid * NN_Q * bc * (sizeof(uint64_t) + 2 * sizeof(int32_t)) + 256;
 }
 
 template <int P>
@@ -766,12 +802,12 @@ static cudaError_t launch_nn_t(const double *X, const float *X32, const float *r
     cudaError_t e = cudaFuncSetAttribute(nn_pool_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int bc = nn_bufcap(Nprime, sorted != 0);
-    float *samp = (float *)w;
-    w += (size_t)grid * NN_Q * NN_SAMPLE * sizeof(float);
+    int32_t *bcmp = (int32_t *)w;
+    w += (size_t)grid * NN_Q * bc * sizeof(int32_t);
     uint64_t *bk = (uint64_t *)w;
     w += (size_t)grid * NN_Q * bc * sizeof(uint64_t);
     int32_t *bi = (int32_t *)w;
-    nn_pool_kernel<P><<<grid, NN_THREADS, smem, st>>>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, bc, sorted, pool, d2, samp,
+    nn_pool_kernel<P><<<grid, NN_THREADS, smem, st>>>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, bc, sorted, pool, d2, bcmp,
                                                       bk, bi, fb);
     return cudaGetLastError();
 }
@@ -780,7 +816,7 @@ int nn_grid(int64_t M, int num_sms, int Nprime) {
     int64_t groups = (M + NN_Q - 1) / NN_Q;
     int64_t g = 2LL * num_sms;  // 2 CTAs/SM fit (~110 KB smem each)
     // keep the survivor buffers under ~2 GiB for large pools
-    const int64_t per_cta = (int64_t)NN_Q * nn_bufcap(Nprime, false) * 12;
+    const int64_t per_cta = (int64_t)NN_Q * nn_bufcap(Nprime, false) * 16;
     const int64_t gmax = ((int64_t)2 << 30) / per_cta;
     if (g > gmax) g = gmax > 1 ? gmax : 1;
     return (int)(groups < g ? (groups > 0 ? groups : 1) : g);
