@@ -125,7 +125,7 @@ alc_incremental_kernel(AlcArgs A, int S) {
         }
         __syncthreads();
 
-        // Three barriers per step: two in the argmax, one after the publish. The
+        // Two barriers per step: one in the argmax, one after the publish. The
         // publish slots and the argmax scratch alternate by step parity, so a slot
         // is rewritten only after every thread has passed the next step's barriers.
         int j = 0;  // current design size
@@ -161,7 +161,7 @@ alc_incremental_kernel(AlcArgs A, int S) {
                 }
                 if (__any_sync(0xffffffffu, sentinel) && lane == 0) atomicOr(&fl, (uint32_t)LAGP_FLAG_SENTINEL);
                 if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(&fl, (uint32_t)LAGP_FLAG_NONFINITE);
-                const ArgTop best = block_argtop_db(bd1, bi, bd2, bp, red, par);
+                const ArgTop best = block_argtop_1b(bd1, bi, bd2, bp, red, par);
                 if (best.i1 < 0) {
                     if (tid == 0) fl |= LAGP_FLAG_EXHAUSTED;
                     break;

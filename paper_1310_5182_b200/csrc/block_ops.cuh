@@ -187,6 +187,43 @@ __device__ __forceinline__ ArgTop block_argtop_db(double d1, int i1, double d2, 
     return r;
 }
 
+// block_argtop with ONE barrier: lane 0 of every warp posts the warp's result,
+// then every warp reduces the posts itself (redundantly). `scratch` >= 200
+// doubles, double-buffered by `parity`; safe when at least one other barrier
+// separates two calls with the same parity.
+__device__ __forceinline__ ArgTop block_argtop_1b(double d1, int i1, double d2, int pos, double *scratch,
+                                                  int parity) {
+    unsigned long long k1 = (unsigned long long)__double_as_longlong(d1 > 0.0 ? d1 : 0.0);
+    unsigned long long k2 = (unsigned long long)__double_as_longlong(d2 > 0.0 ? d2 : 0.0);
+    unsigned ii = (unsigned)i1;
+    warp_argtop(k1, ii, k2, pos);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long *sk = reinterpret_cast<unsigned long long *>(scratch) + parity * 100;
+    if (lane == 0) {
+        sk[3 * wid + 0] = k1;
+        sk[3 * wid + 1] = ((unsigned long long)(unsigned)pos << 32) | ii;
+        sk[3 * wid + 2] = k2;
+    }
+    __syncthreads();
+    const int nw = blockDim.x >> 5;
+    unsigned long long a1 = 0, a2 = 0;
+    unsigned ai = 0xffffffffu;
+    int ap = -1;
+    if (lane < nw) {
+        a1 = sk[3 * lane + 0];
+        ai = (unsigned)sk[3 * lane + 1];
+        ap = (int)(unsigned)(sk[3 * lane + 1] >> 32);
+        a2 = sk[3 * lane + 2];
+    }
+    warp_argtop(a1, ai, a2, ap);
+    ArgTop r;
+    r.d1 = __longlong_as_double((long long)a1);
+    r.i1 = (int)ai;
+    r.pos = ap;
+    r.d2 = __longlong_as_double((long long)a2);
+    return r;
+}
+
 // Partitioned-inverse append (a4; Eq (6)): given the
 // explicit K_j^{-1} in Kinv (leading dimension ld, symmetric), k = k_j(x_new)
 // and kdiag = K(x_new,x_new) + eta, overwrite Kinv with K_{j+1}^{-1}:
