@@ -23,6 +23,9 @@ FLAG_NEAR_TIE = 1
 FLAG_SENTINEL = 2
 FLAG_EXHAUSTED = 4
 FLAG_NONFINITE = 8
+MLE_FLAG_MAXIT = 32
+MLE_FLAG_BOUND = 16
+MLE_FLAG_FAIL = 64
 
 
 def build(force: bool = False) -> str:
@@ -56,8 +59,13 @@ def lib():
                                              I32, D, D, D, U32, D, D, D]
         _lib.oracle_alc_batch.argtypes = [D, i64, i32, D, D, i64, dbl, dbl, i32, i32, i32, i32,
                                           I32, D, D, D, U32, D, D, D]
+        _lib.oracle_loglik.argtypes = [i32, i32, D, D, dbl, dbl, i32, D, D, D]
+        _lib.oracle_mle.argtypes = [i32, i32, D, D, dbl, dbl, dbl, dbl, D, D, ctypes.POINTER(ctypes.c_int), U32]
+        _lib.oracle_local_fit_batch.argtypes = [D, i64, i32, D, D, i64, dbl, dbl, dbl, dbl, i32, i32, i32, i32,
+                                                i32, I32, D, D, D, D, U32]
         for f in ("oracle_nn", "oracle_invert_spd", "oracle_alc_scores", "oracle_pinv_update",
-                  "oracle_predict", "oracle_local_design", "oracle_alc_batch"):
+                  "oracle_predict", "oracle_local_design", "oracle_alc_batch", "oracle_loglik", "oracle_mle",
+                  "oracle_local_fit_batch"):
             getattr(_lib, f).restype = ctypes.c_int
     return _lib
 
@@ -163,3 +171,50 @@ def alc_batch(X, Z, XX, d, g, n0, n, Nprime, threads=0):
 def local_design(X, Z, x, d, g, n0, n, Nprime):
     r = alc_batch(X, Z, np.atleast_2d(x), d, g, n0, n, Nprime, threads=1)
     return {k: (v[0] if isinstance(v, np.ndarray) else v) for k, v in r.items()}
+
+
+def loglik(Xn, Yn, d, g, deriv=True):
+    """Eq (3) log likelihood on (Xn, Yn) and, with deriv, its first and second
+    derivatives in tau = log(theta) (reading R20). Returns (l, dl, d2l); l = -inf
+    when K is not SPD or psi <= 0."""
+    Xn, pX = _d(np.atleast_2d(Xn))
+    Yn, pY = _d(Yn)
+    n, p = Xn.shape
+    l, dl, d2l = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    lib().oracle_loglik(n, p, pX, pY, d, g, 1 if deriv else 0, ctypes.byref(l), ctypes.byref(dl), ctypes.byref(d2l))
+    return l.value, dl.value, d2l.value
+
+
+def mle(Xn, Yn, d0, lo, hi, g):
+    """Fig 1 step 3: theta-hat on (Xn, Yn) by the safeguarded Newton of reading
+    R21. Returns (theta_hat, l(theta_hat), iterations, flags)."""
+    Xn, pX = _d(np.atleast_2d(Xn))
+    Yn, pY = _d(Yn)
+    n, p = Xn.shape
+    th, lh, it, fl = ctypes.c_double(), ctypes.c_double(), ctypes.c_int(), ctypes.c_uint32()
+    lib().oracle_mle(n, p, pX, pY, d0, lo, hi, g, ctypes.byref(th), ctypes.byref(lh), ctypes.byref(it),
+                     ctypes.byref(fl))
+    return th.value, lh.value, it.value, fl.value
+
+
+def local_fit(X, Z, XX, d0, lo, hi, g, n0, n, Nprime, stages=2, threads=0):
+    """Fig 1 steps 1-5 (multi-stage: design, MLE, repeat, predict) for every row
+    of XX. theta is stages x M (theta_x after each stage)."""
+    if not 1 <= stages <= 16:
+        raise ValueError("stages must be in [1, 16]")
+    X, pX = _d(X)
+    Z, pZ = _d(Z)
+    XX, pXX = _d(np.atleast_2d(XX))
+    N, p = X.shape
+    M = XX.shape[0]
+    idx = np.empty((M, n), np.int32)
+    theta = np.empty((stages, M))
+    mean = np.empty(M)
+    s2 = np.empty(M)
+    var = np.empty(M)
+    flags = np.empty(M, np.uint32)
+    used = lib().oracle_local_fit_batch(
+        pX, N, p, pZ, pXX, M, d0, lo, hi, g, n0, n, Nprime, stages, threads,
+        _p(idx, ctypes.c_int32), _p(theta, ctypes.c_double), _p(mean, ctypes.c_double),
+        _p(s2, ctypes.c_double), _p(var, ctypes.c_double), _p(flags, ctypes.c_uint32))
+    return dict(idx=idx, theta=theta, mean=mean, s2=s2, var=var, flags=flags, threads=used)

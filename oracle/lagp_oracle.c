@@ -387,3 +387,222 @@ int oracle_alc_batch(const double *X, int64_t N, int p, const double *Z, const d
     }
     return used;
 }
+
+/* ========================================================================= */
+/* Row f2: local MLE of the lengthscale and the multi-stage scheme
+ * of Fig 1 steps 1-5 ("two-stage scheme").
+ *
+ * Concentrated log likelihood, Eq (3) on D_n(x):
+ *   l(theta) = lgamma(n/2) - (n/2) log(2 pi) - (1/2) log|K| - (n/2) log(psi/2),
+ *   K = C + eta I, C_ab = exp(-D_ab/theta), psi = Y^T K^{-1} Y.
+ * The paper only says its derivatives "are also available analytically"
+ * (P:201-203); reading R20 writes them out in tau = log(theta):
+ *   P = dK/dtau,    P_ab = C_ab (D_ab/theta)
+ *   Q = d2K/dtau2,  Q_ab = C_ab (D_ab/theta) (D_ab/theta - 1)
+ *   alpha = K^{-1} Y
+ *   dl/dtau   = -1/2 tr(K^{-1}P) + (n/2) alpha^T P alpha / psi
+ *   d2l/dtau2 = -1/2 tr(K^{-1}Q) + 1/2 tr(K^{-1}P K^{-1}P)
+ *               - (n/2) (2 alpha^T P K^{-1} P alpha - alpha^T Q alpha) / psi
+ *               + (n/2) (alpha^T P alpha / psi)^2
+ * Plain dense linear algebra: textbook Cholesky, explicit inverse by solves. */
+#define OR_MLE_MAXIT 64
+#define OR_MLE_BOUND 16u   /* theta-hat at a bound            */
+#define OR_MLE_MAXITS 32u  /* iteration limit reached         */
+#define OR_MLE_FAIL 64u    /* non-finite likelihood at start  */
+
+typedef struct { double l, g, h; } or_lik;
+
+/* Returns 0 and fills out (l, dl/dtau, d2l/dtau2) at theta; 1 if K is not SPD
+ * or psi <= 0 (l = -inf). want_deriv = 0 skips the derivatives. */
+int oracle_loglik(int n, int p, const double *Xn, const double *Yn, double theta, double eta,
+                  int want_deriv, double *l, double *g, double *h) {
+    double *D = (double *)malloc(sizeof(double) * (size_t)n * n + 8);
+    double *C = (double *)malloc(sizeof(double) * (size_t)n * n + 8);
+    double *K = (double *)malloc(sizeof(double) * (size_t)n * n + 8);
+    double *L = (double *)malloc(sizeof(double) * (size_t)n * n + 8);
+    double *A = (double *)malloc(sizeof(double) * (size_t)n * n + 8);
+    double *T = (double *)malloc(sizeof(double) * (size_t)n * n + 8);
+    double *al = (double *)malloc(sizeof(double) * (size_t)n + 8);
+    double *v = (double *)malloc(sizeof(double) * (size_t)n + 8);
+    double *e = (double *)malloc(sizeof(double) * (size_t)n + 8);
+    int rc = 0;
+    *l = -INFINITY;
+    if (g) *g = NAN;
+    if (h) *h = NAN;
+    if (!D || !C || !K || !L || !A || !T || !al || !v || !e) { rc = 4; goto out; }
+    for (int a = 0; a < n; a++)
+        for (int b = 0; b < n; b++) {
+            D[a * n + b] = sqdist(Xn + a * p, Xn + b * p, p);
+            C[a * n + b] = exp(-D[a * n + b] / theta);
+            K[a * n + b] = C[a * n + b] + (a == b ? eta : 0.0);
+        }
+    if (cholesky(n, K, L)) { rc = 1; goto out; }
+    double logdet = 0.0;
+    for (int a = 0; a < n; a++) logdet += 2.0 * log(L[a * n + a]);
+    for (int a = 0; a < n; a++) al[a] = Yn[a];
+    chol_solve(n, L, al);
+    double psi = 0.0;
+    for (int a = 0; a < n; a++) psi += Yn[a] * al[a];
+    if (!(psi > 0.0)) { rc = 1; goto out; }
+    *l = lgamma(0.5 * n) - 0.5 * n * log(2.0 * M_PI) - 0.5 * logdet - 0.5 * n * log(0.5 * psi);
+    if (!want_deriv) goto out;
+    /* explicit K^{-1} */
+    for (int b = 0; b < n; b++) {
+        for (int i = 0; i < n; i++) e[i] = (i == b) ? 1.0 : 0.0;
+        chol_solve(n, L, e);
+        for (int a = 0; a < n; a++) A[a * n + b] = e[a];
+    }
+    /* P (into K's storage) and T = K^{-1} P */
+    for (int a = 0; a < n; a++)
+        for (int b = 0; b < n; b++) K[a * n + b] = C[a * n + b] * (D[a * n + b] / theta);
+    for (int a = 0; a < n; a++)
+        for (int b = 0; b < n; b++) {
+            double s = 0.0;
+            for (int t = 0; t < n; t++) s += A[a * n + t] * K[t * n + b];
+            T[a * n + b] = s;
+        }
+    double trAP = 0.0, trAQ = 0.0, trTT = 0.0, aPa = 0.0, aQa = 0.0;
+    for (int a = 0; a < n; a++) {
+        double pv = 0.0;
+        for (int b = 0; b < n; b++) {
+            const double r = D[a * n + b] / theta;
+            const double Pab = K[a * n + b];
+            const double Qab = C[a * n + b] * r * (r - 1.0);
+            trAP += A[a * n + b] * Pab;
+            trAQ += A[a * n + b] * Qab;
+            trTT += T[a * n + b] * T[b * n + a];
+            aQa += al[a] * Qab * al[b];
+            pv += Pab * al[b];
+        }
+        v[a] = pv;  /* v = P alpha */
+        aPa += al[a] * pv;
+    }
+    double vAv = 0.0;
+    for (int a = 0; a < n; a++)
+        for (int b = 0; b < n; b++) vAv += v[a] * A[a * n + b] * v[b];
+    const double q = aPa / psi;
+    *g = -0.5 * trAP + 0.5 * n * q;
+    *h = -0.5 * trAQ + 0.5 * trTT - 0.5 * n * (2.0 * vAv - aQa) / psi + 0.5 * n * q * q;
+out:
+    free(D); free(C); free(K); free(L); free(A); free(T); free(al); free(v); free(e);
+    return rc;
+}
+
+/* Local MLE theta-hat_n(x) | D_n(x), Fig 1 step 3: safeguarded
+ * Newton on tau = log(theta) inside [log lo, log hi] (reading R21):
+ *   evaluate (l, g, h) at tau; stop at a bound whose outward side the gradient
+ *   points to; step = -g/h when h < 0, else sign(g); |step| <= 1; clamp into the
+ *   bounds; steps longer than 1/4 (or non-Newton steps) are halved until l does
+ *   not decrease (<= 40 halvings); stop when |tau_new - tau| <= 1e-10 max(1,|tau|)
+ *   or after OR_MLE_MAXIT iterations. A start with non-finite l returns theta0
+ *   (flag OR_MLE_FAIL; the incoming theta is kept, SPEC S:279 reading). */
+int oracle_mle(int n, int p, const double *Xn, const double *Yn, double theta0, double lo, double hi,
+               double eta, double *theta_hat, double *lhat, int *iters, uint32_t *flags) {
+    const double tlo = log(lo), thi = log(hi);
+    double tau = log(theta0);
+    if (tau < tlo) tau = tlo;
+    if (tau > thi) tau = thi;
+    uint32_t fl = 0;
+    double l, g, h;
+    int it = 0;
+    if (oracle_loglik(n, p, Xn, Yn, exp(tau), eta, 1, &l, &g, &h) || !isfinite(g) || !isfinite(h)) {
+        *theta_hat = theta0; *lhat = l; *iters = 0; *flags = OR_MLE_FAIL;
+        return 0;
+    }
+    for (it = 1; it <= OR_MLE_MAXIT; it++) {
+        if ((tau <= tlo && g <= 0.0) || (tau >= thi && g >= 0.0)) { fl |= OR_MLE_BOUND; break; }
+        if (g == 0.0 && !(h < 0.0)) break;
+        double step = (h < 0.0) ? -g / h : (g > 0.0 ? 1.0 : -1.0);
+        if (step > 1.0) step = 1.0;
+        if (step < -1.0) step = -1.0;
+        double tn = tau + step;
+        if (tn < tlo) tn = tlo;
+        if (tn > thi) tn = thi;
+        double ln, gn, hn;
+        int bad = oracle_loglik(n, p, Xn, Yn, exp(tn), eta, 1, &ln, &gn, &hn) || !isfinite(gn) || !isfinite(hn);
+        if (fabs(step) > 0.25 || !(h < 0.0)) {
+            for (int t = 0; t < 40 && (bad || ln < l); t++) {
+                tn = 0.5 * (tau + tn);
+                bad = oracle_loglik(n, p, Xn, Yn, exp(tn), eta, 1, &ln, &gn, &hn) || !isfinite(gn) || !isfinite(hn);
+            }
+            if (bad || ln < l) break;  /* no ascent along the step: stay at tau */
+        } else if (bad) {
+            break;
+        }
+        const double dt = fabs(tn - tau);
+        tau = tn; l = ln; g = gn; h = hn;
+        if (dt <= 1e-10 * (fabs(tau) > 1.0 ? fabs(tau) : 1.0)) break;
+    }
+    if (it > OR_MLE_MAXIT) fl |= OR_MLE_MAXITS;
+    if (tau <= tlo || tau >= thi) fl |= OR_MLE_BOUND;
+    *theta_hat = exp(tau);
+    *lhat = l;
+    *iters = it > OR_MLE_MAXIT ? OR_MLE_MAXIT : it;
+    *flags = fl;
+    return 0;
+}
+
+/* Multi-stage scheme, Fig 1 for ONE location x:
+ *   1. theta_x = theta0;
+ *   2. local design X_n(x, theta_x) (oracle_local_design: NN start + greedy ALC);
+ *   3. theta_x = theta-hat_n(x) | D_n(x, theta_x)  (oracle_mle, started at theta_x);
+ *   4. repeat 2-3 `stages` times in all;
+ *   5. predict with theta_x on the last D_n(x) (oracle_predict, fresh Cholesky).
+ * theta_out[s] = theta_x after stage s; flags = last design's flags | last MLE's. */
+int oracle_local_fit(const double *X, int64_t N, int p, const double *Z, const double *x,
+                     double theta0, double lo, double hi, double eta, int n0, int n, int Nprime, int stages,
+                     int32_t *idx, double *theta_out, double *mean, double *s2, double *var, uint32_t *flags) {
+    double th = theta0;
+    uint32_t fl = 0;
+    int G = n - n0;
+    double *gaps = (double *)malloc(sizeof(double) * (size_t)(G > 0 ? G : 1));
+    double *best = (double *)malloc(sizeof(double) * (size_t)(G > 0 ? G : 1));
+    double *Xn = (double *)malloc(sizeof(double) * (size_t)n * p);
+    double *Yn = (double *)malloc(sizeof(double) * (size_t)n);
+    if (!gaps || !best || !Xn || !Yn) { free(gaps); free(best); free(Xn); free(Yn); return 4; }
+    int j = n;
+    for (int s = 0; s < stages; s++) {
+        double mu, sc, vr;
+        uint32_t dfl = 0;
+        int rc = oracle_local_design(X, N, p, Z, x, th, eta, n0, n, Nprime, idx, &mu, &sc, &vr, &dfl, gaps, best, NULL);
+        if (rc) { free(gaps); free(best); free(Xn); free(Yn); return rc; }
+        for (j = 0; j < n && idx[j] >= 0; j++) {
+            memcpy(Xn + j * p, X + (size_t)idx[j] * p, sizeof(double) * p);
+            Yn[j] = Z[idx[j]];
+        }
+        double lh;
+        int its;
+        uint32_t mfl = 0;
+        oracle_mle(j, p, Xn, Yn, th, lo, hi, eta, &th, &lh, &its, &mfl);
+        theta_out[s] = th;
+        fl = dfl | mfl;
+    }
+    if (oracle_predict(j, p, Xn, Yn, x, th, eta, mean, s2, var)) {
+        fl |= OR_FLAG_NONFINITE;
+        *mean = NAN; *s2 = NAN; *var = NAN;
+    }
+    if (!isfinite(*mean) || !isfinite(*s2)) fl |= OR_FLAG_NONFINITE;
+    *flags = fl;
+    free(gaps); free(best); free(Xn); free(Yn);
+    return 0;
+}
+
+/* All M locations (OpenMP over locations). theta_out is stages x M. */
+int oracle_local_fit_batch(const double *X, int64_t N, int p, const double *Z, const double *XX, int64_t M,
+                           double theta0, double lo, double hi, double eta, int n0, int n, int Nprime,
+                           int stages, int nthreads, int32_t *idx, double *theta_out, double *mean, double *s2,
+                           double *var, uint32_t *flags) {
+    int used = 1;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+    used = nthreads;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+#endif
+    for (int64_t i = 0; i < M; i++) {
+        double th[16];
+        oracle_local_fit(X, N, p, Z, XX + i * p, theta0, lo, hi, eta, n0, n, Nprime, stages, idx + i * n, th,
+                         mean + i, s2 + i, var + i, flags + i);
+        for (int s = 0; s < stages && s < 16; s++) theta_out[(size_t)s * M + i] = th[s];
+    }
+    return used;
+}
