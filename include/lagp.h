@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define LAGP_ABI_VERSION 1
+#define LAGP_ABI_VERSION 2
 #define LAGP_NMAX 128  /* largest local design size n supported (Fig 4 uses n <= 512: NEXT f4) */
 #define LAGP_PMAX 16   /* largest input dimension p */
 #define LAGP_NPRIME_MAX 65536 /* largest candidate pool N' (laGP_alc_batch; the incremental
@@ -49,7 +49,11 @@ enum {
     LAGP_FLAG_NEAR_TIE = 1u << 0,  /* some step had top-2 relative gap < 1e-12 (or all Delta == 0)   */
     LAGP_FLAG_SENTINEL = 1u << 1,  /* some candidate had m^{-1} = s_c <= 1e-12 and was excluded */
     LAGP_FLAG_EXHAUSTED = 1u << 2, /* no valid candidate before size n; idx tail = -1          */
-    LAGP_FLAG_NONFINITE = 1u << 3  /* a non-finite score or prediction                                */
+    LAGP_FLAG_NONFINITE = 1u << 3, /* a non-finite score or prediction                                */
+    /* row f2 (local MLE, laGP_mle / laGP_local_fit) */
+    LAGP_FLAG_MLE_BOUND = 1u << 4, /* theta-hat ended on theta_min or theta_max                      */
+    LAGP_FLAG_MLE_MAXIT = 1u << 5, /* the Newton iteration limit (64) was reached                    */
+    LAGP_FLAG_MLE_FAIL = 1u << 6   /* l(theta) not finite at the start: theta-hat = incoming theta   */
 };
 
 /* Which formulation the ALC step uses (both select the same x_{j+1} in exact
@@ -79,7 +83,8 @@ typedef struct {
 
 /*
  * laGP_alc_batch — Fig 1 steps 2 and 5 for every row of XX, with a
- * fixed global theta (Fig 1 step 1; the local MLE of steps 3-4 is NEXT).
+ * fixed global theta (Fig 1 step 1; the local MLE of steps 3-4 is
+ * laGP_mle / laGP_local_fit below).
  * For each predictive location x = XX[i]:
  *   (a1) pool = the N' nearest rows of X by the key (d^2, row index), with d^2
  *        accumulated by fma in the order k = 0..p-1 (R8);
@@ -182,6 +187,67 @@ lagp_status laGP_pinv_update(int32_t B, int32_t j, const double *Kinv, const dou
 lagp_status laGP_predict(int32_t B, int32_t n, int32_t p, const double *Xn, const double *Yn,
                          const double *x, double d, double g, double *mean_out, double *s2_out,
                          double *var_out, void *cuda_stream);
+
+/*
+ * laGP_alc_batch_theta — laGP_alc_batch_ex with a per-location lengthscale
+ * theta [M] (device, each finite and > 0; not checked on the device): location
+ * i uses theta[i] in every correlation of a2-a5 (Fig 1 step 2 with theta_x,
+ * P:362-371; the NN pool a1 does not depend on theta). d is still validated and
+ * otherwise unused.
+ */
+lagp_status laGP_alc_batch_theta(const double *X, int64_t N, int32_t p, const double *Z,
+                                 const double *XX, int64_t M, const double *theta, double d, double g,
+                                 int32_t n0, int32_t n, int32_t Nprime,
+                                 int32_t *idx_out, double *mean_out, double *s2_out,
+                                 double *var_out, uint32_t *flags_out, double *gap_out,
+                                 int32_t alc_form, lagp_timing *timing, void *cuda_stream);
+
+/*
+ * laGP_mle — SURVEY §8f row f2, Fig 1 step 3: for each location i,
+ * the local MLE theta-hat_n(x_i) of the concentrated likelihood Eq (3)
+ * on D_n(x_i) = (X[idx[i,:]], Z[idx[i,:]]) (the valid prefix of the
+ * row when it has a -1 tail), then the prediction of Fig 1 step 5 (Eq (1)-(2),
+ * P:171-187) at x_i = XX[i] with theta-hat on the same design.
+ *   Search (readings R20-R21): safeguarded Newton on tau = log(theta) with the
+ *   analytic first and second derivatives, inside [theta_min, theta_max], started
+ *   at theta_in[i] (or theta0 when theta_in is NULL) clamped into the bounds;
+ *   Newton steps capped at |1| in tau; long or non-Newton steps halved until l
+ *   does not decrease; stops at a bound the gradient points out of, when
+ *   |step| <= 1e-10 max(1, |tau|), or after 64 iterations.
+ * Arguments
+ *   X [N×p], Z [N], XX [M×p]; idx [M×n] int32 local designs (e.g. laGP_alc_batch's idx_out)
+ *   theta_in [M] nullable; theta0 > 0 (used when theta_in is NULL)
+ *   0 < theta_min <= theta_max finite;  g (eta >= 0) nugget;  1 <= n <= LAGP_NMAX
+ *   theta_out [M]; loglik_out [M] nullable (l at theta-hat); iters_out [M] int32 nullable
+ *   flags_out [M] nullable: LAGP_FLAG_MLE_* (and NONFINITE) bits are OR-ed in
+ *   mean_out [M], s2_out [M], var_out [M] (nullable): prediction at theta-hat
+ * A location whose l is not finite at its start keeps the incoming theta
+ * (LAGP_FLAG_MLE_FAIL) and predicts with it.
+ */
+lagp_status laGP_mle(const double *X, int64_t N, int32_t p, const double *Z, const double *XX, int64_t M,
+                     const int32_t *idx, int32_t n, const double *theta_in, double theta0,
+                     double theta_min, double theta_max, double g,
+                     double *theta_out, double *loglik_out, int32_t *iters_out, uint32_t *flags_out,
+                     double *mean_out, double *s2_out, double *var_out, void *cuda_stream);
+
+/*
+ * laGP_local_fit — the multi-stage scheme of Fig 1 (the "two-stage
+ * scheme" of P:351-355): theta_x = theta0 (step 1); then `stages` times: the
+ * local design X_n(x, theta_x) (step 2, as laGP_alc_batch_theta) and
+ * theta_x = theta-hat_n(x) | D_n(x, theta_x) (step 3, as laGP_mle started at
+ * theta_x); finally the prediction with theta_x on the last D_n(x) (step 5).
+ * The NN pool (a1) is computed once per location.
+ *   1 <= stages <= 16;  theta_out [stages×M]: theta_x after each stage
+ *   idx_out [M×n]: the last stage's design;  mean/s2/var: step 5
+ *   flags_out [M] nullable: the last design's flags | the last MLE's flags
+ *   timing nullable: nn_ms = a1, alc_ms = all designs, predict_ms = all MLE+predict
+ * Other arguments and constraints as laGP_alc_batch_ex and laGP_mle.
+ */
+lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *Z,
+                           const double *XX, int64_t M, double theta0, double theta_min, double theta_max,
+                           double g, int32_t n0, int32_t n, int32_t Nprime, int32_t stages, int32_t alc_form,
+                           int32_t *idx_out, double *theta_out, double *mean_out, double *s2_out,
+                           double *var_out, uint32_t *flags_out, lagp_timing *timing, void *cuda_stream);
 
 /* Thread-local message for the last non-OK status of this thread. */
 const char *lagp_last_error(void);

@@ -22,6 +22,9 @@ from ._lib import (  # noqa: F401
     ALC_EXPLICIT,
     ALC_INCREMENTAL,
     FLAG_EXHAUSTED,
+    FLAG_MLE_BOUND,
+    FLAG_MLE_FAIL,
+    FLAG_MLE_MAXIT,
     FLAG_NEAR_TIE,
     FLAG_NONFINITE,
     FLAG_SENTINEL,
@@ -81,10 +84,12 @@ def _stream(device) -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
-def alc_batch(X, Z, XX, d, g, n0, n, Nprime, form="explicit", gaps=False, timing=False, out=None):
+def alc_batch(X, Z, XX, d, g, n0, n, Nprime, form="explicit", gaps=False, timing=False, out=None, theta=None):
     """laGP_alc_batch_ex on CUDA tensors. Returns a dict with idx [M×n] int32,
     mean, s2, var [M] float64, flags [M] int32 (uint32 bits), optionally
-    gaps [M×(n-n0)] and the phase timing, plus ``status`` (OK or PARTIAL)."""
+    gaps [M×(n-n0)] and the phase timing, plus ``status`` (OK or PARTIAL).
+    With ``theta`` (CUDA float64 [M]) every location uses its own lengthscale
+    (laGP_alc_batch_theta); ``d`` is then only validated."""
     X = _dev(X, "X")
     Z = _dev(Z, "Z")
     XX = _dev(XX, "XX")
@@ -102,10 +107,70 @@ def alc_batch(X, Z, XX, d, g, n0, n, Nprime, form="explicit", gaps=False, timing
         if gaps:
             out["gaps"] = torch.empty((M, n - n0), dtype=torch.float64, device=dev)
     tm = Timing()
-    st = lib().laGP_alc_batch_ex(
-        _ptr(X), N, p, _ptr(Z), _ptr(XX), M, float(d), float(g), int(n0), int(n), int(Nprime),
-        _ptr(out["idx"]), _ptr(out["mean"]), _ptr(out["s2"]), _ptr(out["var"]), _ptr(out["flags"]),
-        _ptr(out.get("gaps")), FORMS[form], ctypes.byref(tm) if timing else None, _stream(dev))
+    if theta is None:
+        st = lib().laGP_alc_batch_ex(
+            _ptr(X), N, p, _ptr(Z), _ptr(XX), M, float(d), float(g), int(n0), int(n), int(Nprime),
+            _ptr(out["idx"]), _ptr(out["mean"]), _ptr(out["s2"]), _ptr(out["var"]), _ptr(out["flags"]),
+            _ptr(out.get("gaps")), FORMS[form], ctypes.byref(tm) if timing else None, _stream(dev))
+    else:
+        theta = _dev(theta, "theta")
+        if theta.shape != (M,):
+            raise ValueError(f"theta must have shape ({M},)")
+        st = lib().laGP_alc_batch_theta(
+            _ptr(X), N, p, _ptr(Z), _ptr(XX), M, _ptr(theta), float(d), float(g), int(n0), int(n), int(Nprime),
+            _ptr(out["idx"]), _ptr(out["mean"]), _ptr(out["s2"]), _ptr(out["var"]), _ptr(out["flags"]),
+            _ptr(out.get("gaps")), FORMS[form], ctypes.byref(tm) if timing else None, _stream(dev))
+    _check(st, (LAGP_OK, LAGP_PARTIAL))
+    out["status"] = st
+    if timing:
+        out["timing"] = tm.as_dict()
+    return out
+
+
+def mle(X, Z, XX, idx, d0, lo, hi, g, theta_in=None):
+    """laGP_mle (row f2, Fig 1 step 3 + step 5): theta-hat of every local design
+    idx [M×n] (CUDA int32) started at theta_in [M] (or d0), inside [lo, hi]; and
+    the prediction at theta-hat. Returns theta, loglik, iters, flags, mean, s2, var."""
+    X = _dev(X, "X")
+    Z = _dev(Z, "Z")
+    XX = _dev(XX, "XX")
+    idx = _dev(idx, "idx", torch.int32)
+    dev = X.device
+    N, p = X.shape
+    M, n = idx.shape
+    if theta_in is not None:
+        theta_in = _dev(theta_in, "theta_in")
+    f64 = dict(dtype=torch.float64, device=dev)
+    out = dict(theta=torch.empty(M, **f64), loglik=torch.empty(M, **f64),
+               iters=torch.empty(M, dtype=torch.int32, device=dev),
+               flags=torch.zeros(M, dtype=torch.int32, device=dev),
+               mean=torch.empty(M, **f64), s2=torch.empty(M, **f64), var=torch.empty(M, **f64))
+    st = lib().laGP_mle(_ptr(X), N, p, _ptr(Z), _ptr(XX), M, _ptr(idx), n, _ptr(theta_in), float(d0), float(lo),
+                        float(hi), float(g), _ptr(out["theta"]), _ptr(out["loglik"]), _ptr(out["iters"]),
+                        _ptr(out["flags"]), _ptr(out["mean"]), _ptr(out["s2"]), _ptr(out["var"]), _stream(dev))
+    _check(st)
+    return out
+
+
+def local_fit(X, Z, XX, d0, lo, hi, g, n0, n, Nprime, stages=2, form="incremental", timing=False):
+    """laGP_local_fit (Fig 1 steps 1-5): NN pool once, then ``stages`` times
+    {local design with theta_x, theta_x = MLE}, then the prediction. Returns idx
+    (last design), theta [stages×M], mean, s2, var, flags, status (+ timing)."""
+    X = _dev(X, "X")
+    Z = _dev(Z, "Z")
+    XX = _dev(XX, "XX")
+    dev = X.device
+    N, p = X.shape
+    M = XX.shape[0]
+    f64 = dict(dtype=torch.float64, device=dev)
+    out = dict(idx=torch.empty((M, n), dtype=torch.int32, device=dev), theta=torch.empty((stages, M), **f64),
+               mean=torch.empty(M, **f64), s2=torch.empty(M, **f64), var=torch.empty(M, **f64),
+               flags=torch.empty(M, dtype=torch.int32, device=dev))
+    tm = Timing()
+    st = lib().laGP_local_fit(_ptr(X), N, p, _ptr(Z), _ptr(XX), M, float(d0), float(lo), float(hi), float(g),
+                              int(n0), int(n), int(Nprime), int(stages), FORMS[form], _ptr(out["idx"]),
+                              _ptr(out["theta"]), _ptr(out["mean"]), _ptr(out["s2"]), _ptr(out["var"]),
+                              _ptr(out["flags"]), ctypes.byref(tm) if timing else None, _stream(dev))
     _check(st, (LAGP_OK, LAGP_PARTIAL))
     out["status"] = st
     if timing:

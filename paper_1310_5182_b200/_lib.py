@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(_PKG, "liblagp_b200.so")
 
 LAGP_OK, LAGP_PARTIAL, LAGP_EINVAL, LAGP_ECUDA, LAGP_ENOMEM = 0, 1, 2, 3, 4
 FLAG_NEAR_TIE, FLAG_SENTINEL, FLAG_EXHAUSTED, FLAG_NONFINITE = 1, 2, 4, 8
+FLAG_MLE_BOUND, FLAG_MLE_MAXIT, FLAG_MLE_FAIL = 16, 32, 64
 ALC_EXPLICIT, ALC_INCREMENTAL, ALC_EXPLICIT_DFMA = 0, 1, 2
 NMAX, PMAX = 128, 16
 
@@ -25,6 +26,9 @@ EXPORTS = (
     "laGP_alc_scores",
     "laGP_pinv_update",
     "laGP_predict",
+    "laGP_alc_batch_theta",
+    "laGP_mle",
+    "laGP_local_fit",
     "lagp_last_error",
     "lagp_abi_version",
 )
@@ -61,6 +65,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.laGP_alc_scores.argtypes = [_i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _vp, _vp, _vp, _vp]
     lib.laGP_pinv_update.argtypes = [_i32, _i32, _vp, _vp, _dbl, _vp, _vp]
     lib.laGP_predict.argtypes = [_i32, _i32, _i32, _vp, _vp, _vp, _dbl, _dbl, _vp, _vp, _vp, _vp]
+    lib.laGP_alc_batch_theta.argtypes = [_vp, _i64, _i32, _vp, _vp, _i64, _vp, _dbl, _dbl, _i32, _i32, _i32,
+                                         _vp, _vp, _vp, _vp, _vp, _vp, _i32, ctypes.POINTER(Timing), _vp]
+    lib.laGP_mle.argtypes = [_vp, _i64, _i32, _vp, _vp, _i64, _vp, _i32, _vp, _dbl, _dbl, _dbl, _dbl,
+                             _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+    lib.laGP_local_fit.argtypes = [_vp, _i64, _i32, _vp, _vp, _i64, _dbl, _dbl, _dbl, _dbl, _i32, _i32, _i32,
+                                   _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.POINTER(Timing), _vp]
     for f in EXPORTS[:-2]:
         getattr(lib, f).restype = ctypes.c_int
     lib.lagp_last_error.argtypes = []

@@ -104,58 +104,100 @@ extern "C" {
 const char *lagp_last_error(void) { return g_err.c_str(); }
 int lagp_abi_version(void) { return LAGP_ABI_VERSION; }
 
-lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const double *Z, const double *XX, int64_t M,
-                              double d, double g, int32_t n0, int32_t n, int32_t Nprime, int32_t *idx_out,
-                              double *mean_out, double *s2_out, double *var_out, uint32_t *flags_out,
-                              double *gap_out, int32_t alc_form, lagp_timing *timing, void *cuda_stream) {
-    lagp_status chk = check_batch_args(X, N, p, Z, XX, M, d, g, n0, n, Nprime, idx_out, mean_out, s2_out);
-    if (chk != LAGP_OK) return chk;
+}  // extern "C"
+
+namespace {
+
+// Launch configuration of the local-design kernels for one call (rows a2-a5).
+struct DesignPlan {
+    int sms = 1, ld = 0, Npad = 0;
+    int64_t cache_stride = 0;
+    bool incremental = false, use_cluster = false, use_dmma = false;
+    lagp::IncPlan inc{};
+    int alc_grid = 0, nn_grid = 0;
+    int64_t chunk = 0;
+};
+
+lagp_status check_form(int32_t alc_form) {
     if (alc_form != LAGP_ALC_EXPLICIT && alc_form != LAGP_ALC_INCREMENTAL && alc_form != LAGP_ALC_EXPLICIT_DFMA)
         return fail(LAGP_EINVAL,
                     "alc_form must be LAGP_ALC_EXPLICIT, LAGP_ALC_INCREMENTAL or LAGP_ALC_EXPLICIT_DFMA (got %d)",
                     alc_form);
+    return LAGP_OK;
+}
+
+// (queries the device: call only when there is work)
+lagp_status plan_design(int32_t p, int32_t n, int32_t Nprime, int64_t M, int32_t alc_form, DesignPlan &P) {
+    P.sms = num_sms();
+    P.ld = (n + 3) & ~3;
+    P.Npad = (Nprime + 3) & ~3;
+    P.cache_stride = (int64_t)n * P.Npad + 1024;  // + max tile width (tile overrun)
+    P.incremental = alc_form == LAGP_ALC_INCREMENTAL;
+    // incremental form: the single-CTA kernel by default; LAGP_CLUSTER=1 selects the
+    // 2-CTA cluster variant (measured slower on C2: 27.8 vs 15.1 ms, DESIGN.md §5.7)
+    const char *cl = getenv("LAGP_CLUSTER");
+    P.use_cluster = P.incremental && lagp::inc_cluster_supported(n, p, Nprime) && (cl && cl[0] == '1');
+    // explicit form: DMMA (FP64 tensor) micro-kernel for n <= 64, DFMA otherwise
+    P.use_dmma = (alc_form == LAGP_ALC_EXPLICIT) && n <= 64;
+    int alc_bps = 0;
+    if (P.incremental) {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        P.inc = lagp::inc_plan(n, p, Nprime, P.Npad, (size_t)optin - 2048);
+        if (!P.inc.ok)
+            return fail(LAGP_EINVAL, "incremental form: Nprime=%d / n=%d exceed this build's limits", Nprime, n);
+        alc_bps = 1;
+        P.cache_stride = (int64_t)P.inc.global_entries * P.Npad + 1024;
+    } else {
+        alc_bps = P.use_dmma ? lagp::alc_explicit_dmma_blocks_per_sm(n, p, P.Npad)
+                             : lagp::alc_explicit_blocks_per_sm(P.ld, n, p, P.Npad);
+    }
+    if (alc_bps <= 0)
+        return fail(LAGP_EINVAL, "local-design state does not fit in shared memory (n=%d, Nprime=%d)", n, Nprime);
+    const int alc_grid_max = alc_bps * P.sms;
+    // chunk of locations per NN+ALC round: bounds the pool buffer (chunk × N' int32)
+    // (at most 65,536 locations and a ~1 GiB pool buffer per chunk)
+    P.chunk = M < 65536 ? M : 65536;
+    const int64_t chunk_pool = ((int64_t)1 << 28) / Nprime;
+    if (P.chunk > chunk_pool) P.chunk = chunk_pool > 1 ? chunk_pool : 1;
+    P.nn_grid = lagp::nn_grid(P.chunk, P.sms, Nprime);
+    P.alc_grid = (int)(P.chunk < alc_grid_max ? P.chunk : alc_grid_max);
+    return LAGP_OK;
+}
+
+cudaError_t launch_design(const DesignPlan &P, const lagp::AlcArgs &a, cudaStream_t st) {
+    const int grid = (int)(a.M < P.alc_grid ? a.M : P.alc_grid);
+    if (P.incremental && P.use_cluster) return lagp::launch_alc_inc_cluster(a, P.sms, st);
+    if (P.incremental) return lagp::launch_alc_incremental(a, P.inc, grid, st);
+    return P.use_dmma ? lagp::launch_alc_explicit_dmma(a, grid, st) : lagp::launch_alc_explicit(a, grid, st);
+}
+
+lagp::AlcArgs design_args(const DesignPlan &P, const double *X, int64_t N, int32_t p, const double *Z, double d,
+                          double g, int32_t n0, int32_t n, int32_t Nprime) {
+    lagp::AlcArgs a{};
+    a.X = X; a.N = N; a.p = p; a.Z = Z;
+    a.eta = g; a.rtheta = 1.0 / d; a.theta_vec = nullptr;
+    a.n0 = n0; a.n = n; a.Nprime = Nprime; a.ld = P.ld; a.Npad = P.Npad; a.cache_stride = P.cache_stride;
+    return a;
+}
+
+lagp_status alc_batch_impl(const double *X, int64_t N, int32_t p, const double *Z, const double *XX, int64_t M,
+                           const double *theta, double d, double g, int32_t n0, int32_t n, int32_t Nprime,
+                           int32_t *idx_out, double *mean_out, double *s2_out, double *var_out, uint32_t *flags_out,
+                           double *gap_out, int32_t alc_form, lagp_timing *timing, void *cuda_stream) {
+    lagp_status chk = check_batch_args(X, N, p, Z, XX, M, d, g, n0, n, Nprime, idx_out, mean_out, s2_out);
+    if (chk != LAGP_OK) return chk;
+    chk = check_form(alc_form);
+    if (chk != LAGP_OK) return chk;
     cudaStream_t st = (cudaStream_t)cuda_stream;
     lagp_status st_ret = LAGP_OK;
     if (timing) std::memset(timing, 0, sizeof *timing);
     if (M == 0) return LAGP_OK;
+    DesignPlan P;
+    chk = plan_design(p, n, Nprime, M, alc_form, P);
+    if (chk != LAGP_OK) return chk;
     cudaGetLastError();  // this library's (static) runtime state only: start from a clean error slot
-
-    const int sms = num_sms();
-    const int ld = (n + 3) & ~3;
-    const int Npad = (Nprime + 3) & ~3;
-    int64_t cache_stride = (int64_t)n * Npad + 1024;  // + max tile width (tile overrun)
-    const bool incremental = alc_form == LAGP_ALC_INCREMENTAL;
-    // incremental form: the single-CTA kernel by default; LAGP_CLUSTER=1 selects the
-    // 2-CTA cluster variant (measured slower on C2: 27.8 vs 15.1 ms, DESIGN.md §5.7)
-    const char *cl = getenv("LAGP_CLUSTER");
-    const bool use_cluster = incremental && lagp::inc_cluster_supported(n, p, Nprime) && (cl && cl[0] == '1');
-    // explicit form: DMMA (FP64 tensor) micro-kernel for n <= 64, DFMA otherwise
-    const bool use_dmma = (alc_form == LAGP_ALC_EXPLICIT) && n <= 64;
-    lagp::IncPlan plan{};
-    int alc_bps = 0;
-    if (incremental) {
-        int dev = 0, optin = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        plan = lagp::inc_plan(n, p, Nprime, Npad, (size_t)optin - 2048);
-        if (!plan.ok)
-            return fail(LAGP_EINVAL, "incremental form: Nprime=%d / n=%d exceed this build's limits", Nprime, n);
-        alc_bps = 1;
-        cache_stride = (int64_t)plan.global_entries * Npad + 1024;
-    } else {
-        alc_bps = use_dmma ? lagp::alc_explicit_dmma_blocks_per_sm(n, p, Npad)
-                           : lagp::alc_explicit_blocks_per_sm(ld, n, p, Npad);
-    }
-    if (alc_bps <= 0)
-        return fail(LAGP_EINVAL, "local-design state does not fit in shared memory (n=%d, Nprime=%d)", n, Nprime);
-    const int alc_grid_max = alc_bps * sms;
-    // chunk of locations per NN+ALC round: bounds the pool buffer (chunk × N' int32)
-    // (at most 65,536 locations and a ~1 GiB pool buffer per chunk)
-    int64_t chunk = M < 65536 ? M : 65536;
-    const int64_t chunk_pool = ((int64_t)1 << 28) / Nprime;
-    if (chunk > chunk_pool) chunk = chunk_pool > 1 ? chunk_pool : 1;
-    const int nn_grid = lagp::nn_grid(chunk, sms, Nprime);
-    const int alc_grid = (int)(chunk < alc_grid_max ? chunk : alc_grid_max);
 
     Workspace ws(st);
     int32_t *pool = nullptr;
@@ -167,27 +209,26 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
     int launches = 0;
     int host_counters[2] = {0, 0};
 
-    LAGP_CUDA(ws.alloc((void **)&pool, (size_t)chunk * Nprime * sizeof(int32_t)));
-    LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(nn_grid, N, p, Nprime, false)));
-    LAGP_CUDA(ws.alloc((void **)&cache, (size_t)alc_grid * cache_stride * sizeof(double)));
+    LAGP_CUDA(ws.alloc((void **)&pool, (size_t)P.chunk * Nprime * sizeof(int32_t)));
+    LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(P.nn_grid, N, p, Nprime, false)));
+    LAGP_CUDA(ws.alloc((void **)&cache, (size_t)P.alc_grid * P.cache_stride * sizeof(double)));
     // per-CTA slab: pool coordinates [p][Npad] (+ kappa and chosen flags for the DFMA kernel)
-    LAGP_CUDA(ws.alloc((void **)&coords, (size_t)alc_grid * (p + 2) * Npad * sizeof(double)));
+    LAGP_CUDA(ws.alloc((void **)&coords, (size_t)P.alc_grid * (p + 2) * P.Npad * sizeof(double)));
     LAGP_CUDA(ws.alloc((void **)&counters, 2 * sizeof(int)));
     LAGP_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int), st));
     if (timing)
         for (int i = 0; i < 4; i++) LAGP_CUDA(cudaEventCreate(&ev[i]));
     if (timing) LAGP_CUDA(cudaEventRecord(ev[0], st));
 
-    for (int64_t m0 = 0; m0 < M; m0 += chunk) {
-        const int64_t mc = (M - m0) < chunk ? (M - m0) : chunk;
+    for (int64_t m0 = 0; m0 < M; m0 += P.chunk) {
+        const int64_t mc = (M - m0) < P.chunk ? (M - m0) : P.chunk;
         if (timing) LAGP_CUDA(cudaEventRecord(ev[1], st));
         LAGP_CUDA(lagp::launch_nn(X, N, p, XX + m0 * p, mc, Nprime, n0, false, pool, nullptr, nnws,
-                                  lagp::nn_grid(mc, sms, Nprime), counters + 1, st, m0 > 0, &launches));
+                                  lagp::nn_grid(mc, P.sms, Nprime), counters + 1, st, m0 > 0, &launches));
         if (timing) LAGP_CUDA(cudaEventRecord(ev[2], st));
-        lagp::AlcArgs a;
-        a.X = X; a.N = N; a.p = p; a.Z = Z; a.XX = XX + m0 * p; a.M = mc;
-        a.eta = g; a.rtheta = 1.0 / d;
-        a.n0 = n0; a.n = n; a.Nprime = Nprime; a.ld = ld; a.Npad = Npad; a.cache_stride = cache_stride;
+        lagp::AlcArgs a = design_args(P, X, N, p, Z, d, g, n0, n, Nprime);
+        a.XX = XX + m0 * p; a.M = mc;
+        a.theta_vec = theta ? theta + m0 : nullptr;
         a.pool = pool;
         a.idx_out = idx_out + m0 * n;
         a.mean = mean_out + m0; a.s2 = s2_out + m0;
@@ -196,13 +237,7 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
         a.gap_out = gap_out ? gap_out + m0 * (n - n0) : nullptr;
         a.cache = cache; a.coords = coords;
         a.n_partial = counters;
-        int grid = (int)(mc < alc_grid ? mc : alc_grid);
-        if (incremental && use_cluster)
-            LAGP_CUDA(lagp::launch_alc_inc_cluster(a, sms, st));
-        else if (incremental)
-            LAGP_CUDA(lagp::launch_alc_incremental(a, plan, grid, st));
-        else
-            LAGP_CUDA(use_dmma ? lagp::launch_alc_explicit_dmma(a, grid, st) : lagp::launch_alc_explicit(a, grid, st));
+        LAGP_CUDA(launch_design(P, a, st));
         launches++;
         if (timing) {
             LAGP_CUDA(cudaEventRecord(ev[3], st));
@@ -232,6 +267,215 @@ lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const doubl
     }
 cleanup:
     for (int i = 0; i < 4; i++)
+        if (ev[i]) cudaEventDestroy(ev[i]);
+    return st_ret;
+}
+
+lagp_status check_mle_args(int64_t N, int32_t p, int64_t M, int32_t n, double theta0, double tmin, double tmax,
+                           double g) {
+    if (N < 1 || N > INT32_MAX) return fail(LAGP_EINVAL, "N must be in [1, 2^31-1] (got %lld)", (long long)N);
+    if (p < 1 || p > LAGP_PMAX) return fail(LAGP_EINVAL, "p must be in [1, %d] (got %d)", LAGP_PMAX, p);
+    if (M < 0) return fail(LAGP_EINVAL, "M must be >= 0 (got %lld)", (long long)M);
+    if (n < 1 || n > LAGP_NMAX) return fail(LAGP_EINVAL, "n must be in [1, %d] (got %d)", LAGP_NMAX, n);
+    if (!finite_pos(theta0)) return fail(LAGP_EINVAL, "theta0 must be finite and > 0 (got %g)", theta0);
+    if (!finite_pos(tmin) || !finite_pos(tmax) || tmin > tmax)
+        return fail(LAGP_EINVAL, "need 0 < theta_min <= theta_max, finite (got %g, %g)", tmin, tmax);
+    if (!(std::isfinite(g) && g >= 0.0)) return fail(LAGP_EINVAL, "g (eta) must be finite and >= 0 (got %g)", g);
+    return LAGP_OK;
+}
+
+// MLE launch plan: matrices in shared memory when they fit, else per-CTA HBM slabs
+struct MlePlan {
+    bool smem = false;
+    int grid = 0;
+    size_t ws = 0;
+};
+
+MlePlan plan_mle(int64_t M, int n, int p) {
+    MlePlan m;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    m.smem = lagp::mle_smem_bytes(n, p) + 2048 <= (size_t)optin;
+    int bps = lagp::mle_blocks_per_sm(n, p, m.smem);
+    if (bps < 1) bps = 1;
+    const int64_t g = (int64_t)bps * num_sms();
+    m.grid = (int)(M < g ? (M > 0 ? M : 1) : g);
+    m.ws = lagp::mle_ws_bytes(m.grid, n, p, m.smem);
+    return m;
+}
+
+}  // namespace
+
+extern "C" {
+
+lagp_status laGP_alc_batch_ex(const double *X, int64_t N, int32_t p, const double *Z, const double *XX, int64_t M,
+                              double d, double g, int32_t n0, int32_t n, int32_t Nprime, int32_t *idx_out,
+                              double *mean_out, double *s2_out, double *var_out, uint32_t *flags_out,
+                              double *gap_out, int32_t alc_form, lagp_timing *timing, void *cuda_stream) {
+    return alc_batch_impl(X, N, p, Z, XX, M, nullptr, d, g, n0, n, Nprime, idx_out, mean_out, s2_out, var_out,
+                          flags_out, gap_out, alc_form, timing, cuda_stream);
+}
+
+lagp_status laGP_alc_batch_theta(const double *X, int64_t N, int32_t p, const double *Z, const double *XX, int64_t M,
+                                 const double *theta, double d, double g, int32_t n0, int32_t n, int32_t Nprime,
+                                 int32_t *idx_out, double *mean_out, double *s2_out, double *var_out,
+                                 uint32_t *flags_out, double *gap_out, int32_t alc_form, lagp_timing *timing,
+                                 void *cuda_stream) {
+    if (M > 0 && !theta) return fail(LAGP_EINVAL, "theta must be non-NULL when M > 0");
+    return alc_batch_impl(X, N, p, Z, XX, M, theta, d, g, n0, n, Nprime, idx_out, mean_out, s2_out, var_out,
+                          flags_out, gap_out, alc_form, timing, cuda_stream);
+}
+
+lagp_status laGP_mle(const double *X, int64_t N, int32_t p, const double *Z, const double *XX, int64_t M,
+                     const int32_t *idx, int32_t n, const double *theta_in, double theta0, double theta_min,
+                     double theta_max, double g, double *theta_out, double *loglik_out, int32_t *iters_out,
+                     uint32_t *flags_out, double *mean_out, double *s2_out, double *var_out, void *cuda_stream) {
+    lagp_status chk = check_mle_args(N, p, M, n, theta0, theta_min, theta_max, g);
+    if (chk != LAGP_OK) return chk;
+    if (!X || !Z) return fail(LAGP_EINVAL, "X and Z must be non-NULL");
+    if (M > 0 && (!XX || !idx || !theta_out || !mean_out || !s2_out))
+        return fail(LAGP_EINVAL, "XX, idx, theta_out, mean_out and s2_out must be non-NULL when M > 0");
+    if (M == 0) return LAGP_OK;
+    cudaGetLastError();
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    lagp_status st_ret = LAGP_OK;
+    {
+        Workspace ws(st);
+        const MlePlan mp = plan_mle(M, n, p);
+        lagp::MleArgs a{};
+        a.X = X; a.p = p; a.Z = Z; a.XX = XX; a.idx = idx; a.M = M; a.n = n;
+        a.theta_in = theta_in; a.theta0 = theta0; a.lo = theta_min; a.hi = theta_max; a.eta = g;
+        a.theta_out = theta_out; a.loglik_out = loglik_out; a.iters_out = iters_out; a.flags_out = flags_out;
+        a.mean = mean_out; a.s2 = s2_out; a.var = var_out;
+        a.use_smem = mp.smem ? 1 : 0;
+        if (!mp.smem) LAGP_CUDA(ws.alloc((void **)&a.ws, mp.ws));
+        LAGP_CUDA(lagp::launch_mle(a, mp.grid, st));
+    cleanup:;
+    }
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess && st_ret == LAGP_OK) st_ret = cuda_fail(e, "cudaStreamSynchronize");
+    return st_ret;
+}
+
+lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *Z, const double *XX, int64_t M,
+                           double theta0, double theta_min, double theta_max, double g, int32_t n0, int32_t n,
+                           int32_t Nprime, int32_t stages, int32_t alc_form, int32_t *idx_out, double *theta_out,
+                           double *mean_out, double *s2_out, double *var_out, uint32_t *flags_out,
+                           lagp_timing *timing, void *cuda_stream) {
+    lagp_status chk = check_batch_args(X, N, p, Z, XX, M, theta0, g, n0, n, Nprime, idx_out, mean_out, s2_out);
+    if (chk != LAGP_OK) return chk;
+    chk = check_mle_args(N, p, M, n, theta0, theta_min, theta_max, g);
+    if (chk != LAGP_OK) return chk;
+    if (stages < 1 || stages > 16) return fail(LAGP_EINVAL, "stages must be in [1, 16] (got %d)", stages);
+    if (M > 0 && !theta_out) return fail(LAGP_EINVAL, "theta_out must be non-NULL when M > 0");
+    chk = check_form(alc_form);
+    if (chk != LAGP_OK) return chk;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    lagp_status st_ret = LAGP_OK;
+    if (timing) std::memset(timing, 0, sizeof *timing);
+    if (M == 0) return LAGP_OK;
+    DesignPlan P;
+    chk = plan_design(p, n, Nprime, M, alc_form, P);
+    if (chk != LAGP_OK) return chk;
+    cudaGetLastError();
+
+    Workspace ws(st);
+    int32_t *pool = nullptr;
+    void *nnws = nullptr;
+    double *cache = nullptr, *coords = nullptr, *mlews = nullptr;
+    uint32_t *fl = nullptr;
+    int *counters = nullptr;
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    float nn_ms = 0.f, alc_ms = 0.f, mle_ms = 0.f, tot_ms = 0.f;
+    int launches = 0;
+    int host_counters[2] = {0, 0};
+    const MlePlan mp = plan_mle(P.chunk, n, p);
+
+    LAGP_CUDA(ws.alloc((void **)&pool, (size_t)P.chunk * Nprime * sizeof(int32_t)));
+    LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(P.nn_grid, N, p, Nprime, false)));
+    LAGP_CUDA(ws.alloc((void **)&cache, (size_t)P.alc_grid * P.cache_stride * sizeof(double)));
+    LAGP_CUDA(ws.alloc((void **)&coords, (size_t)P.alc_grid * (p + 2) * P.Npad * sizeof(double)));
+    LAGP_CUDA(ws.alloc((void **)&counters, 2 * sizeof(int)));
+    if (!flags_out) LAGP_CUDA(ws.alloc((void **)&fl, (size_t)P.chunk * sizeof(uint32_t)));
+    if (!mp.smem) LAGP_CUDA(ws.alloc((void **)&mlews, mp.ws));
+    LAGP_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int), st));
+    if (timing)
+        for (int i = 0; i < 5; i++) LAGP_CUDA(cudaEventCreate(&ev[i]));
+    if (timing) LAGP_CUDA(cudaEventRecord(ev[0], st));
+
+    for (int64_t m0 = 0; m0 < M; m0 += P.chunk) {
+        const int64_t mc = (M - m0) < P.chunk ? (M - m0) : P.chunk;
+        if (timing) LAGP_CUDA(cudaEventRecord(ev[1], st));
+        LAGP_CUDA(lagp::launch_nn(X, N, p, XX + m0 * p, mc, Nprime, n0, false, pool, nullptr, nnws,
+                                  lagp::nn_grid(mc, P.sms, Nprime), counters + 1, st, m0 > 0, &launches));
+        if (timing) {
+            LAGP_CUDA(cudaEventRecord(ev[2], st));
+            LAGP_CUDA(cudaEventSynchronize(ev[2]));
+            float t = 0.f;
+            cudaEventElapsedTime(&t, ev[1], ev[2]);
+            nn_ms += t;
+        }
+        uint32_t *flc = flags_out ? flags_out + m0 : fl;
+        for (int s = 0; s < stages; s++) {
+            if (timing) LAGP_CUDA(cudaEventRecord(ev[2], st));
+            // step 2 with theta_x (stage 0: the global theta0)
+            lagp::AlcArgs a = design_args(P, X, N, p, Z, theta0, g, n0, n, Nprime);
+            a.XX = XX + m0 * p; a.M = mc;
+            a.theta_vec = s == 0 ? nullptr : theta_out + (size_t)(s - 1) * M + m0;
+            a.pool = pool;
+            a.idx_out = idx_out + m0 * n;
+            a.mean = mean_out + m0; a.s2 = s2_out + m0;
+            a.var = var_out ? var_out + m0 : nullptr;
+            a.flags = flc;
+            a.gap_out = nullptr;
+            a.cache = cache; a.coords = coords;
+            a.n_partial = counters;
+            LAGP_CUDA(launch_design(P, a, st));
+            launches++;
+            if (timing) LAGP_CUDA(cudaEventRecord(ev[3], st));
+            // step 3: theta_x = theta-hat_n(x) | D_n(x, theta_x), and step 5 at it
+            lagp::MleArgs ma{};
+            ma.X = X; ma.p = p; ma.Z = Z; ma.XX = XX + m0 * p; ma.idx = idx_out + m0 * n; ma.M = mc; ma.n = n;
+            ma.theta_in = s == 0 ? nullptr : theta_out + (size_t)(s - 1) * M + m0;
+            ma.theta0 = theta0; ma.lo = theta_min; ma.hi = theta_max; ma.eta = g;
+            ma.theta_out = theta_out + (size_t)s * M + m0;
+            ma.flags_out = flc;
+            ma.mean = mean_out + m0; ma.s2 = s2_out + m0; ma.var = var_out ? var_out + m0 : nullptr;
+            ma.use_smem = mp.smem ? 1 : 0;
+            ma.ws = mlews;
+            const int mgrid = (int)(mc < mp.grid ? mc : mp.grid);
+            LAGP_CUDA(lagp::launch_mle(ma, mgrid, st));
+            launches++;
+            if (timing) {
+                LAGP_CUDA(cudaEventRecord(ev[4], st));
+                LAGP_CUDA(cudaEventSynchronize(ev[4]));
+                float t1 = 0.f, t2 = 0.f;
+                cudaEventElapsedTime(&t1, ev[2], ev[3]);
+                cudaEventElapsedTime(&t2, ev[3], ev[4]);
+                alc_ms += t1;
+                mle_ms += t2;
+            }
+        }
+    }
+    LAGP_CUDA(cudaMemcpyAsync(host_counters, counters, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (timing) LAGP_CUDA(cudaEventRecord(ev[4], st));
+    LAGP_CUDA(cudaStreamSynchronize(st));
+    if (timing) {
+        cudaEventElapsedTime(&tot_ms, ev[0], ev[4]);
+        timing->nn_ms = nn_ms;
+        timing->alc_ms = alc_ms;
+        timing->predict_ms = mle_ms;
+        timing->total_ms = tot_ms;
+        timing->launches = launches;
+        timing->nn_fallbacks = host_counters[1];
+    }
+    if (host_counters[0] > 0) {
+        fail(LAGP_PARTIAL, "%d location-stage(s) flagged EXHAUSTED or NONFINITE", host_counters[0]);
+        st_ret = LAGP_PARTIAL;
+    }
+cleanup:
+    for (int i = 0; i < 5; i++)
         if (ev[i]) cudaEventDestroy(ev[i]);
     return st_ret;
 }

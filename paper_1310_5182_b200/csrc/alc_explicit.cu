@@ -125,10 +125,11 @@ alc_explicit_kernel(AlcArgs A) {
     double *coords = A.coords + (size_t)blockIdx.x * (p + 2) * Npad;  // [p][Npad] coords | kap | chosen
     double *kap = coords + (size_t)p * Npad;
     unsigned char *chosen = reinterpret_cast<unsigned char *>(kap + Npad);
-    const double rth = A.rtheta, eta = A.eta;
+    const double eta = A.eta;
     const int G = n - A.n0;
 
     for (int64_t xi = blockIdx.x; xi < A.M; xi += gridDim.x) {
+        const double rth = A.theta_vec ? 1.0 / A.theta_vec[xi] : A.rtheta;  // per-location theta (Fig 1 step 4)
         const int32_t *pool = A.pool + xi * (int64_t)Np;
         int32_t *idx = A.idx_out + xi * (int64_t)n;
         if (tid < p) xq[tid] = A.XX[xi * p + tid];

@@ -71,11 +71,12 @@ alc_incremental_kernel(AlcArgs A, int S) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     double *gw = A.cache + (size_t)blockIdx.x * A.cache_stride;  // entries >= R+S: gw[(a-R-S)*Npad + c]
     double *coords = A.coords + (size_t)blockIdx.x * p * Npad;   // generic-p path only
-    const double rth = A.rtheta, eta = A.eta;
+    const double eta = A.eta;
     const int G = n - n0;
     const int RS = R + S;
 
     for (int64_t xi = blockIdx.x; xi < A.M; xi += gridDim.x) {
+        const double rth = A.theta_vec ? 1.0 / A.theta_vec[xi] : A.rtheta;  // per-location theta (Fig 1 step 4)
         const int32_t *pool = A.pool + xi * (int64_t)Np;
         int32_t *idx = A.idx_out + xi * (int64_t)n;
         if (tid < p) sh[0].xq[tid] = A.XX[xi * p + tid];

@@ -57,12 +57,13 @@ alc_inc_cluster_kernel(AlcArgs A, int S) {
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int c = (int)rank * CL_THREADS + tid;  // pool position owned by this thread
-    const double rth = A.rtheta, eta = A.eta;
+    const double eta = A.eta;
     const int G = n - n0;
     const int nclusters = gridDim.x / 2;
     const int cid = blockIdx.x / 2;
 
     for (int64_t xi = cid; xi < A.M; xi += nclusters) {
+        const double rth = A.theta_vec ? 1.0 / A.theta_vec[xi] : A.rtheta;  // per-location theta (Fig 1 step 4)
         const int32_t *pool = A.pool + xi * (int64_t)Np;
         int32_t *idx = A.idx_out + xi * (int64_t)n;
         if (tid < P) xq[tid] = A.XX[xi * P + tid];

@@ -24,6 +24,7 @@ struct AlcArgs {
     const double *XX;
     int64_t M;
     double eta, rtheta;
+    const double *theta_vec;  // [M] per-location theta (multi-stage scheme), nullptr = 1/rtheta everywhere
     int n0, n, Nprime, ld;
     int Npad;             // Nprime rounded up to a multiple of 4 (16-byte rows)
     int64_t cache_stride; // doubles per CTA cache slab (n*Npad + tile overrun pad)
@@ -57,6 +58,30 @@ bool inc_cluster_supported(int n, int p, int Nprime);
 cudaError_t launch_alc_inc_cluster(const AlcArgs &a, int num_sms, cudaStream_t st);
 cudaError_t launch_alc_incremental(const AlcArgs &a, const IncPlan &pl, int grid, cudaStream_t st);
 int alc_explicit_dmma_blocks_per_sm(int n, int p, int Npad);
+
+// mle.cu (row f2): local MLE of theta on given designs + prediction at theta-hat
+struct MleArgs {
+    const double *X;
+    int p;
+    const double *Z;
+    const double *XX;
+    const int32_t *idx;     // [M][n] local designs (-1 tail = exhausted)
+    int64_t M;
+    int n;
+    const double *theta_in; // [M] starting theta, nullptr = theta0
+    double theta0, lo, hi, eta;
+    double *theta_out;      // [M]
+    double *loglik_out;     // [M] nullable
+    int32_t *iters_out;     // [M] nullable
+    uint32_t *flags_out;    // [M] nullable, OR-ed
+    double *mean, *s2, *var;  // [M] (var nullable): prediction at theta-hat
+    double *ws;             // per-CTA matrices when they do not fit in shared memory
+    int use_smem;
+};
+size_t mle_smem_bytes(int n, int p);
+size_t mle_ws_bytes(int grid, int n, int p, bool use_smem);
+int mle_blocks_per_sm(int n, int p, bool use_smem);
+cudaError_t launch_mle(const MleArgs &a, int grid, cudaStream_t st);
 
 // diag.cu (rows a3, a4, a5 alone)
 cudaError_t launch_alc_scores(int B, int j, int p, int nc, const double *Xj, const double *Kinv, const double *cands,

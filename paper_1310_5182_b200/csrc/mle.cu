@@ -1,0 +1,326 @@
+// mle.cu — row f2: the local MLE theta-hat_n(x) | D_n(x) of Fig 1
+// step 3 on the concentrated likelihood Eq (3), by the
+// safeguarded Newton of reading R21 on tau = log(theta), with the analytic
+// derivatives of reading R20; then the step-5 prediction (Eq (1)-(2))
+// at theta-hat on the same D_n(x).
+//
+//   l(theta)  = lgamma(n/2) - (n/2) log(2 pi) - (1/2) log|K| - (n/2) log(psi/2)
+//   P = dK/dtau   = C o (D/theta),   Q = d2K/dtau2 = C o (D/theta) o (D/theta - 1)
+//   dl/dtau   = -1/2 tr(A P) + (n/2) a^T P a / psi                 (A = K^{-1}, a = A Y)
+//   d2l/dtau2 = -1/2 tr(A Q) + 1/2 tr(A P A P) - (n/2)(2 v^T A v - a^T Q a)/psi
+//               + (n/2)(a^T P a / psi)^2                            (v = P a)
+//
+// B200 mapping: one CTA of 256 threads per location (persistent grid). The
+// n×n matrices (D, K/L, W = L^{-1} then T = A P, A) live in shared memory when
+// 4 n^2 doubles fit (n <= 80), else in a per-CTA HBM slab (L2-resident). Every
+// evaluation: K from the stored D (n^2 exp), right-looking Cholesky with one
+// barrier per column, W by per-column forward substitution, A = W^T W, then
+// the traces and quadratic forms as block reductions. The Newton iteration is
+// executed uniformly by all threads on block-reduced scalars.
+#include <cuda_runtime.h>
+
+#include "block_ops.cuh"
+#include "launch.h"
+
+namespace lagp {
+
+constexpr int MLE_THREADS = 256;
+constexpr int MLE_MAXIT = 64;
+
+struct MleEval {
+    double l, g, h, psi;
+    bool ok;
+};
+
+// K = C + eta I from D at 1/theta into L; Cholesky in place (lower, row-major).
+// Returns false when a pivot is not positive.
+__device__ bool mle_chol(const double *D, double *L, int n, double rth, double eta, double *scratch) {
+    const int tid = threadIdx.x;
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        const int a = e / n, b = e - a * n;
+        if (b <= a) L[e] = exp_nonpos(-D[e] * rth) + (a == b ? eta : 0.0);
+    }
+    __shared__ int bad;
+    if (tid == 0) bad = 0;
+    __syncthreads();
+    // column k: every thread takes 1/sqrt(L_kk) itself; the trailing update uses the
+    // unscaled column times that factor, and column k is scaled one step later
+    // (no conflict: step k+1 touches columns >= k+1 only)
+    for (int k = 0; k < n; k++) {
+        const double dkk = L[k * n + k];
+        if (!(dkk > 0.0)) {
+            if (tid == 0) bad = 1;
+            break;  // uniform: every thread read the same pivot
+        }
+        const double rl = 1.0 / sqrt(dkk);
+        if (k > 0) {  // scale column k-1 (its pivot is settled)
+            const double rp = 1.0 / sqrt(L[(k - 1) * n + (k - 1)]);
+            for (int i = k + tid; i < n; i += blockDim.x) L[i * n + (k - 1)] *= rp;
+        }
+        const int m = n - k - 1;
+        for (int e = tid; e < m * m; e += blockDim.x) {
+            const int r = e / m, c = e - r * m;
+            if (c <= r) {
+                const int i = k + 1 + r, jj = k + 1 + c;
+                L[i * n + jj] = fma(-(L[i * n + k] * rl), L[jj * n + k] * rl, L[i * n + jj]);
+            }
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    if (bad) return false;
+    // every column below the diagonal is scaled (column n-1 has no such entries);
+    // the diagonal takes its square roots last
+    for (int k = tid; k < n; k += blockDim.x) L[k * n + k] = sqrt(L[k * n + k]);
+    __syncthreads();
+    (void)scratch;
+    return true;
+}
+
+// W = L^{-1} (lower) by forward substitution, one thread per column; then
+// A = W^T W (symmetric, both triangles).
+__device__ void mle_inverse(const double *L, double *W, double *A, int n) {
+    const int tid = threadIdx.x;
+    for (int c = tid; c < n; c += blockDim.x) {
+        for (int i = 0; i < c; i++) W[i * n + c] = 0.0;
+        W[c * n + c] = 1.0 / L[c * n + c];
+        for (int i = c + 1; i < n; i++) {
+            double s0 = 0.0, s1 = 0.0;
+            int t = c;
+            for (; t + 1 < i; t += 2) {
+                s0 = fma(L[i * n + t], W[t * n + c], s0);
+                s1 = fma(L[i * n + t + 1], W[(t + 1) * n + c], s1);
+            }
+            if (t < i) s0 = fma(L[i * n + t], W[t * n + c], s0);
+            W[i * n + c] = -(s0 + s1) / L[i * n + i];
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        const int a = e / n, b = e - a * n;
+        if (b <= a) {
+            double s = 0.0;
+            for (int t = a; t < n; t++) s = fma(W[t * n + a], W[t * n + b], s);
+            A[a * n + b] = s;
+            A[b * n + a] = s;
+        }
+    }
+    __syncthreads();
+}
+
+// One evaluation of l (and with deriv, dl/dtau, d2l/dtau2) at theta = exp(tau).
+// On return A = K^{-1} and al = A Y at that theta.
+__device__ MleEval mle_eval(double tau, bool deriv, int n, const double *D, double *L, double *W, double *A,
+                            const double *Y, double *al, double *v, double eta, double *scratch) {
+    MleEval r{};
+    r.l = -INFINITY;
+    r.g = r.h = __longlong_as_double(0x7ff8000000000000LL);
+    const int tid = threadIdx.x;
+    const double theta = exp(tau), rth = 1.0 / theta;
+    if (!mle_chol(D, L, n, rth, eta, scratch)) {
+        r.ok = false;
+        return r;
+    }
+    double ld = 0.0;
+    for (int k = tid; k < n; k += blockDim.x) ld += log(L[k * n + k]);
+    const double logdet = 2.0 * block_sum(ld, scratch);
+    mle_inverse(L, W, A, n);
+    double pp = 0.0;
+    for (int a = tid; a < n; a += blockDim.x) {
+        double s = 0.0;
+        for (int b = 0; b < n; b++) s = fma(A[a * n + b], Y[b], s);
+        al[a] = s;
+        pp = fma(Y[a], s, pp);
+    }
+    const double psi = block_sum(pp, scratch);  // (also orders the al writes)
+    r.psi = psi;
+    if (!(psi > 0.0)) {
+        r.ok = false;
+        return r;
+    }
+    const double hn = 0.5 * (double)n;
+    r.l = lgamma(hn) - hn * log(2.0 * 3.14159265358979323846) - 0.5 * logdet - hn * log(0.5 * psi);
+    r.ok = isfinite(r.l);
+    if (!deriv || !r.ok) return r;
+    // P into L's storage (L no longer needed), then T = A P into W's storage
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        const double q = D[e] * rth;
+        L[e] = exp_nonpos(-q) * q;
+    }
+    __syncthreads();
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        const int a = e / n, b = e - a * n;
+        double s = 0.0;
+        for (int t = 0; t < n; t++) s = fma(A[a * n + t], L[t * n + b], s);
+        W[e] = s;
+    }
+    // v = P a (P symmetric)
+    for (int a = tid; a < n; a += blockDim.x) {
+        double s = 0.0;
+        for (int b = 0; b < n; b++) s = fma(L[a * n + b], al[b], s);
+        v[a] = s;
+    }
+    __syncthreads();
+    double tAP = 0.0, tAQ = 0.0, tTT = 0.0, aQa = 0.0, aPa = 0.0, vAv = 0.0;
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        const int a = e / n, b = e - a * n;
+        const double Pab = L[e];
+        const double Qab = Pab * (D[e] * rth - 1.0);
+        tAP = fma(A[e], Pab, tAP);
+        tAQ = fma(A[e], Qab, tAQ);
+        tTT = fma(W[e], W[b * n + a], tTT);
+        aQa = fma(al[a] * Qab, al[b], aQa);
+        aPa = fma(al[a] * Pab, al[b], aPa);
+        vAv = fma(v[a] * A[e], v[b], vAv);
+    }
+    tAP = block_sum(tAP, scratch);
+    tAQ = block_sum(tAQ, scratch);
+    tTT = block_sum(tTT, scratch);
+    aQa = block_sum(aQa, scratch);
+    aPa = block_sum(aPa, scratch);
+    vAv = block_sum(vAv, scratch);
+    const double q = aPa / psi;
+    r.g = -0.5 * tAP + hn * q;
+    r.h = -0.5 * tAQ + 0.5 * tTT - hn * (2.0 * vAv - aQa) / psi + hn * q * q;
+    r.ok = isfinite(r.g) && isfinite(r.h);
+    return r;
+}
+
+__global__ void __launch_bounds__(MLE_THREADS)
+mle_kernel(MleArgs A) {
+    extern __shared__ __align__(16) double sm[];
+    const int n = A.n, p = A.p;
+    const int tid = threadIdx.x;
+    double *mats = A.use_smem ? sm : A.ws + (size_t)blockIdx.x * 4 * n * n;
+    double *vecs = A.use_smem ? sm + 4 * n * n : A.ws + (size_t)gridDim.x * 4 * n * n + (size_t)blockIdx.x * (4 * n + n * p + 64);
+    double *D = mats, *L = D + n * n, *W = L + n * n, *Am = W + n * n;
+    double *Y = vecs, *al = Y + n, *v = al + n, *hv = v + n, *Xn = hv + n;
+    __shared__ double scratch[40];
+    __shared__ int jn_s;
+    const double lo = log(A.lo), hi = log(A.hi);
+
+    for (int64_t xi = blockIdx.x; xi < A.M; xi += gridDim.x) {
+        const int32_t *idx = A.idx + xi * (int64_t)n;
+        if (tid == 0) jn_s = n;
+        __syncthreads();
+        for (int t = tid; t < n; t += blockDim.x)
+            if (idx[t] < 0) atomicMin(&jn_s, t);
+        __syncthreads();
+        const int m = jn_s;  // the design's valid prefix (exhausted designs are shorter)
+        for (int e = tid; e < m * p; e += blockDim.x) Xn[e] = A.X[(int64_t)idx[e / p] * p + (e % p)];
+        for (int a = tid; a < m; a += blockDim.x) Y[a] = A.Z[idx[a]];
+        __syncthreads();
+        for (int e = tid; e < m * m; e += blockDim.x) {
+            const int a = e / m, b = e - a * m;
+            D[e] = sqdist_fma(Xn + a * p, Xn + b * p, p);
+        }
+        __syncthreads();
+
+        const double theta0 = A.theta_in ? A.theta_in[xi] : A.theta0;
+        double tau = fmin(fmax(log(theta0), lo), hi);
+        uint32_t fl = 0;
+        int it = 0;
+        MleEval cur = mle_eval(tau, true, m, D, L, W, Am, Y, al, v, A.eta, scratch);
+        double theta_hat = theta0;
+        if (!cur.ok) {
+            fl |= LAGP_FLAG_MLE_FAIL;
+        } else {
+            for (it = 1; it <= MLE_MAXIT; it++) {
+                if ((tau <= lo && cur.g <= 0.0) || (tau >= hi && cur.g >= 0.0)) break;
+                if (cur.g == 0.0 && !(cur.h < 0.0)) break;
+                double step = (cur.h < 0.0) ? -cur.g / cur.h : (cur.g > 0.0 ? 1.0 : -1.0);
+                step = fmin(fmax(step, -1.0), 1.0);
+                double tn = fmin(fmax(tau + step, lo), hi);
+                MleEval nx = mle_eval(tn, true, m, D, L, W, Am, Y, al, v, A.eta, scratch);
+                if (fabs(step) > 0.25 || !(cur.h < 0.0)) {
+                    for (int t = 0; t < 40 && (!nx.ok || nx.l < cur.l); t++) {
+                        tn = 0.5 * (tau + tn);
+                        nx = mle_eval(tn, true, m, D, L, W, Am, Y, al, v, A.eta, scratch);
+                            }
+                    if (!nx.ok || nx.l < cur.l) break;  // no ascent: stay at tau
+                } else if (!nx.ok) {
+                    break;
+                }
+                const double dt = fabs(tn - tau);
+                tau = tn;
+                cur = nx;
+                if (dt <= 1e-10 * fmax(1.0, fabs(tau))) break;
+            }
+            if (it > MLE_MAXIT) {
+                fl |= LAGP_FLAG_MLE_MAXIT;
+                it = MLE_MAXIT;
+            }
+            if (tau <= lo || tau >= hi) fl |= LAGP_FLAG_MLE_BOUND;
+            theta_hat = exp(tau);
+        }
+        // Fig 1 step 5 at theta-hat (the incoming theta when the MLE failed), from the
+        // factor: with W = L^{-1}, a = W h and b = W Y give mean = a.b, h^T K^{-1} h = a.a,
+        // psi = b.b (the triangular-solve form of Eq (1)-(2), not the explicit inverse)
+        const double tau_p = cur.ok ? tau : log(theta0);
+        const MleEval fin = mle_eval(tau_p, false, m, D, L, W, Am, Y, al, v, A.eta, scratch);
+        const double rth = 1.0 / exp(tau_p);
+        const double *xq = A.XX + xi * p;
+        for (int a = tid; a < m; a += blockDim.x) hv[a] = corr_from_d2(sqdist_fma(Xn + a * p, xq, p), rth);
+        __syncthreads();
+        double pm = 0.0, ph = 0.0, pp = 0.0;
+        for (int a = tid; a < m; a += blockDim.x) {
+            double sa = 0.0, sb = 0.0;
+            for (int b = 0; b <= a; b++) {
+                sa = fma(W[a * m + b], hv[b], sa);
+                sb = fma(W[a * m + b], Y[b], sb);
+            }
+            pm = fma(sa, sb, pm);
+            ph = fma(sa, sa, ph);
+            pp = fma(sb, sb, pp);
+        }
+        const double mu = block_sum(pm, scratch);
+        const double hAh = block_sum(ph, scratch);
+        const double psi_p = block_sum(pp, scratch);
+        if (tid == 0) {
+            const double sc = psi_p * (1.0 + A.eta - hAh) / (double)m;
+            const double vr = m > 2 ? sc * (double)m / (double)(m - 2) : __longlong_as_double(0x7ff8000000000000LL);
+            if (!fin.ok || !isfinite(mu) || !isfinite(sc)) fl |= LAGP_FLAG_NONFINITE;
+            A.theta_out[xi] = theta_hat;
+            if (A.loglik_out) A.loglik_out[xi] = cur.l;
+            if (A.iters_out) A.iters_out[xi] = it;
+            if (A.flags_out) A.flags_out[xi] |= fl;
+            if (A.mean) A.mean[xi] = mu;
+            if (A.s2) A.s2[xi] = sc;
+            if (A.var) A.var[xi] = vr;
+        }
+        __syncthreads();
+    }
+}
+
+size_t mle_smem_bytes(int n, int p) { return ((size_t)4 * n * n + 4 * n + (size_t)n * p + 64) * sizeof(double); }
+
+size_t mle_ws_bytes(int grid, int n, int p, bool use_smem) {
+    if (use_smem) return 0;
+    return (size_t)grid * ((size_t)4 * n * n + 4 * n + (size_t)n * p + 64) * sizeof(double);
+}
+
+int mle_blocks_per_sm(int n, int p, bool use_smem) {
+    const size_t smem = use_smem ? mle_smem_bytes(n, p) : 0;
+    if (use_smem && cudaFuncSetAttribute(mle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, mle_kernel, MLE_THREADS, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return b;
+}
+
+cudaError_t launch_mle(const MleArgs &a, int grid, cudaStream_t st) {
+    const size_t smem = a.use_smem ? mle_smem_bytes(a.n, a.p) : 0;
+    if (a.use_smem) {
+        cudaError_t e = cudaFuncSetAttribute(mle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    mle_kernel<<<grid, MLE_THREADS, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace lagp

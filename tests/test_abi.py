@@ -28,7 +28,8 @@ def declared_symbols():
 def test_header_declares_expected_entry_points():
     syms = declared_symbols()
     for s in ("laGP_alc_batch", "laGP_alc_scores", "lagp_last_error", "lagp_abi_version", "laGP_nn_pool",
-              "laGP_pinv_update", "laGP_predict", "laGP_alc_batch_ex", "laGP_alc_batch_host"):
+              "laGP_pinv_update", "laGP_predict", "laGP_alc_batch_ex", "laGP_alc_batch_host", "laGP_alc_batch_theta",
+              "laGP_mle", "laGP_local_fit"):
         assert s in syms
 
 
@@ -36,7 +37,7 @@ def test_library_exports_every_declared_symbol(lagp):
     lib = lagp.lib()
     for s in declared_symbols():
         assert hasattr(lib, s), s
-    assert lagp.abi_version() == 1
+    assert lagp.abi_version() == 2
 
 
 def test_library_is_sm100a_only(lagp):
