@@ -57,13 +57,12 @@ __device__ bool mle_chol(const double *D, double *L, int n, double rth, double e
             const double rp = 1.0 / sqrt(L[(k - 1) * n + (k - 1)]);
             for (int i = k + tid; i < n; i += blockDim.x) L[i * n + (k - 1)] *= rp;
         }
-        const int m = n - k - 1;
-        for (int e = tid; e < m * m; e += blockDim.x) {
-            const int r = e / m, c = e - r * m;
-            if (c <= r) {
-                const int i = k + 1 + r, jj = k + 1 + c;
-                L[i * n + jj] = fma(-(L[i * n + k] * rl), L[jj * n + k] * rl, L[i * n + jj]);
-            }
+        // trailing update: rows to warps, columns to lanes (no index division)
+        const int lane = tid & 31, nw = blockDim.x >> 5;
+        for (int i = k + 1 + (tid >> 5); i < n; i += nw) {
+            const double li = L[i * n + k] * rl;
+            for (int jj = k + 1 + lane; jj <= i; jj += 32)
+                L[i * n + jj] = fma(-li, L[jj * n + k] * rl, L[i * n + jj]);
         }
         __syncthreads();
     }
@@ -81,9 +80,12 @@ __device__ bool mle_chol(const double *D, double *L, int n, double rth, double e
 // A = W^T W (symmetric, both triangles).
 __device__ void mle_inverse(const double *L, double *W, double *A, int n) {
     const int tid = threadIdx.x;
+    // 1/L_ii first (keeps the divisions off the substitution chains)
+    for (int i = tid; i < n; i += blockDim.x) A[i] = 1.0 / L[i * n + i];
+    __syncthreads();
     for (int c = tid; c < n; c += blockDim.x) {
         for (int i = 0; i < c; i++) W[i * n + c] = 0.0;
-        W[c * n + c] = 1.0 / L[c * n + c];
+        W[c * n + c] = A[c];
         for (int i = c + 1; i < n; i++) {
             double s0 = 0.0, s1 = 0.0;
             int t = c;
@@ -92,19 +94,19 @@ __device__ void mle_inverse(const double *L, double *W, double *A, int n) {
                 s1 = fma(L[i * n + t + 1], W[(t + 1) * n + c], s1);
             }
             if (t < i) s0 = fma(L[i * n + t], W[t * n + c], s0);
-            W[i * n + c] = -(s0 + s1) / L[i * n + i];
+            W[i * n + c] = -(s0 + s1) * A[i];
         }
     }
     __syncthreads();
-    for (int e = tid; e < n * n; e += blockDim.x) {
-        const int a = e / n, b = e - a * n;
-        if (b <= a) {
+    // A = W^T W: rows a to warps, columns b <= a to lanes
+    const int lane = tid & 31, nw = blockDim.x >> 5;
+    for (int a = tid >> 5; a < n; a += nw)
+        for (int b = lane; b <= a; b += 32) {
             double s = 0.0;
             for (int t = a; t < n; t++) s = fma(W[t * n + a], W[t * n + b], s);
             A[a * n + b] = s;
             A[b * n + a] = s;
         }
-    }
     __syncthreads();
 }
 
