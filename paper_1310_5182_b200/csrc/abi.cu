@@ -144,11 +144,19 @@ lagp_status plan_design(int32_t p, int32_t n, int32_t Nprime, int64_t M, int32_t
         int dev = 0, optin = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        P.inc = lagp::inc_plan(n, p, Nprime, P.Npad, (size_t)optin - 2048);
-        if (!P.inc.ok)
-            return fail(LAGP_EINVAL, "incremental form: Nprime=%d / n=%d exceed this build's limits", Nprime, n);
+        // v2 kernel (one barrier per step) where it applies; LAGP_INC_V1=1 forces the
+        // 1024-thread kernel of alc_incremental.cu (kept for N' > 1024 and other p)
+        const char *v1 = getenv("LAGP_INC_V1");
+        const bool force_v1 = v1 && v1[0] == '1';
+        if (force_v1 || P.use_cluster || !lagp::inc_v2_plan(n, p, Nprime, (size_t)optin - 2048, P.inc)) {
+            P.inc = lagp::inc_plan(n, p, Nprime, P.Npad, (size_t)optin - 2048);
+            if (!P.inc.ok)
+                return fail(LAGP_EINVAL, "incremental form: Nprime=%d / n=%d exceed this build's limits", Nprime, n);
+            P.cache_stride = (int64_t)P.inc.global_entries * P.Npad + 1024;
+        } else {
+            P.cache_stride = P.inc.cache_doubles;
+        }
         alc_bps = 1;
-        P.cache_stride = (int64_t)P.inc.global_entries * P.Npad + 1024;
     } else {
         alc_bps = P.use_dmma ? lagp::alc_explicit_dmma_blocks_per_sm(n, p, P.Npad)
                              : lagp::alc_explicit_blocks_per_sm(P.ld, n, p, P.Npad);
@@ -169,6 +177,7 @@ lagp_status plan_design(int32_t p, int32_t n, int32_t Nprime, int64_t M, int32_t
 cudaError_t launch_design(const DesignPlan &P, const lagp::AlcArgs &a, cudaStream_t st) {
     const int grid = (int)(a.M < P.alc_grid ? a.M : P.alc_grid);
     if (P.incremental && P.use_cluster) return lagp::launch_alc_inc_cluster(a, P.sms, st);
+    if (P.incremental && P.inc.v2) return lagp::launch_alc_incremental_v2(a, P.inc, grid, st);
     if (P.incremental) return lagp::launch_alc_incremental(a, P.inc, grid, st);
     return P.use_dmma ? lagp::launch_alc_explicit_dmma(a, grid, st) : lagp::launch_alc_explicit(a, grid, st);
 }

@@ -1,0 +1,445 @@
+// alc_incremental_v2.cu — LAGP_ALC_INCREMENTAL for pools of
+// N' <= 1024 candidates and p <= 8: the greedy ALC local design of Fig 1 step 2
+// (Eq (5)-(6)) by per-candidate Schur-complement
+// downdates, with ONE block barrier per greedy step.
+//
+// Arithmetic (same as alc_incremental.cu, restated): with K_j = L_j L_j^T every
+// pool candidate c carries
+//   w_c   = L_j^{-1} k_j(x_c)                   (j entries)
+//   s_c   = 1 + eta - ||w_c||^2 = m_j^{-1}(x_c)  (Eq 6)
+//   cov_c = kappa_c - z^T w_c,   z = L_j^{-1} h (kappa_c = K(x_c, x))
+//   t_c   = y_c - y~^T w_c,      y~ = L_j^{-1} Y_j
+// so Delta_c = cov_c^2 / s_c is Eq (5) (App A.1). Appending the winner c*
+// (rho = sqrt(s_{c*})) is the partitioned-inverse step (a4) on the
+// factor, L_{j+1} = [[L_j, 0], [w_{c*}^T, rho]], and every candidate downdates
+//   e_c = K(x_c, x*) - w_{c*}^T w_c,  w_c[j] = e_c / rho,
+//   s_c -= w_c[j]^2,  cov_c -= z_j w_c[j],  t_c -= y~_j w_c[j],
+// with z_j = cov_{c*}/rho and y~_j = t_{c*}/rho. a5 (Eq 1-2) then
+// needs only three running sums: mean = z^T y~, psi = ||y~||^2,
+// s2 = psi (1 + eta - ||z||^2) / n.
+//
+// B200 mapping (differences from alc_incremental.cu):
+//  * 512 threads, CPT = 1 or 2 candidates per thread (candidate c = tid + q*512):
+//    128 registers per thread hold R entries of w_c per candidate (R = 12..16),
+//    and the per-step broadcast reads of the winner's data are shared by CPT
+//    candidates.
+//  * Shared entries are stored in PAIRS (entry-major pairs of rows,
+//    double2 per (pair, candidate)): one LDS.128 per two entries of a column,
+//    the row stride is a compile-time constant (immediate offsets).
+//  * One barrier per step: each warp's best candidate posts its whole record
+//    (key, x_c, 1/rho, z_j, y~_j, register entries) before the barrier; after
+//    it every warp reduces the 16 warp keys itself (redux.sync) and reads the
+//    winner's record — no second barrier, no separate publish phase.
+//  * y~ is maintained per candidate (t_c) instead of a warp-0 dot per step.
+//  * Flags are accumulated per thread and reduced once per location.
+#include <cuda_runtime.h>
+
+#include "block_ops.cuh"
+#include "launch.h"
+
+namespace lagp {
+
+constexpr int V2_THREADS = 512;
+constexpr int V2_NW = V2_THREADS / 32;
+
+// register entries per candidate for (P, CPT)
+template <int P, int CPT>
+struct V2R {
+    static constexpr int value = (CPT == 1) ? 16 : (P <= 4 ? 8 : 4);
+};
+
+// warp post record (doubles): key | gidx,pos | key2 | - | x[8] | rrho z y - | w[R]
+enum { RK = 0, RI = 1, RK2 = 2, RX = 4, RRHO = 12, RZN = 13, RYN = 14, RW = 16 };
+__host__ __device__ constexpr int v2_rec(int R) { return RW + R; }
+
+__device__ __forceinline__ double fast_div_pos(double a, double b) {
+    // a / b for finite b > 0 (not tiny): reciprocal seed + Newton, then one
+    // residual correction of the quotient (no special-case path).
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+    double e = fma(-b, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-b, r, 1.0);
+    r = fma(r, e, r);
+    double q = a * r;
+    const double res = fma(-b, q, a);
+    return fma(res, r, q);
+}
+
+template <int P, int CPT>
+__global__ void __launch_bounds__(V2_THREADS, 1)
+alc_incremental_v2_kernel(AlcArgs A, int S) {
+    constexpr int R = V2R<P, CPT>::value;
+    constexpr int NPC = V2_THREADS * CPT;  // columns (candidates) per pair row
+    constexpr int REC = v2_rec(R);
+    extern __shared__ __align__(16) double sm[];
+    double2 *wsm2 = reinterpret_cast<double2 *>(sm);          // [S/2][NPC] pairs of entries [R, R+S)
+    double *post = sm + (size_t)S * NPC;                      // [2][NW][REC]
+    const int n = A.n, Np = A.Nprime, n0 = A.n0;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int RS = R + S;
+    const int G = n - n0;
+    const double eta = A.eta;
+    double2 *gw2 = reinterpret_cast<double2 *>(A.cache + (size_t)blockIdx.x * A.cache_stride);  // [(a-RS)/2][NPC]
+    __shared__ double xq[8];
+    __shared__ double sums[3];
+
+    for (int64_t xi = blockIdx.x; xi < A.M; xi += gridDim.x) {
+        const double rth = A.theta_vec ? 1.0 / A.theta_vec[xi] : A.rtheta;  // per-location theta (Fig 1 step 4)
+        const int32_t *pool = A.pool + xi * (int64_t)Np;
+        int32_t *idx = A.idx_out + xi * (int64_t)n;
+        if (tid < P) xq[tid] = A.XX[xi * P + tid];
+        for (int t = tid; t < n; t += V2_THREADS) idx[t] = (t < n0) ? pool[t] : -1;
+        __syncthreads();
+
+        // ---- per-candidate state
+        double xc[CPT][P];
+        double s[CPT], cov[CPT], tc[CPT];
+        double wr[CPT][R];
+        bool chosen[CPT];
+        int gidx[CPT];
+        uint32_t fl = 0;
+#pragma unroll
+        for (int q = 0; q < CPT; q++) {
+            const int c = tid + q * V2_THREADS;
+            const bool valid = c < Np;
+            chosen[q] = !valid;  // padding columns never compete
+            gidx[q] = valid ? pool[c] : 0x7fffffff - c;  // unique keys for the warp argmax
+            double d2 = 0.0;
+#pragma unroll
+            for (int k = 0; k < P; k++) {
+                xc[q][k] = valid ? A.X[(int64_t)gidx[q] * P + k] : 0.0;
+                const double diff = __dsub_rn(xc[q][k], xq[k]);
+                d2 = __fma_rn(diff, diff, d2);
+            }
+            s[q] = 1.0 + eta;
+            cov[q] = valid ? corr_from_d2(d2, rth) : 0.0;  // kappa_c (z is empty at j = 0)
+            tc[q] = valid ? A.Z[gidx[q]] : 0.0;             // y_c (y~ is empty at j = 0)
+#pragma unroll
+            for (int a = 0; a < R; a++) wr[q][a] = 0.0;
+        }
+        if (tid == 0) sums[0] = sums[1] = sums[2] = 0.0;  // a5: z^T y~, ||y~||^2, ||z||^2
+        bool near_tie = false, exhausted = false;
+
+        int j = 0;
+        for (; j < n; j++) {
+            const int par = j & 1;
+            double *pst = post + par * (V2_NW * REC);
+            const double *rec;
+            if (j < n0) {
+                // forced NN append (a2): pool position j (thread j, q = 0) posts to slot 0
+                if (tid == j) {
+                    double *r = pst;
+                    const double rho = sqrt(s[0]);
+                    const double rr = 1.0 / rho;
+#pragma unroll
+                    for (int k = 0; k < P; k++) r[RX + k] = xc[0][k];
+                    r[RRHO] = rr;
+                    r[RZN] = cov[0] * rr;
+                    r[RYN] = tc[0] * rr;
+#pragma unroll
+                    for (int a = 0; a < R; a += 2)
+                        *reinterpret_cast<double2 *>(r + RW + a) = make_double2(wr[0][a], wr[0][a + 1]);
+                    reinterpret_cast<unsigned long long *>(r)[RI] =
+                        ((unsigned long long)(unsigned)j << 32) | (unsigned)gidx[0];
+                    chosen[0] = true;
+                    if (!(s[0] > 0.0)) fl |= LAGP_FLAG_NONFINITE;
+                }
+                __syncthreads();
+                rec = pst;
+            } else {
+                // ---- a3: keys of Delta_c = cov_c^2 / s_c (0 = not a candidate)
+                unsigned long long key[CPT];
+#pragma unroll
+                for (int q = 0; q < CPT; q++) {
+                    bool ok = !chosen[q];
+                    if (ok && !(s[q] > kSMin)) {
+                        fl |= LAGP_FLAG_SENTINEL;
+                        ok = false;
+                    }
+                    const double dl = fast_div_pos(cov[q] * cov[q], s[q]);
+                    if (ok && !(dl < INFINITY)) {  // NaN or inf
+                        fl |= LAGP_FLAG_NONFINITE;
+                        ok = false;
+                    }
+                    key[q] = ok ? (unsigned long long)__double_as_longlong(dl) + 1ull : 0ull;
+                }
+                unsigned long long kb = key[0], k2 = 0;
+                int gb = gidx[0], qb = 0;
+                if (CPT == 2) {
+                    const bool b1 = key[CPT - 1] > key[0] || (key[CPT - 1] == key[0] && gidx[CPT - 1] < gidx[0]);
+                    kb = b1 ? key[CPT - 1] : key[0];
+                    k2 = b1 ? key[0] : key[CPT - 1];
+                    gb = b1 ? gidx[CPT - 1] : gidx[0];
+                    qb = b1 ? 1 : 0;
+                }
+                // warp argmax on (key desc, gidx asc) with 32-bit redux
+                const unsigned hi = (unsigned)(kb >> 32), lo = (unsigned)kb;
+                const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+                const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+                const bool tie = hi == mh && lo == ml;
+                const unsigned mi = __reduce_min_sync(0xffffffffu, tie ? (unsigned)gb : 0xffffffffu);
+                const bool wl = tie && (unsigned)gb == mi;  // unique: gidx are distinct
+                // the warp's second-best key (top-2 gap diagnostic)
+                const unsigned long long sk = wl ? k2 : kb;
+                const unsigned sh = __reduce_max_sync(0xffffffffu, (unsigned)(sk >> 32));
+                const unsigned sl = __reduce_max_sync(0xffffffffu, (unsigned)(sk >> 32) == sh ? (unsigned)sk : 0u);
+                if (wl) {
+                    double *r = pst + wid * REC;
+                    reinterpret_cast<unsigned long long *>(r)[RK] = kb;
+                    reinterpret_cast<unsigned long long *>(r)[RI] =
+                        ((unsigned long long)(unsigned)(tid + qb * V2_THREADS) << 32) | (unsigned)gb;
+                    reinterpret_cast<unsigned long long *>(r)[RK2] = ((unsigned long long)sh << 32) | sl;
+#pragma unroll
+                    for (int q = 0; q < CPT; q++) {
+                        if (q == qb) {
+                            const double rho = sqrt(s[q]);
+                            const double rr = 1.0 / rho;
+#pragma unroll
+                            for (int k = 0; k < P; k++) r[RX + k] = xc[q][k];
+                            r[RRHO] = rr;
+                            r[RZN] = cov[q] * rr;
+                            r[RYN] = tc[q] * rr;
+#pragma unroll
+                            for (int a = 0; a < R; a += 2)
+                                *reinterpret_cast<double2 *>(r + RW + a) = make_double2(wr[q][a], wr[q][a + 1]);
+                        }
+                    }
+                }
+                __syncthreads();
+                // every warp: argmax over the warp posts
+                unsigned long long pk = 0;
+                unsigned pg = 0xffffffffu;
+                if (lane < V2_NW) {
+                    pk = reinterpret_cast<const unsigned long long *>(pst + lane * REC)[RK];
+                    pg = (unsigned)reinterpret_cast<const unsigned long long *>(pst + lane * REC)[RI];
+                }
+                const unsigned ph = (unsigned)(pk >> 32), pl = (unsigned)pk;
+                const unsigned qh = __reduce_max_sync(0xffffffffu, ph);
+                const unsigned ql = __reduce_max_sync(0xffffffffu, ph == qh ? pl : 0u);
+                if ((qh | ql) == 0u) {  // no valid candidate left (uniform)
+                    exhausted = true;
+                    break;
+                }
+                const bool ptie = ph == qh && pl == ql;
+                const unsigned qi = __reduce_min_sync(0xffffffffu, ptie ? pg : 0xffffffffu);
+                const int W = __ffs(__ballot_sync(0xffffffffu, ptie && pg == qi)) - 1;
+                rec = pst + W * REC;
+                if (wid == 0) {  // top-2 gap: max(winner warp's second, other warps' best)
+                    const unsigned long long v =
+                        lane == W ? reinterpret_cast<const unsigned long long *>(pst + lane * REC)[RK2] : pk;
+                    const unsigned vh = __reduce_max_sync(0xffffffffu, (unsigned)(v >> 32));
+                    const unsigned vl = __reduce_max_sync(0xffffffffu, (unsigned)(v >> 32) == vh ? (unsigned)v : 0u);
+                    if (lane == 0) {
+                        const unsigned long long k1 = ((unsigned long long)qh << 32) | ql;
+                        const unsigned long long k2b = ((unsigned long long)vh << 32) | vl;
+                        const double d1 = __longlong_as_double((long long)(k1 - 1ull));
+                        const double d2 = k2b ? __longlong_as_double((long long)(k2b - 1ull)) : 0.0;
+                        const double gap = top2_gap(d1, d2);
+                        if (!(d1 > 0.0) || gap < kTieGap) near_tie = true;
+                        if (A.gap_out) A.gap_out[xi * G + (j - n0)] = gap;
+                        idx[j] = (int)qi;
+                    }
+                }
+            }
+            // ---- a4 on the factor: every candidate takes its new entry and downdates
+            const unsigned long long ri = reinterpret_cast<const unsigned long long *>(rec)[RI];
+            const int cstar = (int)(ri >> 32);
+#pragma unroll
+            for (int q = 0; q < CPT; q++)
+                if (cstar == tid + q * V2_THREADS) chosen[q] = true;
+            const double rrho = rec[RRHO], znew = rec[RZN], ynew = rec[RYN];
+            if (tid == 0) {  // running a5 sums
+                sums[0] = fma(znew, ynew, sums[0]);
+                sums[1] = fma(ynew, ynew, sums[1]);
+                sums[2] = fma(znew, znew, sums[2]);
+            }
+
+            double acc[CPT][2];
+#pragma unroll
+            for (int q = 0; q < CPT; q++) acc[q][0] = acc[q][1] = 0.0;
+            // slab entries [RS, j) first (independent loads, latency overlapped)
+            if (j > RS) {
+                const int m = j - RS;
+                const double2 *gwin = gw2 + cstar;
+                const double2 *gown = gw2 + tid;
+                const int np = m >> 1;
+                for (int pr = 0; pr < np; pr++) {
+                    const double2 wv = gwin[pr * NPC];
+#pragma unroll
+                    for (int q = 0; q < CPT; q++) {
+                        const double2 o = gown[pr * NPC + q * V2_THREADS];
+                        acc[q][0] = fma(wv.x, o.x, acc[q][0]);
+                        acc[q][1] = fma(wv.y, o.y, acc[q][1]);
+                    }
+                }
+                if (m & 1) {
+                    const double wv = reinterpret_cast<const double *>(gwin + np * NPC)[0];
+#pragma unroll
+                    for (int q = 0; q < CPT; q++)
+                        acc[q][0] = fma(wv, reinterpret_cast<const double *>(gown + np * NPC + q * V2_THREADS)[0],
+                                        acc[q][0]);
+                }
+            }
+            // register entries (entries >= j are 0 on both sides)
+#pragma unroll
+            for (int a = 0; a < R; a += 2) {
+                const double2 wv = *reinterpret_cast<const double2 *>(rec + RW + a);
+#pragma unroll
+                for (int q = 0; q < CPT; q++) {
+                    acc[q][0] = fma(wv.x, wr[q][a], acc[q][0]);
+                    acc[q][1] = fma(wv.y, wr[q][a + 1], acc[q][1]);
+                }
+            }
+            // shared entries [R, min(j, RS))
+            if (j > R) {
+                const int m = (j < RS ? j : RS) - R;
+                const double2 *swin = wsm2 + cstar;
+                const double2 *sown = wsm2 + tid;
+                const int np = m >> 1;
+#pragma unroll 2
+                for (int pr = 0; pr < np; pr++) {
+                    const double2 wv = swin[pr * NPC];
+#pragma unroll
+                    for (int q = 0; q < CPT; q++) {
+                        const double2 o = sown[pr * NPC + q * V2_THREADS];
+                        acc[q][0] = fma(wv.x, o.x, acc[q][0]);
+                        acc[q][1] = fma(wv.y, o.y, acc[q][1]);
+                    }
+                }
+                if (m & 1) {
+                    const double wv = reinterpret_cast<const double *>(swin + np * NPC)[0];
+#pragma unroll
+                    for (int q = 0; q < CPT; q++)
+                        acc[q][0] = fma(wv, reinterpret_cast<const double *>(sown + np * NPC + q * V2_THREADS)[0],
+                                        acc[q][0]);
+                }
+            }
+            // K(x_c, x*) and the downdates
+            double kx[CPT];
+            {
+                double d2[CPT];
+#pragma unroll
+                for (int q = 0; q < CPT; q++) d2[q] = 0.0;
+#pragma unroll
+                for (int k = 0; k < P; k++) {
+                    const double xs = rec[RX + k];
+#pragma unroll
+                    for (int q = 0; q < CPT; q++) {
+                        const double diff = __dsub_rn(xc[q][k], xs);
+                        d2[q] = __fma_rn(diff, diff, d2[q]);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < CPT; q++) kx[q] = corr_from_d2(d2[q], rth);
+            }
+#pragma unroll
+            for (int q = 0; q < CPT; q++) {
+                const int c = tid + q * V2_THREADS;
+                const double wn = (kx[q] - (acc[q][0] + acc[q][1])) * rrho;
+                if (j < R) {
+#pragma unroll
+                    for (int b = 0; b < R; b++)
+                        if (b == j) wr[q][b] = wn;
+                } else if (j < RS) {
+                    reinterpret_cast<double *>(wsm2 + ((j - R) >> 1) * NPC + c)[(j - R) & 1] = wn;
+                } else {
+                    reinterpret_cast<double *>(gw2 + ((j - RS) >> 1) * NPC + c)[(j - RS) & 1] = wn;
+                }
+                s[q] = fma(-wn, wn, s[q]);
+                cov[q] = fma(-znew, wn, cov[q]);
+                tc[q] = fma(-ynew, wn, tc[q]);
+            }
+        }
+
+        // ---- flags and a5: mean = z^T y~, psi = ||y~||^2, s2 = psi (1 + eta - ||z||^2) / j
+        const bool any_sent = __syncthreads_or((fl & LAGP_FLAG_SENTINEL) != 0);
+        const bool any_nonf = __syncthreads_or((fl & LAGP_FLAG_NONFINITE) != 0);
+        if (tid == 0) {
+            uint32_t f = (any_sent ? LAGP_FLAG_SENTINEL : 0u) | (any_nonf ? LAGP_FLAG_NONFINITE : 0u) |
+                         (near_tie ? LAGP_FLAG_NEAR_TIE : 0u) | (exhausted ? LAGP_FLAG_EXHAUSTED : 0u);
+            const double mu = sums[0], psi = sums[1], zz = sums[2];
+            const double sc = psi * (1.0 + eta - zz) / (double)j;
+            const double vr = j > 2 ? sc * (double)j / (double)(j - 2) : __longlong_as_double(0x7ff8000000000000LL);
+            if (!isfinite(mu) || !isfinite(sc)) f |= LAGP_FLAG_NONFINITE;
+            A.mean[xi] = mu;
+            A.s2[xi] = sc;
+            if (A.var) A.var[xi] = vr;
+            if (A.flags) A.flags[xi] = f;
+            if (f & (LAGP_FLAG_EXHAUSTED | LAGP_FLAG_NONFINITE)) atomicAdd(A.n_partial, 1);
+            if (A.gap_out)
+                for (int t = (j > n0 ? j : n0) - n0; t < G; t++)
+                    A.gap_out[xi * G + t] = __longlong_as_double(0x7ff8000000000000LL);
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- host side
+template <int P, int CPT>
+static cudaError_t v2_launch_t(const AlcArgs &a, int S, int grid, size_t smem, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(alc_incremental_v2_kernel<P, CPT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    alc_incremental_v2_kernel<P, CPT><<<grid, V2_THREADS, smem, st>>>(a, S);
+    return cudaGetLastError();
+}
+
+static int v2_R(int p, int cpt) {
+    switch (cpt * 16 + p) {
+        case 16 + 1: return V2R<1, 1>::value;
+        case 16 + 2: return V2R<2, 1>::value;
+        case 16 + 3: return V2R<3, 1>::value;
+        case 16 + 4: return V2R<4, 1>::value;
+        case 16 + 8: return V2R<8, 1>::value;
+        case 32 + 1: return V2R<1, 2>::value;
+        case 32 + 2: return V2R<2, 2>::value;
+        case 32 + 3: return V2R<3, 2>::value;
+        case 32 + 4: return V2R<4, 2>::value;
+        case 32 + 8: return V2R<8, 2>::value;
+        default: return -1;
+    }
+}
+
+bool inc_v2_plan(int n, int p, int Nprime, size_t smem_optin, IncPlan &pl) {
+    if (Nprime > 2 * V2_THREADS) return false;
+    const int cpt = Nprime <= V2_THREADS ? 1 : 2;
+    const int R = v2_R(p, cpt);
+    if (R < 0) return false;
+    const int npc = V2_THREADS * cpt;
+    const size_t fixed = (size_t)2 * V2_NW * v2_rec(R) * sizeof(double);
+    if (smem_optin < fixed + 2048) return false;
+    const size_t pair_bytes = (size_t)npc * 2 * sizeof(double);
+    int S = 2 * (int)((smem_optin - fixed - 2048) / pair_bytes);
+    const int need = n - R > 0 ? n - R : 0;
+    const int need2 = (need + 1) & ~1;
+    if (S > need2) S = need2;
+    pl = IncPlan{};
+    pl.ok = true;
+    pl.v2 = true;
+    pl.cpt = cpt;
+    pl.R = R;
+    pl.S = S;
+    pl.global_entries = n - R - S > 0 ? n - R - S : 0;
+    pl.smem = (size_t)S * npc * sizeof(double) + fixed;
+    pl.wsz = S * npc;
+    pl.cache_doubles = (int64_t)((pl.global_entries + 1) & ~1) * npc + 16;
+    return true;
+}
+
+cudaError_t launch_alc_incremental_v2(const AlcArgs &a, const IncPlan &pl, int grid, cudaStream_t st) {
+#define V2_DISPATCH(CPT_)                                                         \
+    switch (a.p) {                                                                \
+        case 1: return v2_launch_t<1, CPT_>(a, pl.S, grid, pl.smem, st);          \
+        case 2: return v2_launch_t<2, CPT_>(a, pl.S, grid, pl.smem, st);          \
+        case 3: return v2_launch_t<3, CPT_>(a, pl.S, grid, pl.smem, st);          \
+        case 4: return v2_launch_t<4, CPT_>(a, pl.S, grid, pl.smem, st);          \
+        case 8: return v2_launch_t<8, CPT_>(a, pl.S, grid, pl.smem, st);          \
+        default: return cudaErrorInvalidValue;                                    \
+    }
+    if (pl.cpt == 1) { V2_DISPATCH(1) }
+    V2_DISPATCH(2)
+#undef V2_DISPATCH
+}
+
+}  // namespace lagp

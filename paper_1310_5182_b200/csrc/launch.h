@@ -51,8 +51,13 @@ struct IncPlan {
     int global_entries;  // entries in the per-CTA HBM slab (A.cache)
     int wsz;             // doubles of the shared w region (>= S*Npad, >= predict scratch)
     size_t smem;         // dynamic shared memory bytes
+    bool v2;             // alc_incremental_v2.cu (N' <= 1024, p in {1,2,3,4,8})
+    int64_t cache_doubles;  // per-CTA slab doubles (v2)
 };
 IncPlan inc_plan(int n, int p, int Nprime, int Npad, size_t smem_optin);
+// alc_incremental_v2.cu: one barrier per step, 512 threads, 1-2 candidates per thread
+bool inc_v2_plan(int n, int p, int Nprime, size_t smem_optin, IncPlan &pl);
+cudaError_t launch_alc_incremental_v2(const AlcArgs &a, const IncPlan &pl, int grid, cudaStream_t st);
 // alc_incremental_cluster.cu: 2-CTA cluster per location (N' <= 1024, n <= 64, p in {2,3,8})
 bool inc_cluster_supported(int n, int p, int Nprime);
 cudaError_t launch_alc_inc_cluster(const AlcArgs &a, int num_sms, cudaStream_t st);
