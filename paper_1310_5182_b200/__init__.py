@@ -251,6 +251,14 @@ def predict(Xn, Yn, x, d, g):
     return mean, s2, var
 
 
+def exp_nonpos(x):
+    """laGP_exp_nonpos: the incremental kernels' exp for x <= 0, elementwise on a CUDA tensor."""
+    x = _dev(x, "x").contiguous()
+    y = torch.empty_like(x)
+    _check(lib().laGP_exp_nonpos(_ptr(x), _ptr(y), x.numel(), _stream(x.device)))
+    return y
+
+
 def shard_bounds(M: int, rank: int, world: int):
     """Rank r of R gets rows [r*ceil(M/R), min(M, (r+1)*ceil(M/R))) of XX."""
     per = -(-M // world)

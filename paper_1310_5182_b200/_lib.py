@@ -29,6 +29,7 @@ EXPORTS = (
     "laGP_alc_batch_theta",
     "laGP_mle",
     "laGP_local_fit",
+    "laGP_exp_nonpos",
     "lagp_last_error",
     "lagp_abi_version",
 )
@@ -71,6 +72,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
                              _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     lib.laGP_local_fit.argtypes = [_vp, _i64, _i32, _vp, _vp, _i64, _dbl, _dbl, _dbl, _dbl, _i32, _i32, _i32,
                                    _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.POINTER(Timing), _vp]
+    lib.laGP_exp_nonpos.argtypes = [_vp, _vp, _i64, _vp]
     for f in EXPORTS[:-2]:
         getattr(lib, f).restype = ctypes.c_int
     lib.lagp_last_error.argtypes = []

@@ -626,4 +626,16 @@ lagp_status laGP_predict(int32_t B, int32_t n, int32_t p, const double *Xn, cons
     return LAGP_OK;
 }
 
+lagp_status laGP_exp_nonpos(const double *x, double *y, int64_t n, void *cuda_stream) {
+    if (n < 0) return fail(LAGP_EINVAL, "n must be >= 0");
+    if (n > 0 && (!x || !y)) return fail(LAGP_EINVAL, "x and y must be non-NULL");
+    if (n == 0) return LAGP_OK;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    cudaError_t e = lagp::launch_exp_nonpos(x, y, n, st);
+    if (e != cudaSuccess) return cuda_fail(e, "exp_nonpos_kernel");
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    return LAGP_OK;
+}
+
 }  // extern "C"

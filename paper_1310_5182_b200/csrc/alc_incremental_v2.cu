@@ -33,19 +33,20 @@
 //  * y~ is maintained per candidate (t_c) instead of a warp-0 dot per step.
 //  * Flags are accumulated per thread and reduced once per location.
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "block_ops.cuh"
 #include "launch.h"
 
 namespace lagp {
 
-constexpr int V2_THREADS = 512;
-constexpr int V2_NW = V2_THREADS / 32;
+// threads per CTA by candidates per thread: N' <= 512 -> 512 x 1, else 1024/CPT x CPT
+__host__ __device__ constexpr int v2_threads(int cpt) { return cpt == 1 ? 512 : 1024 / cpt; }
 
 // register entries per candidate for (P, CPT)
 template <int P, int CPT>
 struct V2R {
-    static constexpr int value = (CPT == 1) ? 16 : (P <= 4 ? 8 : 4);
+    static constexpr int value = (CPT == 1) ? 16 : (CPT == 2 ? (P <= 4 ? 8 : 4) : (P <= 4 ? 8 : 6));
 };
 
 // warp post record (doubles): key | gidx,pos | key2 | - | x[8] | rrho z y - | w[R]
@@ -53,23 +54,44 @@ enum { RK = 0, RI = 1, RK2 = 2, RX = 4, RRHO = 12, RZN = 13, RYN = 14, RW = 16 }
 __host__ __device__ constexpr int v2_rec(int R) { return RW + R; }
 
 __device__ __forceinline__ double fast_div_pos(double a, double b) {
-    // a / b for finite b > 0 (not tiny): reciprocal seed + Newton, then one
-    // residual correction of the quotient (no special-case path).
+    // a / b for finite b > 0 (not tiny): reciprocal seed, one Newton step, then
+    // one residual correction of the quotient (no special-case path)
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
-    double e = fma(-b, r, 1.0);
+    const double e = fma(-b, r, 1.0);
     r = fma(r, e, r);
-    e = fma(-b, r, 1.0);
-    r = fma(r, e, r);
-    double q = a * r;
+    const double q = a * r;
     const double res = fma(-b, q, a);
     return fma(res, r, q);
 }
 
-template <int P, int CPT>
-__global__ void __launch_bounds__(V2_THREADS, 1)
+
+
+#ifdef LAGP_V2_PROF
+// clock probes of thread 0 on its first location (profiling builds only)
+__device__ long long g_v2_prof[160][8];
+__device__ volatile double g_v2_sink;
+#define V2_PROBE(k, v)                                                              \
+    do {                                                                            \
+        if (tid == 0 && xi == blockIdx.x && blockIdx.x == 0 && j < 160) {           \
+            g_v2_sink = (v);                                                        \
+            long long t_;                                                           \
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_)::"memory");            \
+            g_v2_prof[j][k] = t_;                                                   \
+        }                                                                           \
+    } while (0)
+#else
+#define V2_PROBE(k, v) \
+    do {               \
+    } while (0)
+#endif
+
+template <int P, int CPT, int TH>
+__global__ void __launch_bounds__(TH, 1)
 alc_incremental_v2_kernel(AlcArgs A, int S) {
     constexpr int R = V2R<P, CPT>::value;
+    constexpr int V2_THREADS = TH;
+    constexpr int V2_NW = TH / 32;
     constexpr int NPC = V2_THREADS * CPT;  // columns (candidates) per pair row
     constexpr int REC = v2_rec(R);
     extern __shared__ __align__(16) double sm[];
@@ -82,7 +104,9 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
     const double eta = A.eta;
     double2 *gw2 = reinterpret_cast<double2 *>(A.cache + (size_t)blockIdx.x * A.cache_stride);  // [(a-RS)/2][NPC]
     __shared__ double xq[8];
-    __shared__ double sums[3];
+    __shared__ double zyv[2][LAGP_NMAX];  // z_j, y~_j of every append (a5)
+    __shared__ double s_exptab[32];        // 2^(k/32) for exp_nonpos_tab
+    if (threadIdx.x < 32) s_exptab[threadIdx.x] = c_exp2_32[threadIdx.x];
 
     for (int64_t xi = blockIdx.x; xi < A.M; xi += gridDim.x) {
         const double rth = A.theta_vec ? 1.0 / A.theta_vec[xi] : A.rtheta;  // per-location theta (Fig 1 step 4)
@@ -113,21 +137,22 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
                 d2 = __fma_rn(diff, diff, d2);
             }
             s[q] = 1.0 + eta;
-            cov[q] = valid ? corr_from_d2(d2, rth) : 0.0;  // kappa_c (z is empty at j = 0)
+            cov[q] = valid ? exp_nonpos_tab(-d2 * rth, s_exptab) : 0.0;  // kappa_c (z is empty at j = 0)
             tc[q] = valid ? A.Z[gidx[q]] : 0.0;             // y_c (y~ is empty at j = 0)
 #pragma unroll
             for (int a = 0; a < R; a++) wr[q][a] = 0.0;
         }
-        if (tid == 0) sums[0] = sums[1] = sums[2] = 0.0;  // a5: z^T y~, ||y~||^2, ||z||^2
         bool near_tie = false, exhausted = false;
 
         int j = 0;
         for (; j < n; j++) {
+            V2_PROBE(0, (double)j);
             const int par = j & 1;
             double *pst = post + par * (V2_NW * REC);
             const double *rec;
             if (j < n0) {
-                // forced NN append (a2): pool position j (thread j, q = 0) posts to slot 0
+                // forced NN append (a2): pool position j (thread j, q = 0; j < n <= LAGP_NMAX <= TH)
+                // posts to slot 0
                 if (tid == j) {
                     double *r = pst;
                     const double rho = sqrt(s[0]);
@@ -166,13 +191,15 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
                 }
                 unsigned long long kb = key[0], k2 = 0;
                 int gb = gidx[0], qb = 0;
-                if (CPT == 2) {
-                    const bool b1 = key[CPT - 1] > key[0] || (key[CPT - 1] == key[0] && gidx[CPT - 1] < gidx[0]);
-                    kb = b1 ? key[CPT - 1] : key[0];
-                    k2 = b1 ? key[0] : key[CPT - 1];
-                    gb = b1 ? gidx[CPT - 1] : gidx[0];
-                    qb = b1 ? 1 : 0;
+#pragma unroll
+                for (int q = 1; q < CPT; q++) {
+                    const bool b = key[q] > kb || (key[q] == kb && gidx[q] < gb);
+                    k2 = b ? kb : (key[q] > k2 ? key[q] : k2);
+                    kb = b ? key[q] : kb;
+                    gb = b ? gidx[q] : gb;
+                    qb = b ? q : qb;
                 }
+                V2_PROBE(1, (double)kb);
                 // warp argmax on (key desc, gidx asc) with 32-bit redux
                 const unsigned hi = (unsigned)(kb >> 32), lo = (unsigned)kb;
                 const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
@@ -180,6 +207,7 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
                 const bool tie = hi == mh && lo == ml;
                 const unsigned mi = __reduce_min_sync(0xffffffffu, tie ? (unsigned)gb : 0xffffffffu);
                 const bool wl = tie && (unsigned)gb == mi;  // unique: gidx are distinct
+                V2_PROBE(2, (double)mi);
                 // the warp's second-best key (top-2 gap diagnostic)
                 const unsigned long long sk = wl ? k2 : kb;
                 const unsigned sh = __reduce_max_sync(0xffffffffu, (unsigned)(sk >> 32));
@@ -225,7 +253,8 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
                 const unsigned qi = __reduce_min_sync(0xffffffffu, ptie ? pg : 0xffffffffu);
                 const int W = __ffs(__ballot_sync(0xffffffffu, ptie && pg == qi)) - 1;
                 rec = pst + W * REC;
-                if (wid == 0) {  // top-2 gap: max(winner warp's second, other warps' best)
+                V2_PROBE(3, (double)W);
+                if (wid == V2_NW - 1) {  // top-2 gap: max(winner warp's second, other warps' best)
                     const unsigned long long v =
                         lane == W ? reinterpret_cast<const unsigned long long *>(pst + lane * REC)[RK2] : pk;
                     const unsigned vh = __reduce_max_sync(0xffffffffu, (unsigned)(v >> 32));
@@ -249,75 +278,22 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
             for (int q = 0; q < CPT; q++)
                 if (cstar == tid + q * V2_THREADS) chosen[q] = true;
             const double rrho = rec[RRHO], znew = rec[RZN], ynew = rec[RYN];
-            if (tid == 0) {  // running a5 sums
-                sums[0] = fma(znew, ynew, sums[0]);
-                sums[1] = fma(ynew, ynew, sums[1]);
-                sums[2] = fma(znew, znew, sums[2]);
+            V2_PROBE(4, rrho);
+            if (tid == V2_THREADS - 1) {  // a5 state (summed once at the end)
+                zyv[0][j] = znew;
+                zyv[1][j] = ynew;
             }
 
+            // Two phases per candidate: K(x_c, x*) (FP64 pipe) and the dot w_{c*}^T w_c
+            // (shared-memory / L2 bandwidth). Odd warps run them in the opposite order,
+            // so the two units are busy at the same time across the CTA.
+            double kx[CPT];
             double acc[CPT][2];
 #pragma unroll
             for (int q = 0; q < CPT; q++) acc[q][0] = acc[q][1] = 0.0;
-            // slab entries [RS, j) first (independent loads, latency overlapped)
-            if (j > RS) {
-                const int m = j - RS;
-                const double2 *gwin = gw2 + cstar;
-                const double2 *gown = gw2 + tid;
-                const int np = m >> 1;
-                for (int pr = 0; pr < np; pr++) {
-                    const double2 wv = gwin[pr * NPC];
-#pragma unroll
-                    for (int q = 0; q < CPT; q++) {
-                        const double2 o = gown[pr * NPC + q * V2_THREADS];
-                        acc[q][0] = fma(wv.x, o.x, acc[q][0]);
-                        acc[q][1] = fma(wv.y, o.y, acc[q][1]);
-                    }
-                }
-                if (m & 1) {
-                    const double wv = reinterpret_cast<const double *>(gwin + np * NPC)[0];
-#pragma unroll
-                    for (int q = 0; q < CPT; q++)
-                        acc[q][0] = fma(wv, reinterpret_cast<const double *>(gown + np * NPC + q * V2_THREADS)[0],
-                                        acc[q][0]);
-                }
-            }
-            // register entries (entries >= j are 0 on both sides)
-#pragma unroll
-            for (int a = 0; a < R; a += 2) {
-                const double2 wv = *reinterpret_cast<const double2 *>(rec + RW + a);
-#pragma unroll
-                for (int q = 0; q < CPT; q++) {
-                    acc[q][0] = fma(wv.x, wr[q][a], acc[q][0]);
-                    acc[q][1] = fma(wv.y, wr[q][a + 1], acc[q][1]);
-                }
-            }
-            // shared entries [R, min(j, RS))
-            if (j > R) {
-                const int m = (j < RS ? j : RS) - R;
-                const double2 *swin = wsm2 + cstar;
-                const double2 *sown = wsm2 + tid;
-                const int np = m >> 1;
-#pragma unroll 2
-                for (int pr = 0; pr < np; pr++) {
-                    const double2 wv = swin[pr * NPC];
-#pragma unroll
-                    for (int q = 0; q < CPT; q++) {
-                        const double2 o = sown[pr * NPC + q * V2_THREADS];
-                        acc[q][0] = fma(wv.x, o.x, acc[q][0]);
-                        acc[q][1] = fma(wv.y, o.y, acc[q][1]);
-                    }
-                }
-                if (m & 1) {
-                    const double wv = reinterpret_cast<const double *>(swin + np * NPC)[0];
-#pragma unroll
-                    for (int q = 0; q < CPT; q++)
-                        acc[q][0] = fma(wv, reinterpret_cast<const double *>(sown + np * NPC + q * V2_THREADS)[0],
-                                        acc[q][0]);
-                }
-            }
-            // K(x_c, x*) and the downdates
-            double kx[CPT];
-            {
+            // K(x_c, x*) first: branch-free, so the CPT chains interleave and overlap
+            // the slab loads below
+            auto kx_phase = [&]() {
                 double d2[CPT];
 #pragma unroll
                 for (int q = 0; q < CPT; q++) d2[q] = 0.0;
@@ -331,7 +307,78 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
                     }
                 }
 #pragma unroll
-                for (int q = 0; q < CPT; q++) kx[q] = corr_from_d2(d2[q], rth);
+                for (int q = 0; q < CPT; q++) kx[q] = exp_nonpos_tab(-d2[q] * rth, s_exptab);
+            };
+            auto dot_phase = [&]() {
+            // slab entries [RS, j) (L2-resident), two pairs per iteration
+            if (j > RS) {
+                const int m = j - RS;
+                const double2 *gwin = gw2 + cstar;
+                const double2 *gown = gw2 + tid;
+                const int np = m >> 1;
+#pragma unroll 2
+                for (int pr = 0; pr < np; pr++) {
+                    const double2 wv = *gwin;
+#pragma unroll
+                    for (int q = 0; q < CPT; q++) {
+                        const double2 o = gown[q * V2_THREADS];
+                        acc[q][0] = fma(wv.x, o.x, acc[q][0]);
+                        acc[q][1] = fma(wv.y, o.y, acc[q][1]);
+                    }
+                    gwin += NPC;
+                    gown += NPC;
+                }
+                if (m & 1) {
+                    const double wv = reinterpret_cast<const double *>(gwin)[0];
+#pragma unroll
+                    for (int q = 0; q < CPT; q++)
+                        acc[q][0] = fma(wv, reinterpret_cast<const double *>(gown + q * V2_THREADS)[0], acc[q][0]);
+                }
+            }
+            // register entries (entries >= j are 0 on both sides)
+#pragma unroll
+            for (int a = 0; a < R; a += 2) {
+                const double2 wv = *reinterpret_cast<const double2 *>(rec + RW + a);
+#pragma unroll
+                for (int q = 0; q < CPT; q++) {
+                    acc[q][0] = fma(wv.x, wr[q][a], acc[q][0]);
+                    acc[q][1] = fma(wv.y, wr[q][a + 1], acc[q][1]);
+                }
+            }
+            // shared entries [R, min(j, RS)): one LDS.128 per two entries of a column
+            if (j > R) {
+                const int m = (j < RS ? j : RS) - R;
+                const double2 *swin = wsm2 + cstar;
+                const double2 *sown = wsm2 + tid;
+                const int np = m >> 1;
+#pragma unroll 2
+                for (int pr = 0; pr < np; pr++) {
+                    const double2 wv = *swin;
+#pragma unroll
+                    for (int q = 0; q < CPT; q++) {
+                        const double2 o = sown[q * V2_THREADS];
+                        acc[q][0] = fma(wv.x, o.x, acc[q][0]);
+                        acc[q][1] = fma(wv.y, o.y, acc[q][1]);
+                    }
+                    swin += NPC;
+                    sown += NPC;
+                }
+                if (m & 1) {
+                    const double wv = reinterpret_cast<const double *>(swin)[0];
+#pragma unroll
+                    for (int q = 0; q < CPT; q++)
+                        acc[q][0] = fma(wv, reinterpret_cast<const double *>(sown + q * V2_THREADS)[0], acc[q][0]);
+                }
+            }
+            };
+            if ((wid >> 2) & 1) {  // warps w and w+4 share an SMSP: opposite orders
+                dot_phase();
+                kx_phase();
+            } else {
+                kx_phase();
+                V2_PROBE(5, kx[0]);
+                dot_phase();
+                V2_PROBE(6, acc[0][0] + acc[0][1]);
             }
 #pragma unroll
             for (int q = 0; q < CPT; q++) {
@@ -347,6 +394,7 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
                     reinterpret_cast<double *>(gw2 + ((j - RS) >> 1) * NPC + c)[(j - RS) & 1] = wn;
                 }
                 s[q] = fma(-wn, wn, s[q]);
+
                 cov[q] = fma(-znew, wn, cov[q]);
                 tc[q] = fma(-ynew, wn, tc[q]);
             }
@@ -355,10 +403,22 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
         // ---- flags and a5: mean = z^T y~, psi = ||y~||^2, s2 = psi (1 + eta - ||z||^2) / j
         const bool any_sent = __syncthreads_or((fl & LAGP_FLAG_SENTINEL) != 0);
         const bool any_nonf = __syncthreads_or((fl & LAGP_FLAG_NONFINITE) != 0);
-        if (tid == 0) {
+        if (wid == V2_NW - 1) {  // the warp holding near_tie (its lane 0)
+            double mu = 0.0, psi = 0.0, zz = 0.0;
+            for (int a = lane; a < j; a += 32) {
+                mu = fma(zyv[0][a], zyv[1][a], mu);
+                psi = fma(zyv[1][a], zyv[1][a], psi);
+                zz = fma(zyv[0][a], zyv[0][a], zz);
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                mu += __shfl_xor_sync(0xffffffffu, mu, off);
+                psi += __shfl_xor_sync(0xffffffffu, psi, off);
+                zz += __shfl_xor_sync(0xffffffffu, zz, off);
+            }
+            if (lane == 0) {
             uint32_t f = (any_sent ? LAGP_FLAG_SENTINEL : 0u) | (any_nonf ? LAGP_FLAG_NONFINITE : 0u) |
                          (near_tie ? LAGP_FLAG_NEAR_TIE : 0u) | (exhausted ? LAGP_FLAG_EXHAUSTED : 0u);
-            const double mu = sums[0], psi = sums[1], zz = sums[2];
             const double sc = psi * (1.0 + eta - zz) / (double)j;
             const double vr = j > 2 ? sc * (double)j / (double)(j - 2) : __longlong_as_double(0x7ff8000000000000LL);
             if (!isfinite(mu) || !isfinite(sc)) f |= LAGP_FLAG_NONFINITE;
@@ -370,6 +430,7 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
             if (A.gap_out)
                 for (int t = (j > n0 ? j : n0) - n0; t < G; t++)
                     A.gap_out[xi * G + t] = __longlong_as_double(0x7ff8000000000000LL);
+            }
         }
         __syncthreads();
     }
@@ -378,36 +439,40 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
 // ---------------------------------------------------------------- host side
 template <int P, int CPT>
 static cudaError_t v2_launch_t(const AlcArgs &a, int S, int grid, size_t smem, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(alc_incremental_v2_kernel<P, CPT>,
+    constexpr int TH = v2_threads(CPT);
+    cudaError_t e = cudaFuncSetAttribute(alc_incremental_v2_kernel<P, CPT, TH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    alc_incremental_v2_kernel<P, CPT><<<grid, V2_THREADS, smem, st>>>(a, S);
+    alc_incremental_v2_kernel<P, CPT, TH><<<grid, TH, smem, st>>>(a, S);
     return cudaGetLastError();
 }
 
-static int v2_R(int p, int cpt) {
-    switch (cpt * 16 + p) {
-        case 16 + 1: return V2R<1, 1>::value;
-        case 16 + 2: return V2R<2, 1>::value;
-        case 16 + 3: return V2R<3, 1>::value;
-        case 16 + 4: return V2R<4, 1>::value;
-        case 16 + 8: return V2R<8, 1>::value;
-        case 32 + 1: return V2R<1, 2>::value;
-        case 32 + 2: return V2R<2, 2>::value;
-        case 32 + 3: return V2R<3, 2>::value;
-        case 32 + 4: return V2R<4, 2>::value;
-        case 32 + 8: return V2R<8, 2>::value;
+template <int CPT>
+static int v2_R_cpt(int p) {
+    switch (p) {
+        case 1: return V2R<1, CPT>::value;
+        case 2: return V2R<2, CPT>::value;
+        case 3: return V2R<3, CPT>::value;
+        case 4: return V2R<4, CPT>::value;
+        case 8: return V2R<8, CPT>::value;
         default: return -1;
     }
 }
 
+static int v2_R(int p, int cpt) {
+    return cpt == 1 ? v2_R_cpt<1>(p) : cpt == 2 ? v2_R_cpt<2>(p) : v2_R_cpt<4>(p);
+}
+
 bool inc_v2_plan(int n, int p, int Nprime, size_t smem_optin, IncPlan &pl) {
-    if (Nprime > 2 * V2_THREADS) return false;
-    const int cpt = Nprime <= V2_THREADS ? 1 : 2;
+    if (Nprime > 1024) return false;
+    int cpt = Nprime <= 512 ? 1 : 2;
+    const char *ev = getenv("LAGP_V2_CPT");  // A/B experiments: 2 or 4 for N' in (512, 1024]
+    if (ev && cpt > 1 && (ev[0] == '2' || ev[0] == '4')) cpt = ev[0] - '0';
     const int R = v2_R(p, cpt);
     if (R < 0) return false;
-    const int npc = V2_THREADS * cpt;
-    const size_t fixed = (size_t)2 * V2_NW * v2_rec(R) * sizeof(double);
+    const int th = v2_threads(cpt);
+    const int npc = th * cpt;
+    const size_t fixed = (size_t)2 * (th / 32) * v2_rec(R) * sizeof(double);
     if (smem_optin < fixed + 2048) return false;
     const size_t pair_bytes = (size_t)npc * 2 * sizeof(double);
     int S = 2 * (int)((smem_optin - fixed - 2048) / pair_bytes);
@@ -438,8 +503,15 @@ cudaError_t launch_alc_incremental_v2(const AlcArgs &a, const IncPlan &pl, int g
         default: return cudaErrorInvalidValue;                                    \
     }
     if (pl.cpt == 1) { V2_DISPATCH(1) }
-    V2_DISPATCH(2)
+    if (pl.cpt == 2) { V2_DISPATCH(2) }
+    V2_DISPATCH(4)
 #undef V2_DISPATCH
 }
 
 }  // namespace lagp
+
+#ifdef LAGP_V2_PROF
+extern "C" int lagp_v2_prof(long long *out) {
+    return (int)cudaMemcpyFromSymbol(out, lagp::g_v2_prof, sizeof(lagp::g_v2_prof));
+}
+#endif

@@ -11,6 +11,23 @@ namespace lagp {
 
 constexpr int DIAG_THREADS = 256;
 
+// the table exponential of the incremental kernels, elementwise (laGP_exp_nonpos)
+__global__ void exp_nonpos_kernel(const double *__restrict__ x, double *__restrict__ y, int64_t n) {
+    __shared__ double tab[32];
+    if (threadIdx.x < 32) tab[threadIdx.x] = c_exp2_32[threadIdx.x];
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = exp_nonpos_tab(x[i], tab);
+}
+
+cudaError_t launch_exp_nonpos(const double *x, double *y, int64_t n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    exp_nonpos_kernel<<<(int)blocks, 256, 0, st>>>(x, y, n);
+    return cudaGetLastError();
+}
+
 // a3 alone (Fig 2 I/O): one CTA per location, one warp per candidate.
 //   w = K^{-1} h (h = k_j(x)), s_c = 1 + g - k_c^T K^{-1} k_c, cov_c = kappa_c - w^T k_c,
 //   Delta_c = cov_c^2 / s_c (Eq (5)-(6) closed form, R1); -inf if s_c <= 1e-12.

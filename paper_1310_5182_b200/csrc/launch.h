@@ -94,6 +94,7 @@ cudaError_t launch_alc_scores(int B, int j, int p, int nc, const double *Xj, con
                               int32_t *best, double *gap, cudaStream_t st);
 cudaError_t launch_pinv_update(int B, int j, const double *Kinv, const double *k, double kdiag, double *Kout,
                                cudaStream_t st);
+cudaError_t launch_exp_nonpos(const double *x, double *y, int64_t n, cudaStream_t st);
 cudaError_t launch_predict(int B, int n, int p, const double *Xn, const double *Yn, const double *x, double rtheta,
                            double eta, double *mean, double *s2, double *var, cudaStream_t st);
 

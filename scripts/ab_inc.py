@@ -38,9 +38,14 @@ if os.environ.get("AB_CHILD"):
     print(json.dumps({"timing": ts[-1], "status": int(r["status"])}))
     sys.exit(0)
 
-args = sys.argv[1:]
+args = [a for a in sys.argv[1:] if not a.startswith("--variants=")]
+spec = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--variants=")), "v2:;v1:LAGP_INC_V1=1")
+variants = []
+for item in spec.split(";"):
+    name, _, envs = item.partition(":")
+    variants.append((name, dict(kv.split("=") for kv in envs.split(",") if kv)))
 res = {}
-for name, env in (("v2", {}), ("v1", {"LAGP_INC_V1": "1"})):
+for name, env in variants:
     out = f"/tmp/ab_{name}.npz"
     e = dict(os.environ, AB_CHILD="1", **env)
     p = subprocess.run([sys.executable, __file__, *args, "--out", out], env=e, capture_output=True, text=True)
@@ -48,7 +53,9 @@ for name, env in (("v2", {}), ("v1", {"LAGP_INC_V1": "1"})):
     res[name] = out
 import numpy as np  # noqa: E402
 
-a, b = np.load(res["v2"]), np.load(res["v1"])
+names = list(res)
+a, b = np.load(res[names[0]]), np.load(res[names[-1]])
+print("compare", names[0], "vs", names[-1])
 same = (a["idx"] == b["idx"]).all(axis=1)
 print("identical index sequences:", int(same.sum()), "/", len(same))
 rel = np.abs(a["mean"] - b["mean"])[same] / np.maximum(np.abs(b["mean"][same]), np.std(b["mean"]))

@@ -29,7 +29,7 @@ def test_header_declares_expected_entry_points():
     syms = declared_symbols()
     for s in ("laGP_alc_batch", "laGP_alc_scores", "lagp_last_error", "lagp_abi_version", "laGP_nn_pool",
               "laGP_pinv_update", "laGP_predict", "laGP_alc_batch_ex", "laGP_alc_batch_host", "laGP_alc_batch_theta",
-              "laGP_mle", "laGP_local_fit"):
+              "laGP_mle", "laGP_local_fit", "laGP_exp_nonpos"):
         assert s in syms
 
 
@@ -103,3 +103,11 @@ def test_incremental_form_flag_validated(lagp):
     st = lib.laGP_alc_batch_ex(vp(1), 100, 2, vp(1), vp(1), 10, 0.1, 1e-4, 6, 50, 60, vp(1), vp(1), vp(1), None,
                                None, None, 7, None, None)
     assert st == lagp.LAGP_EINVAL and "alc_form" in lagp.last_error()
+
+
+def test_exp_nonpos_validates(lagp):
+    lib = lagp.lib()
+    assert lib.laGP_exp_nonpos(None, None, -1, None) == 2
+    assert "n must be" in lagp.last_error()
+    assert lib.laGP_exp_nonpos(None, None, 4, None) == 2
+    assert lib.laGP_exp_nonpos(None, None, 0, None) == 0

@@ -282,3 +282,27 @@ def test_full_size_C2_sampled(torch_dev, lagp, form):
     srt = np.sort(idx, axis=1)
     assert (np.diff(srt, axis=1) > 0).all()
     assert (r["s2"].cpu().numpy() > 0).all()
+
+
+def test_exp_nonpos_table_ulp(torch_dev, lagp):
+    """The incremental kernels' exp (laGP_exp_nonpos) against the correctly
+    rounded exp of each double input (decimal arithmetic): <= 1 ulp on x in
+    [-708, 0], exact at 0, 0 below -708, NaN propagated."""
+    import math
+    from decimal import Decimal, getcontext
+
+    torch, dev = torch_dev
+    rng = np.random.default_rng(7)
+    x = np.concatenate([-rng.uniform(0, 708, 1500), -rng.uniform(0, 1, 500), -rng.uniform(0, 1e-3, 200),
+                        -np.logspace(-300, 2.85, 300), [0.0, -0.0, -708.0, -707.99999, -1e-320]])
+    y = lagp.exp_nonpos(torch.from_numpy(x).to(dev)).cpu().numpy()
+    getcontext().prec = 40
+    worst = 0.0
+    for xi, yi in zip(x, y):
+        ref = float(Decimal(float(xi)).exp())
+        ulp = math.ulp(ref)
+        worst = max(worst, abs(yi - ref) / ulp)
+    assert worst <= 1.0, worst
+    assert y[x == 0.0].tolist() == [1.0, 1.0]
+    z = lagp.exp_nonpos(torch.tensor([-708.0001, -1e4, float("nan")], dtype=torch.float64, device=dev)).cpu().numpy()
+    assert z[0] == 0.0 and z[1] == 0.0 and np.isnan(z[2])
