@@ -1,6 +1,6 @@
 #!/bin/bash
-# Round-end evidence: bench line, launch list, ncu full captures of the two
-# local-design kernels and the NN kernel at the bench's launch configuration.
+# Round evidence: bench line, launch list, ncu full captures of the local-design
+# kernels and the NN kernel at the bench's launch configuration (M = 10,000).
 # usage: bash scripts/round_profile.sh rNN
 R=${1:-r01}
 cd "$GRAFT_REPO_ROOT"
