@@ -61,6 +61,8 @@ def lib():
                                           I32, D, D, D, U32, D, D, D]
         _lib.oracle_loglik.argtypes = [i32, i32, D, D, dbl, dbl, i32, D, D, D]
         _lib.oracle_mle.argtypes = [i32, i32, D, D, dbl, dbl, dbl, dbl, D, D, ctypes.POINTER(ctypes.c_int), U32]
+        _lib.oracle_sep_scale.argtypes = [D, i64, i32, D, D]
+        _lib.oracle_sep_scale.restype = None
         _lib.oracle_local_fit_batch.argtypes = [D, i64, i32, D, D, i64, dbl, dbl, dbl, dbl, i32, i32, i32, i32,
                                                 i32, I32, D, D, D, D, U32]
         for f in ("oracle_nn", "oracle_invert_spd", "oracle_alc_scores", "oracle_pinv_update",
@@ -166,6 +168,25 @@ def alc_batch(X, Z, XX, d, g, n0, n, Nprime, threads=0):
         _p(best, ctypes.c_double), _p(s2acc, ctypes.c_double))
     return dict(idx=idx, mean=mean, s2=s2, var=var, flags=flags, gaps=gaps, best=best,
                 s2_acc=s2acc, threads=used)
+
+
+def sep_scale(X, theta):
+    """Row f3: x~_k = x_k / sqrt(theta_k) (oracle_sep_scale), so that the separable
+    correlation exp(-sum_k (x_k - x'_k)^2 / theta_k) is exp(-||x~ - x~'||^2)."""
+    X, pX = _d(np.atleast_2d(X))
+    th, pth = _d(np.asarray(theta, dtype=np.float64).ravel())
+    N, p = X.shape
+    if th.shape[0] != p or not np.all(th > 0):
+        raise ValueError("theta must hold p positive lengthscales")
+    out = np.empty_like(X)
+    lib().oracle_sep_scale(pX, N, p, pth, _p(out, ctypes.c_double))
+    return out
+
+
+def alc_batch_sep(X, Z, XX, theta, g, n0, n, Nprime, threads=0):
+    """Row f3: the full path (a1-a5) under the separable correlation with
+    lengthscales theta[p]: the isotropic path with d = 1 on the rescaled inputs."""
+    return alc_batch(sep_scale(X, theta), Z, sep_scale(XX, theta), 1.0, g, n0, n, Nprime, threads=threads)
 
 
 def local_design(X, Z, x, d, g, n0, n, Nprime):

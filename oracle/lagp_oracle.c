@@ -606,3 +606,22 @@ int oracle_local_fit_batch(const double *X, int64_t N, int p, const double *Z, c
     }
     return used;
 }
+
+/* ========================================================================= */
+/* Row f3: separable lengthscales. P:667-670: Steps 2 & 6 of Fig 3
+ * assume the isotropic Gaussian correlation; "simple modification would
+ * accommodate ... a separable version via a vectorized theta parameter":
+ *   K(x, x') = exp(-sum_k (x_k - x'_k)^2 / theta_k)                      (*)
+ * (η on the diagonal as before). Writing s_k = 1/sqrt(theta_k) and
+ * x~_k = s_k x_k, (*) is exp(-||x~ - x~'||^2): the isotropic correlation of
+ * P:213-215 with theta = 1 on the rescaled inputs, and the NN ordering
+ * "relative to the chosen correlation function" is the Euclidean
+ * order of the rescaled inputs (reading R23). This function forms x~ (one
+ * correctly rounded sqrt, one division and one product per entry); the
+ * separable path is then the isotropic path with d = 1 on (X~, XX~). */
+void oracle_sep_scale(const double *X, int64_t N, int p, const double *theta, double *Xs) {
+    for (int k = 0; k < p; k++) {
+        const double s = 1.0 / sqrt(theta[k]);
+        for (int64_t i = 0; i < N; i++) Xs[i * p + k] = X[i * p + k] * s;
+    }
+}
