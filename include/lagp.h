@@ -214,6 +214,26 @@ lagp_status laGP_alc_batch_theta(const double *X, int64_t N, int32_t p, const do
                                  int32_t alc_form, lagp_timing *timing, void *cuda_stream);
 
 /*
+ * laGP_alc_batch_sep — SURVEY §8f row f3: laGP_alc_batch_ex under the separable
+ * Gaussian correlation K(x, x') = exp(-sum_k (x_k - x'_k)^2 / theta_k) + g [x = x']
+ * ("a separable version via a vectorized theta parameter"). The NN
+ * pool (a1) orders rows by the same weighted distance ("relative to
+ * the chosen correlation function"). Evaluated as the isotropic path with d = 1
+ * on inputs rescaled by s_k = 1/sqrt(theta_k) (reading R23): x~_k = x_k * s_k,
+ * s_k formed on the host with IEEE sqrt and division, x~ by one correctly
+ * rounded product per entry (a stream-ordered workspace copy of X and XX).
+ *   theta: HOST array of p lengthscales, each finite and > 0 (else LAGP_EINVAL).
+ * Other arguments, outputs, flags and status as laGP_alc_batch_ex; timing->launches
+ * includes the two rescaling launches.
+ */
+lagp_status laGP_alc_batch_sep(const double *X, int64_t N, int32_t p, const double *Z,
+                               const double *XX, int64_t M, const double *theta, double g,
+                               int32_t n0, int32_t n, int32_t Nprime,
+                               int32_t *idx_out, double *mean_out, double *s2_out,
+                               double *var_out, uint32_t *flags_out, double *gap_out,
+                               int32_t alc_form, lagp_timing *timing, void *cuda_stream);
+
+/*
  * laGP_mle — SURVEY §8f row f2, Fig 1 step 3: for each location i,
  * the local MLE theta-hat_n(x_i) of the concentrated likelihood Eq (3)
  * on D_n(x_i) = (X[idx[i,:]], Z[idx[i,:]]) (the valid prefix of the

@@ -127,6 +127,37 @@ def alc_batch(X, Z, XX, d, g, n0, n, Nprime, form="explicit", gaps=False, timing
     return out
 
 
+def alc_batch_sep(X, Z, XX, theta, g, n0, n, Nprime, form="incremental", gaps=False, timing=False):
+    """laGP_alc_batch_sep (row f3): the full path under the separable correlation
+    exp(-sum_k (x_k - x'_k)^2 / theta_k); ``theta`` is a sequence of p floats (host)."""
+    X = _dev(X, "X")
+    Z = _dev(Z, "Z")
+    XX = _dev(XX, "XX")
+    dev = X.device
+    N, p = X.shape
+    M = XX.shape[0]
+    if len(theta) != p:
+        raise ValueError(f"theta must hold p={p} lengthscales")
+    th = (ctypes.c_double * p)(*[float(v) for v in theta])
+    out = dict(idx=torch.empty((M, n), dtype=torch.int32, device=dev),
+               mean=torch.empty(M, dtype=torch.float64, device=dev),
+               s2=torch.empty(M, dtype=torch.float64, device=dev),
+               var=torch.empty(M, dtype=torch.float64, device=dev),
+               flags=torch.empty(M, dtype=torch.int32, device=dev))
+    if gaps:
+        out["gaps"] = torch.empty((M, n - n0), dtype=torch.float64, device=dev)
+    tm = Timing()
+    st = lib().laGP_alc_batch_sep(
+        _ptr(X), N, p, _ptr(Z), _ptr(XX), M, th, float(g), int(n0), int(n), int(Nprime),
+        _ptr(out["idx"]), _ptr(out["mean"]), _ptr(out["s2"]), _ptr(out["var"]), _ptr(out["flags"]),
+        _ptr(out.get("gaps")), FORMS[form], ctypes.byref(tm) if timing else None, _stream(dev))
+    _check(st, (LAGP_OK, LAGP_PARTIAL))
+    out["status"] = st
+    if timing:
+        out["timing"] = tm.as_dict()
+    return out
+
+
 def mle(X, Z, XX, idx, d0, lo, hi, g, theta_in=None):
     """laGP_mle (row f2, Fig 1 step 3 + step 5): theta-hat of every local design
     idx [M×n] (CUDA int32) started at theta_in [M] (or d0), inside [lo, hi]; and

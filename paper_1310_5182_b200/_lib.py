@@ -30,6 +30,7 @@ EXPORTS = (
     "laGP_mle",
     "laGP_local_fit",
     "laGP_exp_nonpos",
+    "laGP_alc_batch_sep",
     "lagp_last_error",
     "lagp_abi_version",
 )
@@ -73,6 +74,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.laGP_local_fit.argtypes = [_vp, _i64, _i32, _vp, _vp, _i64, _dbl, _dbl, _dbl, _dbl, _i32, _i32, _i32,
                                    _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.POINTER(Timing), _vp]
     lib.laGP_exp_nonpos.argtypes = [_vp, _vp, _i64, _vp]
+    lib.laGP_alc_batch_sep.argtypes = [_vp, _i64, _i32, _vp, _vp, _i64, ctypes.POINTER(ctypes.c_double), _dbl,
+                                       _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
+                                       ctypes.POINTER(Timing), _vp]
     for f in EXPORTS[:-2]:
         getattr(lib, f).restype = ctypes.c_int
     lib.lagp_last_error.argtypes = []

@@ -336,6 +336,47 @@ lagp_status laGP_alc_batch_theta(const double *X, int64_t N, int32_t p, const do
                           flags_out, gap_out, alc_form, timing, cuda_stream);
 }
 
+lagp_status laGP_alc_batch_sep(const double *X, int64_t N, int32_t p, const double *Z, const double *XX,
+                               int64_t M, const double *theta, double g, int32_t n0, int32_t n, int32_t Nprime,
+                               int32_t *idx_out, double *mean_out, double *s2_out, double *var_out,
+                               uint32_t *flags_out, double *gap_out, int32_t alc_form, lagp_timing *timing,
+                               void *cuda_stream) {
+    lagp_status chk = check_batch_args(X, N, p, Z, XX, M, 1.0, g, n0, n, Nprime, idx_out, mean_out, s2_out);
+    if (chk != LAGP_OK) return chk;
+    chk = check_form(alc_form);
+    if (chk != LAGP_OK) return chk;
+    if (!theta) return fail(LAGP_EINVAL, "theta (host, p lengthscales) must be non-NULL");
+    lagp::SepScale sc{};
+    for (int k = 0; k < p; k++) {
+        if (!finite_pos(theta[k])) return fail(LAGP_EINVAL, "theta[%d] must be finite and > 0", k);
+        sc.s[k] = 1.0 / std::sqrt(theta[k]);  // same IEEE operations as oracle_sep_scale
+        if (!finite_pos(sc.s[k])) return fail(LAGP_EINVAL, "theta[%d] gives a non-finite 1/sqrt(theta)", k);
+    }
+    if (timing) std::memset(timing, 0, sizeof *timing);
+    if (M == 0) return LAGP_OK;
+    cudaGetLastError();
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    lagp_status st_ret = LAGP_OK;
+    {
+        Workspace ws(st);
+        double *Xs = nullptr, *XXs = nullptr;
+        LAGP_CUDA(ws.alloc((void **)&Xs, (size_t)N * p * sizeof(double)));
+        LAGP_CUDA(ws.alloc((void **)&XXs, (size_t)M * p * sizeof(double)));
+        LAGP_CUDA(lagp::launch_sep_scale(X, N, p, sc, Xs, st));
+        LAGP_CUDA(lagp::launch_sep_scale(XX, M, p, sc, XXs, st));
+        st_ret = alc_batch_impl(Xs, N, p, Z, XXs, M, nullptr, 1.0, g, n0, n, Nprime, idx_out, mean_out, s2_out,
+                                var_out, flags_out, gap_out, alc_form, timing, cuda_stream);
+        if (timing) timing->launches += 2;
+    }
+cleanup:
+    if (st_ret == LAGP_ECUDA || st_ret == LAGP_ENOMEM) return st_ret;
+    {
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    }
+    return st_ret;
+}
+
 lagp_status laGP_mle(const double *X, int64_t N, int32_t p, const double *Z, const double *XX, int64_t M,
                      const int32_t *idx, int32_t n, const double *theta_in, double theta0, double theta_min,
                      double theta_max, double g, double *theta_out, double *loglik_out, int32_t *iters_out,

@@ -20,6 +20,24 @@ __global__ void exp_nonpos_kernel(const double *__restrict__ x, double *__restri
         y[i] = exp_nonpos_tab(x[i], tab);
 }
 
+// row f3: x~[i][k] = x[i][k] * s[k] (s_k = 1/sqrt(theta_k), formed on the host),
+// the rescaling that turns the separable correlation into the isotropic one
+__global__ void sep_scale_kernel(const double *__restrict__ x, int64_t rows, int p, SepScale s,
+                                 double *__restrict__ out) {
+    const int64_t total = rows * p;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
+        out[e] = __dmul_rn(x[e], s.s[e % p]);
+}
+
+cudaError_t launch_sep_scale(const double *x, int64_t rows, int p, const SepScale &s, double *out, cudaStream_t st) {
+    const int64_t total = rows * p;
+    if (total <= 0) return cudaSuccess;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    sep_scale_kernel<<<(int)blocks, 256, 0, st>>>(x, rows, p, s, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_exp_nonpos(const double *x, double *y, int64_t n, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     int64_t blocks = (n + 255) / 256;

@@ -95,6 +95,10 @@ cudaError_t launch_alc_scores(int B, int j, int p, int nc, const double *Xj, con
 cudaError_t launch_pinv_update(int B, int j, const double *Kinv, const double *k, double kdiag, double *Kout,
                                cudaStream_t st);
 cudaError_t launch_exp_nonpos(const double *x, double *y, int64_t n, cudaStream_t st);
+struct SepScale {
+    double s[16];  // 1/sqrt(theta_k), k < p <= LAGP_PMAX
+};
+cudaError_t launch_sep_scale(const double *x, int64_t rows, int p, const SepScale &s, double *out, cudaStream_t st);
 cudaError_t launch_predict(int B, int n, int p, const double *Xn, const double *Yn, const double *x, double rtheta,
                            double eta, double *mean, double *s2, double *var, cudaStream_t st);
 

@@ -29,7 +29,7 @@ def test_header_declares_expected_entry_points():
     syms = declared_symbols()
     for s in ("laGP_alc_batch", "laGP_alc_scores", "lagp_last_error", "lagp_abi_version", "laGP_nn_pool",
               "laGP_pinv_update", "laGP_predict", "laGP_alc_batch_ex", "laGP_alc_batch_host", "laGP_alc_batch_theta",
-              "laGP_mle", "laGP_local_fit", "laGP_exp_nonpos"):
+              "laGP_mle", "laGP_local_fit", "laGP_exp_nonpos", "laGP_alc_batch_sep"):
         assert s in syms
 
 
@@ -111,3 +111,15 @@ def test_exp_nonpos_validates(lagp):
     assert "n must be" in lagp.last_error()
     assert lib.laGP_exp_nonpos(None, None, 4, None) == 2
     assert lib.laGP_exp_nonpos(None, None, 0, None) == 0
+
+
+def test_alc_batch_sep_validates(lagp):
+    import ctypes
+
+    lib = lagp.lib()
+    th = (ctypes.c_double * 2)(0.1, -1.0)
+    # p = 2, theta[1] <= 0 -> EINVAL before any device work (null device pointers are never touched)
+    st = lib.laGP_alc_batch_sep(1, 10, 2, 1, 1, 4, th, 1e-4, 2, 4, 6, 1, 1, 1, None, None, None, 1, None, None)
+    assert st == 2 and "theta[1]" in lagp.last_error()
+    st = lib.laGP_alc_batch_sep(1, 10, 2, 1, 1, 4, None, 1e-4, 2, 4, 6, 1, 1, 1, None, None, None, 1, None, None)
+    assert st == 2 and "theta" in lagp.last_error()
