@@ -31,7 +31,8 @@ extern "C" {
 #endif
 
 #define LAGP_ABI_VERSION 2
-#define LAGP_NMAX 128  /* largest local design size n supported (Fig 4 uses n <= 512: NEXT f4) */
+#define LAGP_SCORES_JMAX 768 /* laGP_alc_scores: largest j (Fig 4 goes to 512) */
+#define LAGP_NMAX 128  /* largest local design size n of the greedy path (laGP_alc_scores: LAGP_SCORES_JMAX) */
 #define LAGP_PMAX 16   /* largest input dimension p */
 #define LAGP_NPRIME_MAX 65536 /* largest candidate pool N' (laGP_alc_batch; the incremental
                                  form takes N' <= 8192, laGP_nn_pool's sorted output N' <= 8192) */
@@ -159,7 +160,12 @@ lagp_status laGP_nn_pool(const double *X, int64_t N, int32_t p, const double *XX
  *   best_out  [B] int32: position (0..nc-1) of the argmax, ties to the lowest
  *             cand_idx (R7); -1 if every candidate is excluded;
  *   gap_out   [B] nullable: top-2 relative gap.
- * Constraints: 1 <= j <= LAGP_NMAX, nc >= 1, 1 <= p <= LAGP_PMAX.
+ * Constraints: 1 <= j <= LAGP_SCORES_JMAX, nc >= 1, 1 <= p <= LAGP_PMAX.
+ * Also the paper's Fig 4 experiment (one location,
+ * N' = 60,000 candidates, n = 16..512): beyond small batches the scores run as
+ * a dense FP64 tensor-core contraction U = K^{-1}[k_c1..k_cT] over 32-candidate
+ * tiles (alc_scores_gemm.cu), q_c = sum_a k_c[a] U[a][c]; the library owns a
+ * stream-ordered workspace of B·(j + 4·ceil(nc/32)) doubles for the call.
  */
 lagp_status laGP_alc_scores(int32_t B, int32_t j, int32_t p, int32_t nc, const double *Xj,
                             const double *Kinv, const double *cands, const int32_t *cand_idx,

@@ -617,7 +617,8 @@ lagp_status laGP_alc_scores(int32_t B, int32_t j, int32_t p, int32_t nc, const d
                             const double *cands, const int32_t *cand_idx, const double *x, double d, double g,
                             double *delta_out, int32_t *best_out, double *gap_out, void *cuda_stream) {
     if (B < 0) return fail(LAGP_EINVAL, "B must be >= 0");
-    if (j < 1 || j > LAGP_NMAX) return fail(LAGP_EINVAL, "j must be in [1, %d] (got %d)", LAGP_NMAX, j);
+    if (j < 1 || j > LAGP_SCORES_JMAX)
+        return fail(LAGP_EINVAL, "j must be in [1, %d] (got %d)", LAGP_SCORES_JMAX, j);
     if (p < 1 || p > LAGP_PMAX) return fail(LAGP_EINVAL, "p must be in [1, %d] (got %d)", LAGP_PMAX, p);
     if (nc < 1) return fail(LAGP_EINVAL, "nc must be >= 1 (got %d)", nc);
     if (!finite_pos(d)) return fail(LAGP_EINVAL, "d (theta) must be finite and > 0");
@@ -625,12 +626,30 @@ lagp_status laGP_alc_scores(int32_t B, int32_t j, int32_t p, int32_t nc, const d
     if (B > 0 && (!Xj || !Kinv || !cands || !cand_idx || !x || !best_out))
         return fail(LAGP_EINVAL, "Xj, Kinv, cands, cand_idx, x and best_out must be non-NULL");
     if (B == 0) return LAGP_OK;
+    cudaGetLastError();
     cudaStream_t st = (cudaStream_t)cuda_stream;
-    cudaError_t e = lagp::launch_alc_scores(B, j, p, nc, Xj, Kinv, cands, cand_idx, x, 1.0 / d, g, delta_out, best_out,
-                                            gap_out, st);
-    if (e != cudaSuccess) return cuda_fail(e, "alc_scores_kernel");
-    e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    lagp_status st_ret = LAGP_OK;
+    {
+        // many small problems: one CTA per location (K^{-1} in shared memory); otherwise
+        // the DMMA contraction over candidate tiles (row f4, alc_scores_gemm.cu)
+        const bool small = j <= 64 && nc <= 1024 && (int64_t)B * 4 >= num_sms();
+        Workspace ws(st);
+        if (small) {
+            LAGP_CUDA(lagp::launch_alc_scores(B, j, p, nc, Xj, Kinv, cands, cand_idx, x, 1.0 / d, g, delta_out,
+                                              best_out, gap_out, st));
+        } else {
+            void *w = nullptr;
+            LAGP_CUDA(ws.alloc(&w, lagp::alc_scores_gemm_ws_bytes(B, j, nc)));
+            LAGP_CUDA(lagp::launch_alc_scores_gemm(B, j, p, nc, Xj, Kinv, cands, cand_idx, x, 1.0 / d, g, delta_out,
+                                                   best_out, gap_out, w, st, nullptr));
+        }
+    }
+cleanup:
+    {
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (st_ret != LAGP_OK) return st_ret;
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    }
     return LAGP_OK;
 }
 

@@ -92,6 +92,13 @@ cudaError_t launch_mle(const MleArgs &a, int grid, cudaStream_t st);
 cudaError_t launch_alc_scores(int B, int j, int p, int nc, const double *Xj, const double *Kinv, const double *cands,
                               const int32_t *cand_idx, const double *x, double rtheta, double eta, double *delta,
                               int32_t *best, double *gap, cudaStream_t st);
+// alc_scores_gemm.cu (row f4): a3 alone as a dense FP64 DMMA contraction, j <= LAGP_SCORES_JMAX
+size_t alc_scores_gemm_smem(int j, int p);
+size_t alc_scores_gemm_ws_bytes(int B, int j, int nc);
+cudaError_t launch_alc_scores_gemm(int B, int j, int p, int nc, const double *Xj, const double *Kinv,
+                                   const double *cands, const int32_t *cand_idx, const double *x, double rtheta,
+                                   double eta, double *delta, int32_t *best, double *gap, void *ws, cudaStream_t st,
+                                   int *launches);
 cudaError_t launch_pinv_update(int B, int j, const double *Kinv, const double *k, double kdiag, double *Kout,
                                cudaStream_t st);
 cudaError_t launch_exp_nonpos(const double *x, double *y, int64_t n, cudaStream_t st);

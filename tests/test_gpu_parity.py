@@ -58,11 +58,15 @@ def test_nn_pool_massive_ties_fallback(torch_dev, lagp):
 
 
 # ------------------------------------------------------------ a3: ALC score
-@pytest.mark.parametrize("j,p,nc", [(1, 2, 40), (6, 2, 500), (23, 8, 300), (49, 3, 1000), (128, 8, 77)])
-def test_alc_scores_vs_oracle(torch_dev, lagp, j, p, nc):
+@pytest.mark.parametrize("j,p,nc,B", [(1, 2, 40, 4), (6, 2, 500, 4), (23, 8, 300, 4), (49, 3, 1000, 4),
+                                       (128, 8, 77, 4), (6, 2, 500, 600), (100, 3, 5000, 3), (256, 2, 3000, 2),
+                                       (512, 8, 2000, 1), (16, 2, 60000, 1), (768, 4, 300, 1)])
+def test_alc_scores_vs_oracle(torch_dev, lagp, j, p, nc, B):
+    """a3 alone against oracle_alc_scores: the one-CTA-per-location kernel (small
+    batches) and the DMMA contraction (row f4: the paper's Fig 4 scale, j <= 768,
+    N' = 60,000)."""
     torch, dev = torch_dev
     rng = np.random.default_rng(j * 100 + p)
-    B = 4
     d, g = 0.3 if p > 3 else 0.05, 1e-4
     Xj = rng.random((B, j, p))
     cands = rng.random((B, nc, p))
@@ -74,12 +78,25 @@ def test_alc_scores_vs_oracle(torch_dev, lagp, j, p, nc):
                                        T(torch, dev, cidx), T(torch, dev, x), d, g)
     delta = delta.cpu().numpy()
     best = best.cpu().numpy()
-    for b in range(B):
+    for b in range(min(B, 6)):
         ref, _, minv = oracle.alc_scores(Xj[b], Kinv[b], cands[b], x[b], d, g)
         ok = minv > 1e-12
         scale = np.abs(ref[ok]).max()
-        # explicit-inverse noise: eps * cond * j / min(s) (pin P1 ill-conditioned bound)
-        assert np.abs(delta[b][ok] - ref[ok]).max() <= max(1e-9, 1e-5 if p <= 3 else 1e-8) * scale
+        # explicit-inverse noise: eps * cond * j / min(s) (pin P1 ill-conditioned bound), or
+        # per candidate the first-order forward-error bound of two FP64 evaluations of
+        # s = 1 + g - k^T K^{-1} k and cov = kappa - (K^{-1} h)^T k in different orders:
+        # |ds| <= 4 j eps |k|^T |K^{-1}| |k|, |dcov| <= 4 j eps (|K^{-1}| |h|)^T |k|
+        eps = 2.0 ** -53
+        kc = np.exp(-((cands[b][:, None, :] - Xj[b][None]) ** 2).sum(-1) / d)
+        hb = np.exp(-((Xj[b] - x[b]) ** 2).sum(-1) / d)
+        aK = np.abs(Kinv[b])
+        ds = 4 * j * eps * np.einsum("ca,ab,cb->c", kc, aK, kc)
+        dcv = 4 * j * eps * (kc @ (aK @ hb)) + 4 * eps
+        sv = np.where(ok, minv, 1.0)
+        cov = np.sqrt(np.maximum(ref, 0) * sv)
+        bound = (np.maximum(ref, 0) * ds / sv + 2 * cov * dcv / sv + dcv ** 2 / sv)[ok]
+        tol = np.maximum(max(1e-9, 1e-5 if p <= 3 else 1e-8) * scale, 4 * bound)
+        assert np.all(np.abs(delta[b][ok] - ref[ok]) <= tol)
         assert np.all(np.isneginf(delta[b][~ok]))
         o = np.lexsort((cidx[b][ok], -ref[ok]))[0]
         ob = np.where(ok)[0][o]
