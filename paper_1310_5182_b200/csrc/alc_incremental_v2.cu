@@ -49,9 +49,45 @@ struct V2R {
     static constexpr int value = (CPT == 1) ? 16 : (CPT == 2 ? (P <= 4 ? 8 : 4) : (P <= 4 ? 8 : 6));
 };
 
-// warp post record (doubles): key | gidx,pos | key2 | - | x[8] | rrho z y - | w[R]
+// TMEM entries per candidate: each thread owns 512 B of tensor memory (512 columns
+// x 128 lanes / 512 threads), i.e. 64 doubles shared by its CPT candidates
+template <int CPT>
+struct V2T {
+    static constexpr int value = 64 / CPT;
+};
+
+// warp post record (doubles): key | gidx,pos | key2 | - | x[8] | rrho z y - | w[R] | w[TMEM part]
 enum { RK = 0, RI = 1, RK2 = 2, RX = 4, RRHO = 12, RZN = 13, RYN = 14, RW = 16 };
-__host__ __device__ constexpr int v2_rec(int R) { return RW + R; }
+__host__ __device__ constexpr int v2_rec(int R, int T) { return RW + R + T; }
+
+// ---- tensor memory as per-thread storage (tcgen05; thread-private lane rows)
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, double (&v)[4]) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < 4; k++) v[k] = __hiloint2double((int)r[2 * k + 1], (int)r[2 * k]);
+}
+// 16 columns (8 doubles) of this thread's row; tm_wait_ld() before using r
+__device__ __forceinline__ void tm_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ double tm_d(const uint32_t (&r)[16], int k) {
+    return __hiloint2double((int)r[2 * k + 1], (int)r[2 * k]);
+}
+__device__ __forceinline__ void tm_st1(uint32_t taddr, double v) {
+    const uint32_t lo = (uint32_t)__double2loint(v), hi = (uint32_t)__double2hiint(v);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(taddr), "r"(lo), "r"(hi) : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ double fast_div_pos(double a, double b) {
     // a / b for finite b > 0 (not tiny): reciprocal seed, one Newton step, then
@@ -88,22 +124,40 @@ __device__ volatile double g_v2_sink;
 
 template <int P, int CPT, int TH>
 __global__ void __launch_bounds__(TH, 1)
-alc_incremental_v2_kernel(AlcArgs A, int S) {
+alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
     constexpr int R = V2R<P, CPT>::value;
     constexpr int V2_THREADS = TH;
     constexpr int V2_NW = TH / 32;
     constexpr int NPC = V2_THREADS * CPT;  // columns (candidates) per pair row
-    constexpr int REC = v2_rec(R);
+    constexpr int T = V2T<CPT>::value;      // entries [R+S, R+S+T) in tensor memory
+    constexpr int REC = v2_rec(R, T);
+    constexpr int RT = RW + R;              // record offset of the TMEM entries
     extern __shared__ __align__(16) double sm[];
     double2 *wsm2 = reinterpret_cast<double2 *>(sm);          // [S/2][NPC] pairs of entries [R, R+S)
     double *post = sm + (size_t)S * NPC;                      // [2][NW][REC]
     const int n = A.n, Np = A.Nprime, n0 = A.n0;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int RS = R + S;
+    // entry tiers of w_c: registers [0, R), tensor memory [T0, T1), shared memory
+    // [S0, S1), L2 slab [G0, n); tfirst puts tensor memory before shared memory
+    const int T0 = tfirst ? R : R + S, T1 = T0 + T;
+    const int S0 = tfirst ? R + T : R, S1 = S0 + S;
+    const int G0 = R + S + T;
     const int G = n - n0;
     const double eta = A.eta;
-    double2 *gw2 = reinterpret_cast<double2 *>(A.cache + (size_t)blockIdx.x * A.cache_stride);  // [(a-RS)/2][NPC]
+    double2 *gw2 = reinterpret_cast<double2 *>(A.cache + (size_t)blockIdx.x * A.cache_stride);  // [(a-RST)/2][NPC]
     __shared__ double xq[8];
+    __shared__ uint32_t s_taddr;
+    // all 512 TMEM columns (one CTA per SM); warp w owns lanes 32(w%4).. and columns
+    // 128(w/4).. : candidate slot q's entry e at column 2(qT + e)
+    if (wid == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&s_taddr)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tbase = s_taddr + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)(128 * (wid >> 2));
     __shared__ double zyv[2][LAGP_NMAX];  // z_j, y~_j of every append (a5)
     __shared__ double s_exptab[32];        // 2^(k/32) for exp_nonpos_tab
     if (threadIdx.x < 32) s_exptab[threadIdx.x] = c_exp2_32[threadIdx.x];
@@ -152,7 +206,17 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
             const double *rec;
             if (j < n0) {
                 // forced NN append (a2): pool position j (thread j, q = 0; j < n <= LAGP_NMAX <= TH)
-                // posts to slot 0
+                // posts to slot 0; its TMEM entries through a load by its whole warp
+                if (j > T0 && wid == (j >> 5)) {
+                    const int mt = (j < T1 ? j : T1) - T0;
+                    for (int e = 0; e < mt; e += 4) {
+                        double v[4];
+                        tm_ld8(tbase + 2 * e, v);
+                        if (tid == j)
+#pragma unroll
+                            for (int k = 0; k < 4; k++) pst[RT + e + k] = e + k < mt ? v[k] : 0.0;
+                    }
+                }
                 if (tid == j) {
                     double *r = pst;
                     const double rho = sqrt(s[0]);
@@ -212,6 +276,19 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
                 const unsigned long long sk = wl ? k2 : kb;
                 const unsigned sh = __reduce_max_sync(0xffffffffu, (unsigned)(sk >> 32));
                 const unsigned sl = __reduce_max_sync(0xffffffffu, (unsigned)(sk >> 32) == sh ? (unsigned)sk : 0u);
+                if (j > T0) {  // the warp winner's TMEM entries: a warp-collective load of its slot
+                    const int wlane = __ffs(__ballot_sync(0xffffffffu, wl)) - 1;
+                    const int qsel = __shfl_sync(0xffffffffu, qb, wlane);
+                    const int mt = (j < T1 ? j : T1) - T0;
+                    double *r = pst + wid * REC + RT;
+                    for (int e = 0; e < mt; e += 4) {
+                        double v[4];
+                        tm_ld8(tbase + 2 * (qsel * T + e), v);
+                        if (wl)
+#pragma unroll
+                            for (int k = 0; k < 4; k++) r[e + k] = e + k < mt ? v[k] : 0.0;
+                    }
+                }
                 if (wl) {
                     double *r = pst + wid * REC;
                     reinterpret_cast<unsigned long long *>(r)[RK] = kb;
@@ -310,9 +387,28 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
                 for (int q = 0; q < CPT; q++) kx[q] = exp_nonpos_tab(-d2[q] * rth, s_exptab);
             };
             auto dot_phase = [&]() {
-            // slab entries [RS, j) (L2-resident), two pairs per iteration
-            if (j > RS) {
-                const int m = j - RS;
+            // tensor-memory entries [T0, min(j, T1)): own rows by tcgen05.ld, the
+            // winner's from its record
+            if (j > T0) {
+                const int mt = (j < T1 ? j : T1) - T0;
+                for (int e = 0; e < mt; e += 4) {
+                    const double2 w01 = *reinterpret_cast<const double2 *>(rec + RT + e);
+                    const double2 w23 = *reinterpret_cast<const double2 *>(rec + RT + e + 2);
+#pragma unroll
+                    for (int q = 0; q < CPT; q++) {
+                        double v[4];
+                        tm_ld8(tbase + 2 * (q * T + e), v);
+                        // entries >= mt of this chunk are stale on both sides: masked to 0
+                        acc[q][0] = fma(w01.x, v[0], acc[q][0]);
+                        acc[q][1] = fma(w01.y, e + 1 < mt ? v[1] : 0.0, acc[q][1]);
+                        acc[q][0] = fma(w23.x, e + 2 < mt ? v[2] : 0.0, acc[q][0]);
+                        acc[q][1] = fma(w23.y, e + 3 < mt ? v[3] : 0.0, acc[q][1]);
+                    }
+                }
+            }
+            // slab entries [G0, j) (L2-resident), two pairs per iteration
+            if (j > G0) {
+                const int m = j - G0;
                 const double2 *gwin = gw2 + cstar;
                 const double2 *gown = gw2 + tid;
                 const int np = m >> 1;
@@ -345,9 +441,9 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
                     acc[q][1] = fma(wv.y, wr[q][a + 1], acc[q][1]);
                 }
             }
-            // shared entries [R, min(j, RS)): one LDS.128 per two entries of a column
-            if (j > R) {
-                const int m = (j < RS ? j : RS) - R;
+            // shared entries [S0, min(j, S1)): one LDS.128 per two entries of a column
+            if (j > S0) {
+                const int m = (j < S1 ? j : S1) - S0;
                 const double2 *swin = wsm2 + cstar;
                 const double2 *sown = wsm2 + tid;
                 const int np = m >> 1;
@@ -388,16 +484,18 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
 #pragma unroll
                     for (int b = 0; b < R; b++)
                         if (b == j) wr[q][b] = wn;
-                } else if (j < RS) {
-                    reinterpret_cast<double *>(wsm2 + ((j - R) >> 1) * NPC + c)[(j - R) & 1] = wn;
+                } else if (j >= S0 && j < S1) {
+                    reinterpret_cast<double *>(wsm2 + ((j - S0) >> 1) * NPC + c)[(j - S0) & 1] = wn;
+                } else if (j >= T0 && j < T1) {
+                    tm_st1(tbase + 2 * (q * T + (j - T0)), wn);
                 } else {
-                    reinterpret_cast<double *>(gw2 + ((j - RS) >> 1) * NPC + c)[(j - RS) & 1] = wn;
+                    reinterpret_cast<double *>(gw2 + ((j - G0) >> 1) * NPC + c)[(j - G0) & 1] = wn;
                 }
                 s[q] = fma(-wn, wn, s[q]);
-
                 cov[q] = fma(-znew, wn, cov[q]);
                 tc[q] = fma(-ynew, wn, tc[q]);
             }
+            if (j >= T0 && j < T1) tm_wait_st();  // this step's TMEM stores land before the next reads
         }
 
         // ---- flags and a5: mean = z^T y~, psi = ||y~||^2, s2 = psi (1 + eta - ||z||^2) / j
@@ -434,16 +532,19 @@ alc_incremental_v2_kernel(AlcArgs A, int S) {
         }
         __syncthreads();
     }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    if (wid == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(s_taddr));
 }
 
 // ---------------------------------------------------------------- host side
 template <int P, int CPT>
-static cudaError_t v2_launch_t(const AlcArgs &a, int S, int grid, size_t smem, cudaStream_t st) {
+static cudaError_t v2_launch_t(const AlcArgs &a, int S, int tfirst, int grid, size_t smem, cudaStream_t st) {
     constexpr int TH = v2_threads(CPT);
     cudaError_t e = cudaFuncSetAttribute(alc_incremental_v2_kernel<P, CPT, TH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    alc_incremental_v2_kernel<P, CPT, TH><<<grid, TH, smem, st>>>(a, S);
+    alc_incremental_v2_kernel<P, CPT, TH><<<grid, TH, smem, st>>>(a, S, tfirst);
     return cudaGetLastError();
 }
 
@@ -472,7 +573,8 @@ bool inc_v2_plan(int n, int p, int Nprime, size_t smem_optin, IncPlan &pl) {
     if (R < 0) return false;
     const int th = v2_threads(cpt);
     const int npc = th * cpt;
-    const size_t fixed = (size_t)2 * (th / 32) * v2_rec(R) * sizeof(double);
+    const int T = cpt == 1 ? V2T<1>::value : cpt == 2 ? V2T<2>::value : V2T<4>::value;
+    const size_t fixed = (size_t)2 * (th / 32) * v2_rec(R, T) * sizeof(double);
     if (smem_optin < fixed + 2048) return false;
     const size_t pair_bytes = (size_t)npc * 2 * sizeof(double);
     int S = 2 * (int)((smem_optin - fixed - 2048) / pair_bytes);
@@ -482,10 +584,12 @@ bool inc_v2_plan(int n, int p, int Nprime, size_t smem_optin, IncPlan &pl) {
     pl = IncPlan{};
     pl.ok = true;
     pl.v2 = true;
+    const char *tf = getenv("LAGP_V2_TFIRST");  // A/B: 1 = tensor memory before shared memory
+    pl.tfirst = (tf && tf[0] == '1') ? 1 : 0;  // measured: TMEM after shared memory is faster
     pl.cpt = cpt;
     pl.R = R;
     pl.S = S;
-    pl.global_entries = n - R - S > 0 ? n - R - S : 0;
+    pl.global_entries = n - R - S - T > 0 ? n - R - S - T : 0;
     pl.smem = (size_t)S * npc * sizeof(double) + fixed;
     pl.wsz = S * npc;
     pl.cache_doubles = (int64_t)((pl.global_entries + 1) & ~1) * npc + 16;
@@ -495,11 +599,11 @@ bool inc_v2_plan(int n, int p, int Nprime, size_t smem_optin, IncPlan &pl) {
 cudaError_t launch_alc_incremental_v2(const AlcArgs &a, const IncPlan &pl, int grid, cudaStream_t st) {
 #define V2_DISPATCH(CPT_)                                                         \
     switch (a.p) {                                                                \
-        case 1: return v2_launch_t<1, CPT_>(a, pl.S, grid, pl.smem, st);          \
-        case 2: return v2_launch_t<2, CPT_>(a, pl.S, grid, pl.smem, st);          \
-        case 3: return v2_launch_t<3, CPT_>(a, pl.S, grid, pl.smem, st);          \
-        case 4: return v2_launch_t<4, CPT_>(a, pl.S, grid, pl.smem, st);          \
-        case 8: return v2_launch_t<8, CPT_>(a, pl.S, grid, pl.smem, st);          \
+        case 1: return v2_launch_t<1, CPT_>(a, pl.S, pl.tfirst, grid, pl.smem, st);          \
+        case 2: return v2_launch_t<2, CPT_>(a, pl.S, pl.tfirst, grid, pl.smem, st);          \
+        case 3: return v2_launch_t<3, CPT_>(a, pl.S, pl.tfirst, grid, pl.smem, st);          \
+        case 4: return v2_launch_t<4, CPT_>(a, pl.S, pl.tfirst, grid, pl.smem, st);          \
+        case 8: return v2_launch_t<8, CPT_>(a, pl.S, pl.tfirst, grid, pl.smem, st);          \
         default: return cudaErrorInvalidValue;                                    \
     }
     if (pl.cpt == 1) { V2_DISPATCH(1) }
