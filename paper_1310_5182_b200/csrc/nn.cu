@@ -617,6 +617,8 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
             // 4 rows per thread per iteration: each query's coordinates are loaded
             // from shared memory once per 4 rows
             // (the loop bound is warp-uniform: the ballots below need whole warps)
+            // per-warp append counters in registers: lane q holds this warp's count for query q
+            int wcr = 0;
             for (int64_t wbase = tid - lane; wbase < N; wbase += 4 * (int64_t)blockDim.x) {
                 const int64_t base = wbase + lane;
                 float xf[4][P ? P : LAGP_PMAX];
@@ -640,29 +642,34 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                     for (int k = 0; k < (P ? P : LAGP_PMAX); k++) qv[k] = s.qf[q][k];
                     const float qn = s.qn2f[q], thr = s.thrf[q];
                     bool hit[4];
+                    unsigned mm[4];
 #pragma unroll
-                    for (int u = 0; u < 4; u++) hit[u] = fmaf(-2.f, row_dotf<P>(xf[u], qv, p), qn + rn[u]) <= thr;
+                    for (int u = 0; u < 4; u++) {
+                        hit[u] = fmaf(-2.f, row_dotf<P>(xf[u], qv, p), qn + rn[u]) <= thr;
+                        mm[u] = __ballot_sync(0xffffffffu, hit[u]);
+                    }
                     // append to this warp's own segment of the query's buffer: the warp
-                    // owns its counter, so positions come from ballots alone (no atomics)
-                    if (__any_sync(0xffffffffu, hit[0] | hit[1] | hit[2] | hit[3])) {
-                        int wc = s.wcnt[wid][q];
+                    // owns its counter, so positions come from ballots alone (no atomics);
+                    // only the 4-row groups with a hit do any work
+                    if (mm[0] | mm[1] | mm[2] | mm[3]) {
+                        int wc = __shfl_sync(0xffffffffu, wcr, q);
                         const unsigned lt = (1u << lane) - 1u;
                         int32_t *seg = bufi + q * bufcap + wid * segcap;
 #pragma unroll
                         for (int u = 0; u < 4; u++) {
-                            const unsigned m = __ballot_sync(0xffffffffu, hit[u]);
-                            const int pos = wc + __popc(m & lt);
-                            if (hit[u] && pos < segcap) seg[pos] = (int)(base + u * (int64_t)blockDim.x);
-                            wc += __popc(m);
+                            if (mm[u]) {
+                                const int pos = wc + __popc(mm[u] & lt);
+                                if (hit[u] && pos < segcap) seg[pos] = (int)(base + u * (int64_t)blockDim.x);
+                                wc += __popc(mm[u]);
+                            }
                         }
-                        __syncwarp();
-                        if (lane == 0) {
-                            s.wcnt[wid][q] = wc;
-                            if (wc > segcap) s.ovf[q] = 1;
-                        }
-                        __syncwarp();
+                        if (lane == q) wcr = wc;
                     }
                 }
+            }
+            if (lane < NN_Q) {
+                s.wcnt[wid][lane] = wcr;
+                if (wcr > segcap) s.ovf[lane] = 1;
             }
             __syncthreads();
             // dense exact pass over the prefilter survivors (the warp segments read as
