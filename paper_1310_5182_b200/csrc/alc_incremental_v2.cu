@@ -89,6 +89,18 @@ __device__ __forceinline__ void tm_st1(uint32_t taddr, double v) {
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// s^{-1/2} for s > 0: reciprocal-square-root seed and two Newton steps
+// (r <- r + r(1 - s r^2)/2); s <= 0 gives NaN (a non-PD append, flagged NONFINITE)
+__device__ __forceinline__ double rsqrt_nr(double s) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
+    double e = fma(-s * r, r, 1.0);
+    r = fma(0.5 * r, e, r);
+    e = fma(-s * r, r, 1.0);
+    r = fma(0.5 * r, e, r);
+    return s > 0.0 ? r : __longlong_as_double(0x7ff8000000000000LL);
+}
+
 __device__ __forceinline__ double fast_div_pos(double a, double b) {
     // a / b for finite b > 0 (not tiny): reciprocal seed, one Newton step, then
     // one residual correction of the quotient (no special-case path)
@@ -219,13 +231,11 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
                 }
                 if (tid == j) {
                     double *r = pst;
-                    const double rho = sqrt(s[0]);
-                    const double rr = 1.0 / rho;
 #pragma unroll
                     for (int k = 0; k < P; k++) r[RX + k] = xc[0][k];
-                    r[RRHO] = rr;
-                    r[RZN] = cov[0] * rr;
-                    r[RYN] = tc[0] * rr;
+                    r[RRHO] = s[0];  // raw s, cov, t: the readers scale by 1/sqrt(s)
+                    r[RZN] = cov[0];
+                    r[RYN] = tc[0];
 #pragma unroll
                     for (int a = 0; a < R; a += 2)
                         *reinterpret_cast<double2 *>(r + RW + a) = make_double2(wr[0][a], wr[0][a + 1]);
@@ -298,13 +308,11 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
 #pragma unroll
                     for (int q = 0; q < CPT; q++) {
                         if (q == qb) {
-                            const double rho = sqrt(s[q]);
-                            const double rr = 1.0 / rho;
 #pragma unroll
                             for (int k = 0; k < P; k++) r[RX + k] = xc[q][k];
-                            r[RRHO] = rr;
-                            r[RZN] = cov[q] * rr;
-                            r[RYN] = tc[q] * rr;
+                            r[RRHO] = s[q];  // raw s, cov, t: the readers scale by 1/sqrt(s)
+                            r[RZN] = cov[q];
+                            r[RYN] = tc[q];
 #pragma unroll
                             for (int a = 0; a < R; a += 2)
                                 *reinterpret_cast<double2 *>(r + RW + a) = make_double2(wr[q][a], wr[q][a + 1]);
@@ -354,7 +362,8 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
 #pragma unroll
             for (int q = 0; q < CPT; q++)
                 if (cstar == tid + q * V2_THREADS) chosen[q] = true;
-            const double rrho = rec[RRHO], znew = rec[RZN], ynew = rec[RYN];
+            // 1/rho = s*^{-1/2} (off the posting lanes' path: every thread forms it)
+            const double rrho = rsqrt_nr(rec[RRHO]), znew = rec[RZN] * rrho, ynew = rec[RYN] * rrho;
             V2_PROBE(4, rrho);
             if (tid == V2_THREADS - 1) {  // a5 state (summed once at the end)
                 zyv[0][j] = znew;
@@ -371,20 +380,20 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
             // K(x_c, x*) first: branch-free, so the CPT chains interleave and overlap
             // the slab loads below
             auto kx_phase = [&]() {
-                double d2[CPT];
+                double d2[CPT][2];  // two partial sums: half the dependent-chain depth
 #pragma unroll
-                for (int q = 0; q < CPT; q++) d2[q] = 0.0;
+                for (int q = 0; q < CPT; q++) d2[q][0] = d2[q][1] = 0.0;
 #pragma unroll
                 for (int k = 0; k < P; k++) {
                     const double xs = rec[RX + k];
 #pragma unroll
                     for (int q = 0; q < CPT; q++) {
-                        const double diff = __dsub_rn(xc[q][k], xs);
-                        d2[q] = __fma_rn(diff, diff, d2[q]);
+                        const double diff = xc[q][k] - xs;
+                        d2[q][k & 1] = fma(diff, diff, d2[q][k & 1]);
                     }
                 }
 #pragma unroll
-                for (int q = 0; q < CPT; q++) kx[q] = exp_nonpos_tab(-d2[q] * rth, s_exptab);
+                for (int q = 0; q < CPT; q++) kx[q] = exp_nonpos_tab(-(d2[q][0] + d2[q][1]) * rth, s_exptab);
             };
             auto dot_phase = [&]() {
             // tensor-memory entries [T0, min(j, T1)): own rows by tcgen05.ld, the
