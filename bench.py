@@ -5,7 +5,8 @@ Workload (BASELINE.json configs[1], the metric's single-GPU configuration):
 C2 — 8-d borehole, N = 100,000 LHS design, M = 10,000 LHS predictive locations
 per GPU, n0 = 6, n = 50, N' = 1000, d = q10 rule, g = 1e-4.
 A "step" is one laGP_alc_batch call over the rank's M locations (NN pool, ALC
-greedy loop, partitioned-inverse updates, prediction — every §8(a) row).
+greedy loop, partitioned-inverse updates, prediction — every §8(a) row), and
+with N > 1 GPUs the all-gather of every rank's results (NCCL).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
@@ -255,6 +256,8 @@ def main():
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             res = lagp.alc_batch(X, Z, XX, d, g, n0, n, Np, form=form, timing=True)
+            if world > 1:  # the one collective, results all-gathered in input order
+                lagp.gather_shards(res, M_all)
             e1.record(stream)
             barrier()
             total += e0.elapsed_time(e1)
