@@ -18,7 +18,7 @@ from lagp_data import make_config  # noqa: E402
 dev = torch.device("cuda", 0)
 T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
 for name, over, M in (("C1", {}, 6), ("C2", dict(Nprime=300, n=30), 4), ("C1", dict(n0=1, n=12, Nprime=40), 3),
-                      ("C1", dict(n=80, Nprime=600), 2)):
+                      ("C1", dict(n=80, Nprime=600), 2), ("C2", dict(n=64, Nprime=1000), 2)):
     cfg = make_config(name, M=M, N=5000 if name == "C2" else None, **over)
     args = (cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"])
     for form in ("explicit", "explicit_dfma", "incremental"):
@@ -39,3 +39,15 @@ lagp.pinv_update(T(Kinv), T(rng.random((B, j))), 1.001)
 lagp.predict(T(Xj), T(rng.random((B, j))), T(rng.random((B, p))), 0.1, 1e-3)
 torch.cuda.synchronize()
 print("sanitize run done")
+# row f4 path (DMMA contraction), row f3 (separable), row f2 (MLE / two-stage), table exp
+B, j, nc = 1, 100, 2000
+Xj = rng.random((B, j, p))
+K = np.exp(-((Xj[:, :, None] - Xj[:, None]) ** 2).sum(-1) / 0.1) + 1e-3 * np.eye(j)
+lagp.alc_scores(T(Xj), T(np.linalg.inv(K)), T(rng.random((B, nc, p))), T(np.arange(nc, dtype=np.int32)[None]),
+                T(rng.random((B, p))), 0.1, 1e-3)
+cfg = make_config("C1", M=3)
+lagp.alc_batch_sep(T(cfg["X"]), T(cfg["Z"]), T(cfg["XX"]), [0.02, 0.07], cfg["g"], 6, 40, 500)
+lagp.local_fit(T(cfg["X"]), T(cfg["Z"]), T(cfg["XX"]), cfg["d"], 1e-3, 10.0, cfg["g"], 6, 30, 500, stages=2)
+lagp.exp_nonpos(T(-rng.random(1000) * 50))
+torch.cuda.synchronize()
+print("sanitize run done (f2-f4)")
