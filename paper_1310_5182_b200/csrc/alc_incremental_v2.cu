@@ -89,18 +89,6 @@ __device__ __forceinline__ void tm_st1(uint32_t taddr, double v) {
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// s^{-1/2} for s > 0: reciprocal-square-root seed and two Newton steps
-// (r <- r + r(1 - s r^2)/2); s <= 0 gives NaN (a non-PD append, flagged NONFINITE)
-__device__ __forceinline__ double rsqrt_nr(double s) {
-    double r;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
-    double e = fma(-s * r, r, 1.0);
-    r = fma(0.5 * r, e, r);
-    e = fma(-s * r, r, 1.0);
-    r = fma(0.5 * r, e, r);
-    return s > 0.0 ? r : __longlong_as_double(0x7ff8000000000000LL);
-}
-
 __device__ __forceinline__ double fast_div_pos(double a, double b) {
     // a / b for finite b > 0 (not tiny): reciprocal seed, one Newton step, then
     // one residual correction of the quotient (no special-case path)

@@ -98,6 +98,18 @@ __device__ __forceinline__ double exp_nonpos_tab(double x, const double *tab) {
     return x < -708.0 ? 0.0 : (x == x ? v : x);
 }
 
+// s^{-1/2} for s > 0: reciprocal-square-root seed and two Newton steps
+// (r <- r + r(1 - s r^2)/2); s <= 0 gives NaN (a non-PD append, flagged NONFINITE)
+__device__ __forceinline__ double rsqrt_nr(double s) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
+    double e = fma(-s * r, r, 1.0);
+    r = fma(0.5 * r, e, r);
+    e = fma(-s * r, r, 1.0);
+    r = fma(0.5 * r, e, r);
+    return s > 0.0 ? r : __longlong_as_double(0x7ff8000000000000LL);
+}
+
 // Isotropic Gaussian correlation exp(-d2/theta) with rtheta = 1/theta.
 __device__ __forceinline__ double corr_from_d2(double d2, double rtheta) { return exp_nonpos(-d2 * rtheta); }
 

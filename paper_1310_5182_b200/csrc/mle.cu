@@ -32,6 +32,28 @@ struct MleEval {
     bool ok;
 };
 
+// Sums of K values over the CTA in one pass (two barriers); every thread gets
+// the sums. Warp partials by a fixed shuffle tree, then summed in warp order.
+template <int K>
+__device__ __forceinline__ void block_sum_n(double (&v)[K], double *scratch /* >= 8*K */) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; k++)
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < K; k++) scratch[wid * K + k] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        double t = 0.0;
+        for (int w = 0; w < nw; w++) t += scratch[w * K + k];
+        v[k] = t;
+    }
+    __syncthreads();
+}
+
 // K = C + eta I from D at 1/theta into L; Cholesky in place (lower, row-major).
 // Returns false when a pivot is not positive.
 __device__ bool mle_chol(const double *D, double *L, int n, double rth, double eta, double *scratch) {
@@ -52,9 +74,9 @@ __device__ bool mle_chol(const double *D, double *L, int n, double rth, double e
             if (tid == 0) bad = 1;
             break;  // uniform: every thread read the same pivot
         }
-        const double rl = 1.0 / sqrt(dkk);
+        const double rl = rsqrt_nr(dkk);  // 1/sqrt(L_kk), seed + Newton (dkk > 0 here)
         if (k > 0) {  // scale column k-1 (its pivot is settled)
-            const double rp = 1.0 / sqrt(L[(k - 1) * n + (k - 1)]);
+            const double rp = rsqrt_nr(L[(k - 1) * n + (k - 1)]);
             for (int i = k + tid; i < n; i += blockDim.x) L[i * n + (k - 1)] *= rp;
         }
         // trailing update: rows to warps, columns to lanes (no index division)
@@ -175,12 +197,16 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, const double *D, doub
         aPa = fma(al[a] * Pab, al[b], aPa);
         vAv = fma(v[a] * A[e], v[b], vAv);
     }
-    tAP = block_sum(tAP, scratch);
-    tAQ = block_sum(tAQ, scratch);
-    tTT = block_sum(tTT, scratch);
-    aQa = block_sum(aQa, scratch);
-    aPa = block_sum(aPa, scratch);
-    vAv = block_sum(vAv, scratch);
+    {
+        double t6[6] = {tAP, tAQ, tTT, aQa, aPa, vAv};
+        block_sum_n<6>(t6, scratch);
+        tAP = t6[0];
+        tAQ = t6[1];
+        tTT = t6[2];
+        aQa = t6[3];
+        aPa = t6[4];
+        vAv = t6[5];
+    }
     const double q = aPa / psi;
     r.g = -0.5 * tAP + hn * q;
     r.h = -0.5 * tAQ + 0.5 * tTT - hn * (2.0 * vAv - aQa) / psi + hn * q * q;
@@ -197,7 +223,7 @@ mle_kernel(MleArgs A) {
     double *vecs = A.use_smem ? sm + 4 * n * n : A.ws + (size_t)gridDim.x * 4 * n * n + (size_t)blockIdx.x * (4 * n + n * p + 64);
     double *D = mats, *L = D + n * n, *W = L + n * n, *Am = W + n * n;
     double *Y = vecs, *al = Y + n, *v = al + n, *hv = v + n, *Xn = hv + n;
-    __shared__ double scratch[40];
+    __shared__ double scratch[64];
     __shared__ int jn_s;
     const double lo = log(A.lo), hi = log(A.hi);
 
@@ -275,9 +301,9 @@ mle_kernel(MleArgs A) {
             ph = fma(sa, sa, ph);
             pp = fma(sb, sb, pp);
         }
-        const double mu = block_sum(pm, scratch);
-        const double hAh = block_sum(ph, scratch);
-        const double psi_p = block_sum(pp, scratch);
+        double s3[3] = {pm, ph, pp};
+        block_sum_n<3>(s3, scratch);
+        const double mu = s3[0], hAh = s3[1], psi_p = s3[2];
         if (tid == 0) {
             const double sc = psi_p * (1.0 + A.eta - hAh) / (double)m;
             const double vr = m > 2 ? sc * (double)m / (double)(m - 2) : __longlong_as_double(0x7ff8000000000000LL);
