@@ -106,6 +106,15 @@ __device__ __forceinline__ double fast_div_pos(double a, double b) {
 #ifdef LAGP_V2_PROF
 // clock probes of thread 0 on its first location (profiling builds only)
 __device__ long long g_v2_prof[160][8];
+__device__ long long g_v2_arrive[160][32];  // per warp: clock when its lane 0 reaches the step barrier
+#define V2_ARRIVE()                                                                             \
+    do {                                                                                        \
+        if (lane == 0 && xi == blockIdx.x && blockIdx.x == 0 && j < 160) {                      \
+            long long t_;                                                                       \
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_)::"memory");                        \
+            g_v2_arrive[j][wid] = t_;                                                           \
+        }                                                                                       \
+    } while (0)
 __device__ volatile double g_v2_sink;
 #define V2_PROBE(k, v)                                                              \
     do {                                                                            \
@@ -119,6 +128,9 @@ __device__ volatile double g_v2_sink;
 #else
 #define V2_PROBE(k, v) \
     do {               \
+    } while (0)
+#define V2_ARRIVE() \
+    do {            \
     } while (0)
 #endif
 
@@ -307,6 +319,7 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
                         }
                     }
                 }
+                V2_ARRIVE();
                 __syncthreads();
                 // every warp: argmax over the warp posts
                 unsigned long long pk = 0;
@@ -613,6 +626,8 @@ cudaError_t launch_alc_incremental_v2(const AlcArgs &a, const IncPlan &pl, int g
 
 #ifdef LAGP_V2_PROF
 extern "C" int lagp_v2_prof(long long *out) {
-    return (int)cudaMemcpyFromSymbol(out, lagp::g_v2_prof, sizeof(lagp::g_v2_prof));
+    int e = (int)cudaMemcpyFromSymbol(out, lagp::g_v2_prof, sizeof(lagp::g_v2_prof));
+    if (e) return e;
+    return (int)cudaMemcpyFromSymbol(out + 160 * 8, lagp::g_v2_arrive, sizeof(lagp::g_v2_arrive));
 }
 #endif

@@ -27,9 +27,11 @@ X, Z, XX = (torch.from_numpy(cfg[k]).to(dev) for k in ("X", "Z", "XX"))
 r = lagp.alc_batch(X, Z, XX, cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"], form="incremental", timing=True)
 torch.cuda.synchronize()
 print(r["timing"])
-buf = (ctypes.c_longlong * (160 * 8))()
+buf = (ctypes.c_longlong * (160 * 8 + 160 * 32))()
 lagp._LIB.lagp_v2_prof(buf)
-t = np.frombuffer(buf, dtype=np.int64).reshape(160, 8)
+allv = np.frombuffer(buf, dtype=np.int64)
+t = allv[:160 * 8].reshape(160, 8)
+arr = allv[160 * 8:].reshape(160, 32)
 n = cfg["n"]
 names = ["start", "keys", "warpredux", "xwarp", "record", "kx", "dot", "downdate"]
 print("step " + " ".join(f"{x:>9s}" for x in names[1:]) + "      total")
@@ -45,3 +47,10 @@ for j in range(n):
         d.append(f"{row[k] - prev:9d}")
         prev = row[k]
     print(f"{j:4d} " + " ".join(d) + f" {nxt - row[0]:10d}")
+print("barrier arrivals per step (cycles after the first warp; the last warp's id)")
+for j in range(cfg["n0"], n, 4):
+    a = arr[j][:16]
+    if a.min() <= 0:
+        continue
+    rel = a - a.min()
+    print(f"{j:4d} spread {rel.max():6d}  last warp {int(rel.argmax()):2d}  " + " ".join(f"{v:5d}" for v in rel))
