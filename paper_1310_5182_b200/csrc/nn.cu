@@ -201,14 +201,55 @@ __device__ void nn_exact_select(NNSmem &s, const double *__restrict__ X, int64_t
 }
 
 // FP32 copy of X for the prefilter and B = max_i ||X_i||^2 (as ordered uint64 bits).
+// order-preserving map of doubles onto uint64 (min/max by integer atomics; deterministic)
+__device__ __forceinline__ unsigned long long d_ordkey(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double d_from_ordkey(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+// per-dimension min / max of X (the prefilter's centre c = (min + max) / 2)
+__global__ void nn_bounds_kernel(const double *__restrict__ X, int64_t N, int p, unsigned long long *__restrict__ kmin,
+                                 unsigned long long *__restrict__ kmax) {
+    for (int k = 0; k < p; k++) {
+        unsigned long long lo = ~0ull, hi = 0ull;
+        for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
+            const unsigned long long o = d_ordkey(X[r * p + k]);
+            lo = o < lo ? o : lo;
+            hi = o > hi ? o : hi;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, off), b = __shfl_xor_sync(0xffffffffu, hi, off);
+            lo = a < lo ? a : lo;
+            hi = b > hi ? b : hi;
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(kmin + k, lo);
+            atomicMax(kmax + k, hi);
+        }
+    }
+}
+
+__device__ __forceinline__ double nn_centre(const unsigned long long *kmin, const unsigned long long *kmax, int k) {
+    return 0.5 * (d_from_ordkey(kmin[k]) + d_from_ordkey(kmax[k]));
+}
+
+// The prefilter works on x~ = x - c (distances are translation invariant): the
+// rounding margins scale with ||x~||^2 + ||q~||^2, smallest around the centre.
 __global__ void nn_prep_kernel(const double *__restrict__ X, int64_t N, int p, float *__restrict__ X32,
-                               float *__restrict__ rn2f, unsigned long long *__restrict__ maxn2) {
+                               float *__restrict__ rn2f, unsigned long long *__restrict__ maxn2,
+                               const unsigned long long *__restrict__ kmin, const unsigned long long *__restrict__ kmax) {
     double mx = 0.0;
+    double c[LAGP_PMAX];
+    for (int k = 0; k < p; k++) c[k] = nn_centre(kmin, kmax, k);
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
         double n2 = 0.0;
         float f2 = 0.f;
         for (int k = 0; k < p; k++) {
-            const double v = X[r * p + k];
+            const double v = X[r * p + k] - c[k];
             const float vf = (float)v;
             X32[r * p + k] = vf;
             f2 = fmaf(vf, vf, f2);
@@ -481,8 +522,8 @@ __device__ __forceinline__ float row_dotf(const float *xf, const float *qf, int 
 template <int P>
 __global__ void __launch_bounds__(NN_THREADS)
 nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, const float *__restrict__ rn2f,
-               const unsigned long long *maxn2_bits,
-               int64_t N, int p, const double *__restrict__ XX, int64_t M, int Nprime, int n0, int bufcap,
+               const unsigned long long *maxn2_bits, const unsigned long long *__restrict__ kmin,
+               const unsigned long long *__restrict__ kmax, int64_t N, int p, const double *__restrict__ XX, int64_t M, int Nprime, int n0, int bufcap,
                int sorted, int32_t *__restrict__ pool_out, double *__restrict__ d2_out, int32_t *__restrict__ bufc_ws,
                uint64_t *__restrict__ bufk_ws, int32_t *__restrict__ bufi_ws, int *__restrict__ fallback_count) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -514,14 +555,18 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
         for (int e = tid; e < NN_Q * LAGP_PMAX; e += blockDim.x) {
             int q = e / LAGP_PMAX, k = e % LAGP_PMAX;
             const double v = (q < nq && k < p) ? XX[(q0 + q) * p + k] : 0.0;
-            s.qx[q][k] = v;
-            s.nqf[q][k] = -(float)v;
-            s.qf[q][k] = (float)v;
+            const double vc = (q < nq && k < p) ? v - nn_centre(kmin, kmax, k) : 0.0;  // centred (prefilter)
+            s.qx[q][k] = v;  // raw (exact keys)
+            s.nqf[q][k] = -(float)vc;
+            s.qf[q][k] = (float)vc;
         }
         __syncthreads();
         if (tid < NN_Q) {
             double n2 = 0.0;
-            for (int k = 0; k < p; k++) n2 = fma(s.qx[tid][k], s.qx[tid][k], n2);
+            for (int k = 0; k < p; k++) {
+                const double vc = s.qx[tid][k] - nn_centre(kmin, kmax, k);
+                n2 = fma(vc, vc, n2);
+            }
             s.qn2[tid] = n2;
             float f2 = 0.f;
             for (int k = 0; k < p; k++) f2 = fmaf(s.qf[tid][k], s.qf[tid][k], f2);
@@ -792,17 +837,17 @@ static int nn_bufcap(int Nprime, bool sorted) {
     return c;
 }
 
-// Workspace layout: [maxn2 bits (256 B)] [X32: N*p floats] [rn2f: N floats]
+// Workspace layout: [maxn2 bits, per-dimension min / max keys (512 B)] [X32: N*p floats] [rn2f: N floats]
 // [compacted rows] [survivor keys] [filter rows], the last three bufcap per query
 size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime, bool sorted) {
     const size_t bc = (size_t)nn_bufcap(Nprime, sorted);
-    return 256 + (((size_t)N * p * sizeof(float) + 255) & ~(size_t)255) + (((size_t)N * sizeof(float) + 255) & ~(size_t)255) +
+    return 512 + (((size_t)N * p * sizeof(float) + 255) & ~(size_t)255) + (((size_t)N * sizeof(float) + 255) & ~(size_t)255) +
            (size_t)grid * NN_Q * bc * (sizeof(uint64_t) + 2 * sizeof(int32_t)) + 256;
 }
 
 template <int P>
 static cudaError_t launch_nn_t(const double *X, const float *X32, const float *rn2f, const unsigned long long *mx,
-                               int64_t N, int p,
+                               const unsigned long long *kmin, const unsigned long long *kmax, int64_t N, int p,
                                const double *XX, int64_t M, int Nprime, int n0, int sorted, int32_t *pool, double *d2,
                                char *w, int grid, int *fb, cudaStream_t st) {
     size_t smem = sizeof(NNSmem);
@@ -814,8 +859,8 @@ static cudaError_t launch_nn_t(const double *X, const float *X32, const float *r
     uint64_t *bk = (uint64_t *)w;
     w += (size_t)grid * NN_Q * bc * sizeof(uint64_t);
     int32_t *bi = (int32_t *)w;
-    nn_pool_kernel<P><<<grid, NN_THREADS, smem, st>>>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, bc, sorted, pool, d2, bcmp,
-                                                      bk, bi, fb);
+    nn_pool_kernel<P><<<grid, NN_THREADS, smem, st>>>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, bc, sorted,
+                                                      pool, d2, bcmp, bk, bi, fb);
     return cudaGetLastError();
 }
 
@@ -836,27 +881,35 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
                       int *launches) {
     char *w = (char *)ws;
     unsigned long long *mx = (unsigned long long *)w;
-    float *X32 = (float *)(w + 256);
-    float *rn2f = (float *)(w + 256 + (((size_t)N * p * sizeof(float) + 255) & ~(size_t)255));
+    unsigned long long *kmin = mx + 1, *kmax = mx + 1 + LAGP_PMAX;  // 8 + 2*16*8 = 264 <= 512 B
+    float *X32 = (float *)(w + 512);
+    float *rn2f = (float *)(w + 512 + (((size_t)N * p * sizeof(float) + 255) & ~(size_t)255));
     char *rest = (char *)rn2f + (((size_t)N * sizeof(float) + 255) & ~(size_t)255);
     if (!prepared) {
-        cudaError_t e = cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st);
+        cudaError_t e = cudaMemsetAsync(mx, 0, sizeof(unsigned long long) * (1 + LAGP_PMAX), st);  // maxn2, kmin
+        if (e != cudaSuccess) return e;
+        e = cudaMemsetAsync(kmin, 0xff, sizeof(unsigned long long) * LAGP_PMAX, st);
+        if (e != cudaSuccess) return e;
+        e = cudaMemsetAsync(kmax, 0, sizeof(unsigned long long) * LAGP_PMAX, st);
         if (e != cudaSuccess) return e;
         int blocks = (int)((N + 255) / 256);
         if (blocks > 4096) blocks = 4096;
-        nn_prep_kernel<<<blocks, 256, 0, st>>>(X, N, p, X32, rn2f, mx);
+        nn_bounds_kernel<<<blocks < 592 ? blocks : 592, 256, 0, st>>>(X, N, p, kmin, kmax);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        if (launches) (*launches)++;
+        nn_prep_kernel<<<blocks, 256, 0, st>>>(X, N, p, X32, rn2f, mx, kmin, kmax);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        if (launches) (*launches) += 2;
     }
     if (launches) (*launches)++;
     switch (p) {
-        case 1: return launch_nn_t<1>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        case 2: return launch_nn_t<2>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        case 3: return launch_nn_t<3>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        case 4: return launch_nn_t<4>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        case 8: return launch_nn_t<8>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        default: return launch_nn_t<0>(X, X32, rn2f, mx, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 1: return launch_nn_t<1>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 2: return launch_nn_t<2>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 3: return launch_nn_t<3>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 4: return launch_nn_t<4>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 8: return launch_nn_t<8>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        default: return launch_nn_t<0>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
     }
 }
 
