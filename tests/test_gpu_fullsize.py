@@ -1,0 +1,65 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py
+and scripts/run_config.py time: the whole workload on the device (every chunk,
+the persistent grids at their full width), then a seeded sample of locations
+spread over the whole range recomputed one by one by the CPU oracle and compared
+with the rules of tests/parity.py (bit-exact index sequences up to explained near
+ties; mean/s2/var within 1e-8). Whole-output properties (flags, finite values,
+index ranges, distinct rows per design) are checked on every location.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from lagp_data import make_config
+from parity import compare, tau_for
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_dev():
+    import torch
+
+    return torch, torch.device("cuda", 0)
+
+
+@pytest.fixture(scope="module")
+def lagp():
+    import paper_1310_5182_b200 as m
+
+    m.lib()
+    return m
+
+
+def T(torch, dev, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+@pytest.mark.parametrize("name,form,sample", [
+    ("C2", "incremental", 48),   # bench workload: 8-d borehole, N = 1e5, M = 1e4
+    ("C2", "explicit", 24),      # the paper's formulation at the same size
+    ("C3", "incremental", 32),   # LGBB-like grid, M = 5e5 (eight 65,536-location chunks)
+    ("C4", "incremental", 16),   # N = M = 1e6 on one GPU
+])
+def test_fullsize_sampled_parity(torch_dev, lagp, name, form, sample):
+    torch, dev = torch_dev
+    cfg = make_config(name)
+    X, Z, XX = cfg["X"], cfg["Z"], cfg["XX"]
+    M, n = XX.shape[0], cfg["n"]
+    r = lagp.alc_batch(T(torch, dev, X), T(torch, dev, Z), T(torch, dev, XX), cfg["d"], cfg["g"], cfg["n0"], n,
+                       cfg["Nprime"], form=form, gaps=True)
+    idx = r["idx"].cpu().numpy()
+    # whole-output properties
+    assert int(r["status"]) == 0
+    assert np.isfinite(r["mean"].cpu().numpy()).all() and (r["s2"].cpu().numpy() > 0).all()
+    assert idx.min() >= 0 and idx.max() < X.shape[0]
+    srt = np.sort(idx, axis=1)
+    assert (srt[:, 1:] != srt[:, :-1]).all(), "a local design repeats a row"
+    fl = r["flags"].cpu().numpy().astype(np.uint32)
+    assert not (fl & (4 | 8)).any(), "EXHAUSTED / NONFINITE at a full-size workload"
+    # sampled oracle parity (rows spread over every chunk)
+    sel = np.sort(np.random.default_rng(11).choice(M, sample, replace=False))
+    g = {k: v.cpu().numpy()[sel] for k, v in r.items() if hasattr(v, "cpu")}
+    o = oracle.alc_batch(X, Z, XX[sel], cfg["d"], cfg["g"], cfg["n0"], n, cfg["Nprime"])
+    rep = compare(g, o, cfg["n0"], float(np.std(Z)), tau_for(X.shape[1]), max_explained=0.05)
+    print(name, form, rep)
