@@ -9,7 +9,7 @@
 //   U  = K_j^{-1} Kc                                 (DMMA: mma.sync m8n8k4 f64)
 //   q_c = sum_a Kc[a][c] U[a][c],  s_c = 1 + eta - q_c  (= m_j^{-1}(x_c), Eq 6)
 //   cov_c = kappa_c - w^T k_c,     Delta_c = cov_c^2 / s_c (Eq 5, reading R1)
-// With T = 32 candidates per CTA the j × j by j × T product is a genuinely dense
+// With T = 32-64 candidates per CTA the j × j by j × T product is a genuinely dense
 // GEMM (j up to 768), unlike the greedy loop's per-location matvecs: this is the
 // one place of the path where the FP64 tensor instruction is the right tool.
 // Per-CTA (Delta, row) top-2 go to a workspace; a second kernel merges them per
@@ -17,7 +17,7 @@
 //
 // Fragment layouts (PTX ISA, mma.m8n8k4 .f64): A a0 = A[g][k], B b0 = B[k][g],
 // C {c0,c1} = C[g][2k], C[g][2k+1] with g = lane>>2, k = lane&3. The tile row
-// stride SG_TL = 36 ≡ 4 (mod 16) doubles makes every B fragment load conflict-free
+// stride T + 4 ≡ 4 (mod 16) doubles makes every B fragment load conflict-free
 // (64-bit loads are served per half-warp).
 #include <cuda_runtime.h>
 
@@ -27,8 +27,11 @@
 namespace lagp {
 
 constexpr int SG_THREADS = 256;  // 8 warps
-constexpr int SG_T = 32;         // candidates per CTA (4 column blocks of 8)
-constexpr int SG_TL = 36;        // tile row stride (doubles)
+// candidates per CTA: T = 32 or 64 (4 or 8 column blocks of 8); tile row stride
+// TL = T + 4 (≡ 4 mod 16 doubles: conflict-free B fragments). Every A fragment of
+// K^{-1} (streamed from L2) feeds T/8 DMMAs, so T = 64 halves the K^{-1} traffic
+// per flop, but measured slower (occupancy): T = 32 is used.
+__host__ __device__ constexpr int sg_tl(int T) { return T + 4; }
 
 __device__ __forceinline__ void sg_dmma(double &c0, double &c1, double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -60,6 +63,7 @@ alc_scores_prep_kernel(int j, int p, const double *__restrict__ Xj, const double
 }
 
 // scores: grid (ceil(nc / T), B)
+template <int SG_T>
 __global__ void __launch_bounds__(SG_THREADS)
 alc_scores_gemm_kernel(int j, int p, int nc, const double *__restrict__ Xj, const double *__restrict__ Kinv,
                        const double *__restrict__ cands, const int32_t *__restrict__ cand_idx,
@@ -69,6 +73,8 @@ alc_scores_gemm_kernel(int j, int p, int nc, const double *__restrict__ Xj, cons
     const int b = blockIdx.y, c0 = blockIdx.x * SG_T;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int g = lane >> 2, kq = lane & 3;
+    constexpr int SG_TL = sg_tl(SG_T);
+    constexpr int CB = SG_T / 8;                 // column blocks
     const int jr = (j + 7) & ~7;                 // rows padded to the 8-row blocks
     double *Kc = sm;                             // jr × SG_TL
     double *xcs = Kc + (size_t)jr * SG_TL;       // T × p candidate coordinates
@@ -90,11 +96,11 @@ alc_scores_gemm_kernel(int j, int p, int nc, const double *__restrict__ Xj, cons
         Kc[a * SG_TL + c] = v;
     }
     __syncthreads();
-    // cov part: w^T k_c (warp w: columns 4w..4w+3)
+    // cov part: w^T k_c (warp w: columns CB*w .. CB*w + CB - 1)
     {
         const double *wb = wvec + (size_t)b * wl;
-        for (int cc = 0; cc < 4; cc++) {
-            const int c = 4 * wid + cc;
+        for (int cc = 0; cc < CB; cc++) {
+            const int c = CB * wid + cc;
             double acc = 0.0;
             for (int a = lane; a < j; a += 32) acc = fma(wb[a], Kc[a * SG_TL + c], acc);
 #pragma unroll
@@ -104,17 +110,17 @@ alc_scores_gemm_kernel(int j, int p, int nc, const double *__restrict__ Xj, cons
     }
     // U = K^{-1} Kc by 8-row blocks (warp w: row blocks w, w+8, ...), q partials
     const double *K = Kinv + (size_t)b * j * j;
-    double qp[4][2];
+    double qp[CB][2];
 #pragma unroll
-    for (int cb = 0; cb < 4; cb++) qp[cb][0] = qp[cb][1] = 0.0;
+    for (int cb = 0; cb < CB; cb++) qp[cb][0] = qp[cb][1] = 0.0;
     const int nrb = jr >> 3;
     for (int rb = wid; rb < nrb; rb += 8) {
         const int row = 8 * rb + g;
         const bool rok = row < j;
         const double *Krow = K + (size_t)(rok ? row : 0) * j;
-        double acc[4][2];
+        double acc[CB][2];
 #pragma unroll
-        for (int cb = 0; cb < 4; cb++) acc[cb][0] = acc[cb][1] = 0.0;
+        for (int cb = 0; cb < CB; cb++) acc[cb][0] = acc[cb][1] = 0.0;
         int t = 0;
         // main loop: k-steps of 4 with 8 A-fragments in flight
         for (; t + 32 <= j; t += 32) {
@@ -125,7 +131,7 @@ alc_scores_gemm_kernel(int j, int p, int nc, const double *__restrict__ Xj, cons
             for (int u = 0; u < 8; u++) {
                 const double *Brow = Kc + (t + 4 * u + kq) * SG_TL + g;
 #pragma unroll
-                for (int cb = 0; cb < 4; cb++) sg_dmma(acc[cb][0], acc[cb][1], av[u], Brow[8 * cb]);
+                for (int cb = 0; cb < CB; cb++) sg_dmma(acc[cb][0], acc[cb][1], av[u], Brow[8 * cb]);
             }
         }
         for (; t < j; t += 4) {
@@ -133,19 +139,19 @@ alc_scores_gemm_kernel(int j, int p, int nc, const double *__restrict__ Xj, cons
             const double a = (rok && col < j) ? __ldg(Krow + col) : 0.0;
             const double *Brow = Kc + (size_t)col * SG_TL + g;  // rows >= j are 0 in the tile
 #pragma unroll
-            for (int cb = 0; cb < 4; cb++) sg_dmma(acc[cb][0], acc[cb][1], a, col < jr ? Brow[8 * cb] : 0.0);
+            for (int cb = 0; cb < CB; cb++) sg_dmma(acc[cb][0], acc[cb][1], a, col < jr ? Brow[8 * cb] : 0.0);
         }
         // q partial: sum over this row block of Kc[a][c] U[a][c]
         const double *Krw = Kc + (size_t)row * SG_TL;
 #pragma unroll
-        for (int cb = 0; cb < 4; cb++) {
+        for (int cb = 0; cb < CB; cb++) {
             qp[cb][0] = fma(Krw[8 * cb + 2 * kq], acc[cb][0], qp[cb][0]);
             qp[cb][1] = fma(Krw[8 * cb + 2 * kq + 1], acc[cb][1], qp[cb][1]);
         }
     }
     // reduce over g (lane bits 2..4), then across warps
 #pragma unroll
-    for (int cb = 0; cb < 4; cb++)
+    for (int cb = 0; cb < CB; cb++)
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             double v = qp[cb][h];
@@ -155,28 +161,31 @@ alc_scores_gemm_kernel(int j, int p, int nc, const double *__restrict__ Xj, cons
             if (g == 0) qred[wid * SG_T + 8 * cb + 2 * kq + h] = v;
         }
     __syncthreads();
-    // scores and the CTA's top-2 (warp 0)
+    // scores and the CTA's top-2 (warp 0; lane takes columns lane, lane + 32)
     if (wid == 0) {
-        const int c = lane;  // SG_T == 32
-        double q = 0.0;
-#pragma unroll
-        for (int w = 0; w < 8; w++) q += qred[w * SG_T + c];
-        double dl = -INFINITY;
-        int gi = 0x7fffffff;
-        const bool valid = c0 + c < nc;
-        if (valid) {
-            const double s = 1.0 + eta - q;
-            gi = cand_idx[(size_t)b * nc + c0 + c];
-            if (s > kSMin) {
-                const double kap = corr_from_d2(sqdist_fma(xcs + c * p, xq, p), rtheta);
-                const double cov = kap - cvred[c];
-                dl = cov * cov / s;
-            }
-            if (delta_out) delta_out[(size_t)b * nc + c0 + c] = dl;
-        }
         Top2 t2;
         t2.init();
-        if (valid && dl > -INFINITY) t2.push(dl, gi, c0 + c);
+#pragma unroll
+        for (int h = 0; h < SG_T / 32; h++) {
+            const int c = lane + 32 * h;
+            double q = 0.0;
+#pragma unroll
+            for (int w = 0; w < 8; w++) q += qred[w * SG_T + c];
+            double dl = -INFINITY;
+            int gi = 0x7fffffff;
+            const bool valid = c0 + c < nc;
+            if (valid) {
+                const double s = 1.0 + eta - q;
+                gi = cand_idx[(size_t)b * nc + c0 + c];
+                if (s > kSMin) {
+                    const double kap = corr_from_d2(sqdist_fma(xcs + c * p, xq, p), rtheta);
+                    const double cov = kap - cvred[c];
+                    dl = cov * cov / s;
+                }
+                if (delta_out) delta_out[(size_t)b * nc + c0 + c] = dl;
+            }
+            if (valid && dl > -INFINITY) t2.push(dl, gi, c0 + c);
+        }
         warp_merge_top2(t2);
         if (lane == 0) {
             double *pp = part + ((size_t)b * gridDim.x + blockIdx.x) * 4;
@@ -207,16 +216,39 @@ alc_scores_merge_kernel(int nblk, const double *__restrict__ part, int32_t *__re
     }
 }
 
+static int sg_tile(int j) {
+    (void)j;
+    return 32;  // measured: T = 64 (fewer CTAs per SM, 95 registers) is 1.3-1.6x slower at n = 208-336
+}
+
+static size_t sg_smem(int j, int T) {
+    const int jr = (j + 7) & ~7;
+    return ((size_t)jr * sg_tl(T) + (size_t)T * LAGP_PMAX + 8 * (size_t)T + T) * sizeof(double);
+}
+
 size_t alc_scores_gemm_smem(int j, int p) {
     (void)p;
-    const int jr = (j + 7) & ~7;
-    return ((size_t)jr * SG_TL + SG_T * LAGP_PMAX + 8 * SG_T + SG_T) * sizeof(double);
+    return sg_smem(j, sg_tile(j));
 }
 
 size_t alc_scores_gemm_ws_bytes(int B, int j, int nc) {
     const int wl = (j + 3) & ~3;
-    const int nblk = (nc + SG_T - 1) / SG_T;
+    const int T = sg_tile(j);
+    const int nblk = (nc + T - 1) / T;
     return ((size_t)B * wl + (size_t)B * nblk * 4) * sizeof(double);
+}
+
+template <int T>
+static cudaError_t sg_launch(int B, int j, int p, int nc, const double *Xj, const double *Kinv, const double *cands,
+                             const int32_t *cand_idx, const double *x, double rtheta, double eta, const double *wv,
+                             int wl, double *delta, double *part, cudaStream_t st) {
+    const size_t smem = sg_smem(j, T);
+    cudaError_t e = cudaFuncSetAttribute(alc_scores_gemm_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int nblk = (nc + T - 1) / T;
+    alc_scores_gemm_kernel<T><<<dim3(nblk, B), SG_THREADS, smem, st>>>(j, p, nc, Xj, Kinv, cands, cand_idx, x, rtheta,
+                                                                       eta, wv, wl, delta, part);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_alc_scores_gemm(int B, int j, int p, int nc, const double *Xj, const double *Kinv,
@@ -224,19 +256,16 @@ cudaError_t launch_alc_scores_gemm(int B, int j, int p, int nc, const double *Xj
                                    double eta, double *delta, int32_t *best, double *gap, void *ws, cudaStream_t st,
                                    int *launches) {
     const int wl = (j + 3) & ~3;
-    const int nblk = (nc + SG_T - 1) / SG_T;
+    const int T = sg_tile(j);
+    const int nblk = (nc + T - 1) / T;
     double *wv = static_cast<double *>(ws);
     double *part = wv + (size_t)B * wl;
     const size_t sp = (size_t)j * sizeof(double);
     alc_scores_prep_kernel<<<B, SG_THREADS, sp, st>>>(j, p, Xj, Kinv, x, rtheta, wv, wl);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const size_t smem = alc_scores_gemm_smem(j, p);
-    e = cudaFuncSetAttribute(alc_scores_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    alc_scores_gemm_kernel<<<dim3(nblk, B), SG_THREADS, smem, st>>>(j, p, nc, Xj, Kinv, cands, cand_idx, x, rtheta,
-                                                                    eta, wv, wl, delta, part);
-    e = cudaGetLastError();
+    e = (T == 64) ? sg_launch<64>(B, j, p, nc, Xj, Kinv, cands, cand_idx, x, rtheta, eta, wv, wl, delta, part, st)
+                  : sg_launch<32>(B, j, p, nc, Xj, Kinv, cands, cand_idx, x, rtheta, eta, wv, wl, delta, part, st);
     if (e != cudaSuccess) return e;
     alc_scores_merge_kernel<<<B, SG_THREADS, 0, st>>>(nblk, part, best, gap);
     if (launches) *launches += 3;
