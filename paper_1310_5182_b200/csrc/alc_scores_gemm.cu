@@ -33,6 +33,15 @@ constexpr int SG_THREADS = 256;  // 8 warps
 // per flop, but measured slower (occupancy): T = 32 is used.
 __host__ __device__ constexpr int sg_tl(int T) { return T + 4; }
 
+__device__ __forceinline__ void sg_cp16(void *smem, const void *gmem) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(a), "l"(gmem));
+}
+__device__ __forceinline__ void sg_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void sg_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+constexpr int SG_AL = 36;              // staged K^{-1} chunk row stride (≡ 4 mod 16: conflict-free A fragments)
+constexpr int SG_ABUF = 2 * 8 * SG_AL;  // per warp: two 8 × 32 chunks
+
 __device__ __forceinline__ void sg_dmma(double &c0, double &c1, double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
         : "+d"(c0), "+d"(c1)
@@ -63,7 +72,7 @@ alc_scores_prep_kernel(int j, int p, const double *__restrict__ Xj, const double
 }
 
 // scores: grid (ceil(nc / T), B)
-template <int SG_T>
+template <int SG_T, bool STAGE>
 __global__ void __launch_bounds__(SG_THREADS)
 alc_scores_gemm_kernel(int j, int p, int nc, const double *__restrict__ Xj, const double *__restrict__ Kinv,
                        const double *__restrict__ cands, const int32_t *__restrict__ cand_idx,
@@ -80,6 +89,7 @@ alc_scores_gemm_kernel(int j, int p, int nc, const double *__restrict__ Xj, cons
     double *xcs = Kc + (size_t)jr * SG_TL;       // T × p candidate coordinates
     double *qred = xcs + SG_T * LAGP_PMAX;       // 8 warps × T partial q
     double *cvred = qred + 8 * SG_T;             // T: w^T k_c
+    double *Abuf = cvred + SG_T + wid * SG_ABUF; // this warp's staged K^{-1} chunks
     __shared__ double xq[LAGP_PMAX];
     const double *Xb = Xj + (size_t)b * j * p;
     if (tid < p) xq[tid] = xref[(size_t)b * p + tid];
@@ -122,8 +132,41 @@ alc_scores_gemm_kernel(int j, int p, int nc, const double *__restrict__ Xj, cons
 #pragma unroll
         for (int cb = 0; cb < CB; cb++) acc[cb][0] = acc[cb][1] = 0.0;
         int t = 0;
-        // main loop: k-steps of 4 with 8 A-fragments in flight
-        for (; t + 32 <= j; t += 32) {
+        // main loop: 8 × 32 chunks of the warp's K^{-1} row block staged into shared
+        // memory by cp.async (double-buffered: chunk c+1 in flight while chunk c feeds
+        // 8 k-steps × T/8 DMMAs); j even keeps every 16-byte copy aligned
+        const int nfull = (STAGE && j % 2 == 0) ? j / 32 : 0;
+        if (nfull > 0) {
+            auto issue = [&](int ch) {
+                double *dst = Abuf + (ch & 1) * (8 * SG_AL);
+                for (int sg = lane; sg < 128; sg += 32) {
+                    const int r = sg >> 4, cs = (sg & 15) * 2;
+                    const int rr = (8 * rb + r < j) ? 8 * rb + r : 0;  // rows >= j: masked at use
+                    sg_cp16(dst + r * SG_AL + cs, K + (size_t)rr * j + ch * 32 + cs);
+                }
+                sg_commit();
+            };
+            issue(0);
+            for (int ch = 0; ch < nfull; ch++) {
+                if (ch + 1 < nfull)
+                    issue(ch + 1);
+                else
+                    sg_commit();  // empty group: the wait below always means "chunk ch landed"
+                sg_wait1();
+                __syncwarp();
+                const double *Ab = Abuf + (ch & 1) * (8 * SG_AL) + g * SG_AL;
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const double a = rok ? Ab[4 * u + kq] : 0.0;
+                    const double *Brow = Kc + (ch * 32 + 4 * u + kq) * SG_TL + g;
+#pragma unroll
+                    for (int cb = 0; cb < CB; cb++) sg_dmma(acc[cb][0], acc[cb][1], a, Brow[8 * cb]);
+                }
+                __syncwarp();
+            }
+            t = nfull * 32;
+        }
+        for (; t + 32 <= j; t += 32) {  // odd j: A fragments straight from L2
             double av[8];
 #pragma unroll
             for (int u = 0; u < 8; u++) av[u] = rok ? __ldg(Krow + t + 4 * u + kq) : 0.0;
@@ -221,14 +264,19 @@ static int sg_tile(int j) {
     return 32;  // measured: T = 64 (fewer CTAs per SM, 95 registers) is 1.3-1.6x slower at n = 208-336
 }
 
-static size_t sg_smem(int j, int T) {
+static size_t sg_smem(int j, int T, bool stage) {
     const int jr = (j + 7) & ~7;
-    return ((size_t)jr * sg_tl(T) + (size_t)T * LAGP_PMAX + 8 * (size_t)T + T) * sizeof(double);
+    return ((size_t)jr * sg_tl(T) + (size_t)T * LAGP_PMAX + 8 * (size_t)T + T + (stage ? 8 * (size_t)SG_ABUF : 0)) *
+           sizeof(double);
 }
+// K^{-1} staging for j >= 384 (one CTA per SM either way: the copies hide the L2
+// latency) while the tile plus the chunk buffers fit (j <= 640 at T = 32); below 384
+// the 37 KB of buffers would cost resident CTAs (measured 8-15 % slower at 208-336)
+static bool sg_stage(int j) { return j >= 384 && sg_smem(j, 32, true) <= 227 * 1024; }
 
 size_t alc_scores_gemm_smem(int j, int p) {
     (void)p;
-    return sg_smem(j, sg_tile(j));
+    return sg_smem(j, sg_tile(j), sg_stage(j));
 }
 
 size_t alc_scores_gemm_ws_bytes(int B, int j, int nc) {
@@ -238,15 +286,16 @@ size_t alc_scores_gemm_ws_bytes(int B, int j, int nc) {
     return ((size_t)B * wl + (size_t)B * nblk * 4) * sizeof(double);
 }
 
-template <int T>
+template <int T, bool STAGE>
 static cudaError_t sg_launch(int B, int j, int p, int nc, const double *Xj, const double *Kinv, const double *cands,
                              const int32_t *cand_idx, const double *x, double rtheta, double eta, const double *wv,
                              int wl, double *delta, double *part, cudaStream_t st) {
-    const size_t smem = sg_smem(j, T);
-    cudaError_t e = cudaFuncSetAttribute(alc_scores_gemm_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = sg_smem(j, T, STAGE);
+    cudaError_t e =
+        cudaFuncSetAttribute(alc_scores_gemm_kernel<T, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int nblk = (nc + T - 1) / T;
-    alc_scores_gemm_kernel<T><<<dim3(nblk, B), SG_THREADS, smem, st>>>(j, p, nc, Xj, Kinv, cands, cand_idx, x, rtheta,
+    alc_scores_gemm_kernel<T, STAGE><<<dim3(nblk, B), SG_THREADS, smem, st>>>(j, p, nc, Xj, Kinv, cands, cand_idx, x, rtheta,
                                                                        eta, wv, wl, delta, part);
     return cudaGetLastError();
 }
@@ -264,8 +313,12 @@ cudaError_t launch_alc_scores_gemm(int B, int j, int p, int nc, const double *Xj
     alc_scores_prep_kernel<<<B, SG_THREADS, sp, st>>>(j, p, Xj, Kinv, x, rtheta, wv, wl);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    e = (T == 64) ? sg_launch<64>(B, j, p, nc, Xj, Kinv, cands, cand_idx, x, rtheta, eta, wv, wl, delta, part, st)
-                  : sg_launch<32>(B, j, p, nc, Xj, Kinv, cands, cand_idx, x, rtheta, eta, wv, wl, delta, part, st);
+    if (T == 64)
+        e = sg_launch<64, false>(B, j, p, nc, Xj, Kinv, cands, cand_idx, x, rtheta, eta, wv, wl, delta, part, st);
+    else if (sg_stage(j))
+        e = sg_launch<32, true>(B, j, p, nc, Xj, Kinv, cands, cand_idx, x, rtheta, eta, wv, wl, delta, part, st);
+    else
+        e = sg_launch<32, false>(B, j, p, nc, Xj, Kinv, cands, cand_idx, x, rtheta, eta, wv, wl, delta, part, st);
     if (e != cudaSuccess) return e;
     alc_scores_merge_kernel<<<B, SG_THREADS, 0, st>>>(nblk, part, best, gap);
     if (launches) *launches += 3;
