@@ -282,6 +282,14 @@ def main():
                 "peak_basis": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz",
                 "peak_measured_dfma": meas,
                 "kernel_ms_per_launch": alc_launch_ms}
+        if form == "incremental":
+            # secondary view: the per-candidate state w_c streamed every step (sum over steps
+            # of (N'-j-1) j entries x 8 B per location) against the shared-memory bandwidth
+            # (128 B/clk/SM x 148 x 1.965 GHz); part of it is served by registers / TMEM
+            sb = M_rank * sum((Np - jj - 1) * jj * 8.0 for jj in range(n)) / (alc_launch_ms / 1000.0) / 1e9
+            smem_peak = 128 * 148 * 1.965
+            roof["state_stream"] = {"achieved_GBps": sb, "smem_peak_GBps": smem_peak, "frac": sb / smem_peak,
+                                    "bytes": "sum_j (N'-j-1) j 8 B per location (w_c entries read per step)"}
         return dict(ms_step=ms_step, value=M_all / (ms_step / 1000.0), alc_ms=alc_launch_ms,
                     nn_ms=float(t[2]) / args.steps, launches=launches, res=res, clk=clk, roofline=roof)
 
