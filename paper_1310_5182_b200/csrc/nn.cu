@@ -16,6 +16,7 @@
 // re-chosen from the sample; after a few misses the query falls back to an
 // exact 8-bit radix select over the 64-bit keys (robust to massive ties).
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "lagp_internal.cuh"
 #include "launch.h"
@@ -261,6 +262,22 @@ __global__ void nn_prep_kernel(const double *__restrict__ X, int64_t N, int p, f
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
     if ((threadIdx.x & 31) == 0) atomicMax(maxn2, (unsigned long long)__double_as_longlong(mx));
+}
+
+__device__ __forceinline__ uint32_t f32_to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+
+// D = A B (m16n8k8, TF32 inputs, FP32 accumulate from 0) — the warp-level tensor path
+__device__ __forceinline__ void mma_tf32_16x8x8(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                                uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%10, %10, %10, %10};\n"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(0.f));
 }
 
 // FP32 row of the prefilter copy (P compile-time, 0 = generic)
@@ -519,7 +536,10 @@ __device__ __forceinline__ float row_dotf(const float *xf, const float *qf, int 
     return acc.x + acc.y;
 }
 
-template <int P>
+// MMA = true (p = 8 only): the filter's dot products on the tensor path in TF32 —
+// worth it when survivors are rare (N'/N small, e.g. C4), since every hit costs a
+// serial append; the FFMA2 path is faster for denser pools (C2: 3.3 vs 3.9 ms).
+template <int P, bool MMA>
 __global__ void __launch_bounds__(NN_THREADS)
 nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, const float *__restrict__ rn2f,
                const unsigned long long *maxn2_bits, const unsigned long long *__restrict__ kmin,
@@ -651,7 +671,11 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 // <= 4u(||x||^2 + ||q||^2) and the FP32 evaluation by <= 2(p+3)u(||x||^2 + ||q||^2)
                 // (first order), i.e. <= (2p+10)u(||x||^2 + ||q||^2); the margin doubles it, so
                 // every row with exact d2 <= tau passes and the FP64 key alone decides.
-                const double thr = tau + (4.0 * p + 20.0) * u32 * (s.qn2[q] + Bn2);
+                // MMA: TF32 inputs (10-bit mantissas) and FP32 accumulation bound the dot-form
+                // error by (2^-10 + p 2^-20 + (2p+10) 2^-24)(||x~||^2 + ||q~||^2), doubled
+                const double thr = MMA
+                    ? tau + 2.0 * (9.765625e-04 + p * 9.5367431640625e-07 + (2.0 * p + 10.0) * u32) * (s.qn2[q] + Bn2)
+                    : tau + (4.0 * p + 20.0) * u32 * (s.qn2[q] + Bn2);
                 s.thrf[q] = isfinite(thr) ? __double2float_ru(thr) : INFINITY;
             }
             if (tid < NN_Q && s.state[tid] != 0) s.thrf[tid] = __int_as_float(0x7fc00000);  // NaN: inactive
@@ -664,51 +688,126 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
             // (the loop bound is warp-uniform: the ballots below need whole warps)
             // per-warp append counters in registers: lane q holds this warp's count for query q
             int wcr = 0;
-            for (int64_t wbase = tid - lane; wbase < N; wbase += 4 * (int64_t)blockDim.x) {
-                const int64_t base = wbase + lane;
-                float xf[4][P ? P : LAGP_PMAX];
-                float rn[4];
+            if constexpr (MMA && P == 8) {
+                // Tensor-core filter (mma.sync m16n8k8 TF32): a warp takes 16 rows x 8
+                // queries per MMA, D = X~[16x8] Q~^T[8x8]; MMA coordinate k is x~ coordinate
+                // perm(k), perm(t) = 2t, perm(t + 4) = 2t + 1, so each thread's A elements
+                // are one float2 of its row. Lane (g = lane/4, t = lane%4) holds
+                // d[0..3] = dot(rows g, g+8; queries 2t, 2t+1).
+                const int g = lane >> 2, t = lane & 3;
+                uint32_t bq[2][2];
+                float qn_l[2][2], thr_l[2][2];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int64_t r = base + u * (int64_t)blockDim.x;
-                    if (r < N) {
-                        load_row32<P>(X32, r, p, xf[u]);
-                        rn[u] = __ldg(rn2f + r);
-                    } else {
+                for (int gr = 0; gr < 2; gr++) {
+                    bq[gr][0] = f32_to_tf32(s.qf[8 * gr + g][2 * t]);
+                    bq[gr][1] = f32_to_tf32(s.qf[8 * gr + g][2 * t + 1]);
 #pragma unroll
-                        for (int k = 0; k < (P ? P : LAGP_PMAX); k++) xf[u][k] = 0.f;
-                        rn[u] = __int_as_float(0x7fc00000);  // NaN: never <= thr, even thr = +inf
+                    for (int h = 0; h < 2; h++) {
+                        qn_l[gr][h] = s.qn2f[8 * gr + 2 * t + h];
+                        thr_l[gr][h] = s.thrf[8 * gr + 2 * t + h];  // NaN for inactive queries
                     }
                 }
-#pragma unroll 1
-                for (int q = 0; q < NN_Q; q++) {  // inactive queries have thr = NaN: no candidates
-                    float qv[P ? P : LAGP_PMAX];
+                // 4 tiles (64 rows) per warp iteration: all loads issued before any MMA
+                constexpr int NT = 4;
+                for (int64_t rb = (int64_t)wid * 16 * NT; rb < N; rb += (int64_t)nw * 16 * NT) {
+                    float2 xa[NT], xb[NT];
+                    float rnA[NT], rnB[NT];
 #pragma unroll
-                    for (int k = 0; k < (P ? P : LAGP_PMAX); k++) qv[k] = s.qf[q][k];
-                    const float qn = s.qn2f[q], thr = s.thrf[q];
-                    bool hit[4];
-                    unsigned mm[4];
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        hit[u] = fmaf(-2.f, row_dotf<P>(xf[u], qv, p), qn + rn[u]) <= thr;
-                        mm[u] = __ballot_sync(0xffffffffu, hit[u]);
+                    for (int u = 0; u < NT; u++) {
+                        const int64_t rA = rb + 16 * u + g, rB = rA + 8;
+                        xa[u] = make_float2(0.f, 0.f);
+                        xb[u] = make_float2(0.f, 0.f);
+                        rnA[u] = __int_as_float(0x7fc00000);
+                        rnB[u] = __int_as_float(0x7fc00000);
+                        if (rA < N) {
+                            xa[u] = __ldg(reinterpret_cast<const float2 *>(X32 + rA * 8) + t);
+                            rnA[u] = __ldg(rn2f + rA);
+                        }
+                        if (rB < N) {
+                            xb[u] = __ldg(reinterpret_cast<const float2 *>(X32 + rB * 8) + t);
+                            rnB[u] = __ldg(rn2f + rB);
+                        }
                     }
-                    // append to this warp's own segment of the query's buffer: the warp
-                    // owns its counter, so positions come from ballots alone (no atomics);
-                    // only the 4-row groups with a hit do any work
-                    if (mm[0] | mm[1] | mm[2] | mm[3]) {
-                        int wc = __shfl_sync(0xffffffffu, wcr, q);
-                        const unsigned lt = (1u << lane) - 1u;
-                        int32_t *seg = bufi + q * bufcap + wid * segcap;
 #pragma unroll
-                        for (int u = 0; u < 4; u++) {
-                            if (mm[u]) {
-                                const int pos = wc + __popc(mm[u] & lt);
-                                if (hit[u] && pos < segcap) seg[pos] = (int)(base + u * (int64_t)blockDim.x);
-                                wc += __popc(mm[u]);
+                    for (int u = 0; u < NT; u++) {
+                        const int64_t r0 = rb + 16 * u;
+                        const uint32_t a0 = f32_to_tf32(xa[u].x), a1 = f32_to_tf32(xb[u].x), a2 = f32_to_tf32(xa[u].y),
+                                       a3 = f32_to_tf32(xb[u].y);
+#pragma unroll
+                        for (int gr = 0; gr < 2; gr++) {
+                            float d[4];
+                            mma_tf32_16x8x8(d, a0, a1, a2, a3, bq[gr][0], bq[gr][1]);
+                            bool h[4];
+                            h[0] = fmaf(-2.f, d[0], rnA[u] + qn_l[gr][0]) <= thr_l[gr][0];
+                            h[1] = fmaf(-2.f, d[1], rnA[u] + qn_l[gr][1]) <= thr_l[gr][1];
+                            h[2] = fmaf(-2.f, d[2], rnB[u] + qn_l[gr][0]) <= thr_l[gr][0];
+                            h[3] = fmaf(-2.f, d[3], rnB[u] + qn_l[gr][1]) <= thr_l[gr][1];
+                            if (__any_sync(0xffffffffu, h[0] | h[1] | h[2] | h[3])) {
+                                // rare: walk the hits in a fixed order (deterministic segments)
+#pragma unroll
+                                for (int v = 0; v < 4; v++) {
+                                    unsigned m = __ballot_sync(0xffffffffu, h[v]);
+                                    while (m) {
+                                        const int l = __ffs(m) - 1;
+                                        m &= m - 1;
+                                        const int q = 8 * gr + 2 * (l & 3) + (v & 1);
+                                        const int64_t row = r0 + (l >> 2) + 8 * (v >> 1);
+                                        const int pos = __shfl_sync(0xffffffffu, wcr, q);
+                                        if (lane == 0 && pos < segcap) bufi[q * bufcap + wid * segcap + pos] = (int)row;
+                                        if (lane == q) wcr++;
+                                    }
+                                }
                             }
                         }
-                        if (lane == q) wcr = wc;
+                    }
+                }
+            } else {
+                for (int64_t wbase = tid - lane; wbase < N; wbase += 4 * (int64_t)blockDim.x) {
+                    const int64_t base = wbase + lane;
+                    float xf[4][P ? P : LAGP_PMAX];
+                    float rn[4];
+    #pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int64_t r = base + u * (int64_t)blockDim.x;
+                        if (r < N) {
+                            load_row32<P>(X32, r, p, xf[u]);
+                            rn[u] = __ldg(rn2f + r);
+                        } else {
+    #pragma unroll
+                            for (int k = 0; k < (P ? P : LAGP_PMAX); k++) xf[u][k] = 0.f;
+                            rn[u] = __int_as_float(0x7fc00000);  // NaN: never <= thr, even thr = +inf
+                        }
+                    }
+    #pragma unroll 1
+                    for (int q = 0; q < NN_Q; q++) {  // inactive queries have thr = NaN: no candidates
+                        float qv[P ? P : LAGP_PMAX];
+    #pragma unroll
+                        for (int k = 0; k < (P ? P : LAGP_PMAX); k++) qv[k] = s.qf[q][k];
+                        const float qn = s.qn2f[q], thr = s.thrf[q];
+                        bool hit[4];
+                        unsigned mm[4];
+    #pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            hit[u] = fmaf(-2.f, row_dotf<P>(xf[u], qv, p), qn + rn[u]) <= thr;
+                            mm[u] = __ballot_sync(0xffffffffu, hit[u]);
+                        }
+                        // append to this warp's own segment of the query's buffer: the warp
+                        // owns its counter, so positions come from ballots alone (no atomics);
+                        // only the 4-row groups with a hit do any work
+                        if (mm[0] | mm[1] | mm[2] | mm[3]) {
+                            int wc = __shfl_sync(0xffffffffu, wcr, q);
+                            const unsigned lt = (1u << lane) - 1u;
+                            int32_t *seg = bufi + q * bufcap + wid * segcap;
+    #pragma unroll
+                            for (int u = 0; u < 4; u++) {
+                                if (mm[u]) {
+                                    const int pos = wc + __popc(mm[u] & lt);
+                                    if (hit[u] && pos < segcap) seg[pos] = (int)(base + u * (int64_t)blockDim.x);
+                                    wc += __popc(mm[u]);
+                                }
+                            }
+                            if (lane == q) wcr = wc;
+                        }
                     }
                 }
             }
@@ -845,13 +944,13 @@ size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime, bool sorted) {
            (size_t)grid * NN_Q * bc * (sizeof(uint64_t) + 2 * sizeof(int32_t)) + 256;
 }
 
-template <int P>
+template <int P, bool MMA>
 static cudaError_t launch_nn_t(const double *X, const float *X32, const float *rn2f, const unsigned long long *mx,
                                const unsigned long long *kmin, const unsigned long long *kmax, int64_t N, int p,
                                const double *XX, int64_t M, int Nprime, int n0, int sorted, int32_t *pool, double *d2,
                                char *w, int grid, int *fb, cudaStream_t st) {
     size_t smem = sizeof(NNSmem);
-    cudaError_t e = cudaFuncSetAttribute(nn_pool_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(nn_pool_kernel<P, MMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int bc = nn_bufcap(Nprime, sorted != 0);
     int32_t *bcmp = (int32_t *)w;
@@ -859,7 +958,7 @@ static cudaError_t launch_nn_t(const double *X, const float *X32, const float *r
     uint64_t *bk = (uint64_t *)w;
     w += (size_t)grid * NN_Q * bc * sizeof(uint64_t);
     int32_t *bi = (int32_t *)w;
-    nn_pool_kernel<P><<<grid, NN_THREADS, smem, st>>>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, bc, sorted,
+    nn_pool_kernel<P, MMA><<<grid, NN_THREADS, smem, st>>>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, bc, sorted,
                                                       pool, d2, bcmp, bk, bi, fb);
     return cudaGetLastError();
 }
@@ -904,12 +1003,18 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
     }
     if (launches) (*launches)++;
     switch (p) {
-        case 1: return launch_nn_t<1>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        case 2: return launch_nn_t<2>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        case 3: return launch_nn_t<3>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        case 4: return launch_nn_t<4>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        case 8: return launch_nn_t<8>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        default: return launch_nn_t<0>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 1: return launch_nn_t<1, false>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 2: return launch_nn_t<2, false>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 3: return launch_nn_t<3, false>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 4: return launch_nn_t<4, false>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 8: {
+            // tensor-core filter when survivors are rare (~1.5 N'/N of the pairs pass)
+            const char *ev = getenv("LAGP_NN_MMA");
+            const bool mma = ev ? ev[0] == '1' : (double)Nprime <= 0.004 * (double)N;
+            if (mma) return launch_nn_t<8, true>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+            return launch_nn_t<8, false>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        }
+        default: return launch_nn_t<0, false>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
     }
 }
 
