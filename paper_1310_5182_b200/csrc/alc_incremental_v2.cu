@@ -151,8 +151,8 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     // entry tiers of w_c: registers [0, R), tensor memory [T0, T1), shared memory
     // [S0, S1), L2 slab [G0, n); tfirst puts tensor memory before shared memory
-    const int T0 = tfirst ? R : R + S, T1 = T0 + T;
-    const int S0 = tfirst ? R + T : R, S1 = S0 + S;
+    const int T0 = (tfirst & 1) ? R : R + S, T1 = T0 + T;
+    const int S0 = (tfirst & 1) ? R + T : R, S1 = S0 + S;
     const int G0 = R + S + T;
     const int G = n - n0;
     const double eta = A.eta;
@@ -477,7 +477,7 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
                 }
             }
             };
-            if ((wid >> 2) & 1) {  // warps w and w+4 share an SMSP: opposite orders
+            if ((tfirst & 2) ? false : ((wid >> 2) & 1)) {  // warps w and w+4 share an SMSP: opposite orders
                 dot_phase();
                 kx_phase();
             } else {
@@ -596,6 +596,8 @@ bool inc_v2_plan(int n, int p, int Nprime, size_t smem_optin, IncPlan &pl) {
     pl.v2 = true;
     const char *tf = getenv("LAGP_V2_TFIRST");  // A/B: 1 = tensor memory before shared memory
     pl.tfirst = (tf && tf[0] == '1') ? 1 : 0;  // measured: TMEM after shared memory is faster
+    const char *ns = getenv("LAGP_V2_NOSTAGGER");  // A/B: every warp runs K(x_c,x*) before the dot
+    if (ns && ns[0] == '1') pl.tfirst |= 2;
     pl.cpt = cpt;
     pl.R = R;
     pl.S = S;
