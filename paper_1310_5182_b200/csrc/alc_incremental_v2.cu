@@ -40,20 +40,21 @@
 
 namespace lagp {
 
-// threads per CTA by candidates per thread: N' <= 512 -> 512 x 1, else 1024/CPT x CPT
-__host__ __device__ constexpr int v2_threads(int cpt) { return cpt == 1 ? 512 : 1024 / cpt; }
+// CTA shapes (threads TH x candidates per thread CPT): N' <= 512: 512 x 1; N' <= 1024:
+// 512 x 2 (default), 256 x 4 or 1024 x 1 (A/B, LAGP_V2_CPT=4|1)
 
-// register entries per candidate for (P, CPT)
-template <int P, int CPT>
+// register entries per candidate for (P, CPT, TH)
+template <int P, int CPT, int TH>
 struct V2R {
-    static constexpr int value = (CPT == 1) ? 16 : (CPT == 2 ? (P <= 4 ? 8 : 4) : (P <= 4 ? 8 : 6));
+    static constexpr int value =
+        (TH == 1024) ? 2 : (CPT == 1) ? 16 : (CPT == 2 ? (P <= 4 ? 8 : 4) : (P <= 4 ? 8 : 6));
 };
 
-// TMEM entries per candidate: each thread owns 512 B of tensor memory (512 columns
-// x 128 lanes / 512 threads), i.e. 64 doubles shared by its CPT candidates
-template <int CPT>
+// TMEM entries per candidate: each thread owns 256 KB / TH of tensor memory (its warp's
+// 65536/TH columns of its lane quarter), shared by its CPT candidates
+template <int CPT, int TH>
 struct V2T {
-    static constexpr int value = 64 / CPT;
+    static constexpr int value = (65536 / TH) / 2 / CPT;
 };
 
 // warp post record (doubles): key | gidx,pos | key2 | - | x[8] | rrho z y - | w[R] | w[TMEM part]
@@ -137,11 +138,11 @@ __device__ volatile double g_v2_sink;
 template <int P, int CPT, int TH>
 __global__ void __launch_bounds__(TH, 1)
 alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
-    constexpr int R = V2R<P, CPT>::value;
+    constexpr int R = V2R<P, CPT, TH>::value;
     constexpr int V2_THREADS = TH;
     constexpr int V2_NW = TH / 32;
     constexpr int NPC = V2_THREADS * CPT;  // columns (candidates) per pair row
-    constexpr int T = V2T<CPT>::value;      // entries [R+S, R+S+T) in tensor memory
+    constexpr int T = V2T<CPT, TH>::value;  // entries [R+S, R+S+T) in tensor memory
     constexpr int REC = v2_rec(R, T);
     constexpr int RT = RW + R;              // record offset of the TMEM entries
     extern __shared__ __align__(16) double sm[];
@@ -169,7 +170,7 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
-    const uint32_t tbase = s_taddr + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)(128 * (wid >> 2));
+    const uint32_t tbase = s_taddr + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)((65536 / TH) * (wid >> 2));
     __shared__ double zyv[2][LAGP_NMAX];  // z_j, y~_j of every append (a5)
     __shared__ double s_exptab[32];        // 2^(k/32) for exp_nonpos_tab
     if (threadIdx.x < 32) s_exptab[threadIdx.x] = c_exp2_32[threadIdx.x];
@@ -548,9 +549,8 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
 }
 
 // ---------------------------------------------------------------- host side
-template <int P, int CPT>
+template <int P, int CPT, int TH>
 static cudaError_t v2_launch_t(const AlcArgs &a, int S, int tfirst, int grid, size_t smem, cudaStream_t st) {
-    constexpr int TH = v2_threads(CPT);
     cudaError_t e = cudaFuncSetAttribute(alc_incremental_v2_kernel<P, CPT, TH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -558,32 +558,33 @@ static cudaError_t v2_launch_t(const AlcArgs &a, int S, int tfirst, int grid, si
     return cudaGetLastError();
 }
 
-template <int CPT>
-static int v2_R_cpt(int p) {
+template <int CPT, int TH>
+static int v2_R_t(int p) {
     switch (p) {
-        case 1: return V2R<1, CPT>::value;
-        case 2: return V2R<2, CPT>::value;
-        case 3: return V2R<3, CPT>::value;
-        case 4: return V2R<4, CPT>::value;
-        case 8: return V2R<8, CPT>::value;
+        case 1: return V2R<1, CPT, TH>::value;
+        case 2: return V2R<2, CPT, TH>::value;
+        case 3: return V2R<3, CPT, TH>::value;
+        case 4: return V2R<4, CPT, TH>::value;
+        case 8: return V2R<8, CPT, TH>::value;
         default: return -1;
     }
 }
 
-static int v2_R(int p, int cpt) {
-    return cpt == 1 ? v2_R_cpt<1>(p) : cpt == 2 ? v2_R_cpt<2>(p) : v2_R_cpt<4>(p);
+static int v2_R(int p, int cpt, int th) {
+    if (th == 1024) return v2_R_t<1, 1024>(p);
+    return cpt == 1 ? v2_R_t<1, 512>(p) : cpt == 2 ? v2_R_t<2, 512>(p) : v2_R_t<4, 256>(p);
 }
 
 bool inc_v2_plan(int n, int p, int Nprime, size_t smem_optin, IncPlan &pl) {
     if (Nprime > 1024) return false;
-    int cpt = Nprime <= 512 ? 1 : 2;
-    const char *ev = getenv("LAGP_V2_CPT");  // A/B experiments: 2 or 4 for N' in (512, 1024]
-    if (ev && cpt > 1 && (ev[0] == '2' || ev[0] == '4')) cpt = ev[0] - '0';
-    const int R = v2_R(p, cpt);
+    int cpt = Nprime <= 512 ? 1 : 2, th = 512;
+    const char *ev = getenv("LAGP_V2_CPT");  // A/B experiments for N' in (512, 1024]: 4 (256 thr) or 1 (1024 thr)
+    if (ev && Nprime > 512 && ev[0] == '4') { cpt = 4; th = 256; }
+    if (ev && Nprime > 512 && ev[0] == '1') { cpt = 1; th = 1024; }
+    const int R = v2_R(p, cpt, th);
     if (R < 0) return false;
-    const int th = v2_threads(cpt);
     const int npc = th * cpt;
-    const int T = cpt == 1 ? V2T<1>::value : cpt == 2 ? V2T<2>::value : V2T<4>::value;
+    const int T = (65536 / th) / 2 / cpt;
     const size_t fixed = (size_t)2 * (th / 32) * v2_rec(R, T) * sizeof(double);
     if (smem_optin < fixed + 2048) return false;
     const size_t pair_bytes = (size_t)npc * 2 * sizeof(double);
@@ -599,6 +600,7 @@ bool inc_v2_plan(int n, int p, int Nprime, size_t smem_optin, IncPlan &pl) {
     const char *ns = getenv("LAGP_V2_NOSTAGGER");  // A/B: every warp runs K(x_c,x*) before the dot
     if (ns && ns[0] == '1') pl.tfirst |= 2;
     pl.cpt = cpt;
+    pl.threads = th;
     pl.R = R;
     pl.S = S;
     pl.global_entries = n - R - S - T > 0 ? n - R - S - T : 0;
@@ -609,18 +611,19 @@ bool inc_v2_plan(int n, int p, int Nprime, size_t smem_optin, IncPlan &pl) {
 }
 
 cudaError_t launch_alc_incremental_v2(const AlcArgs &a, const IncPlan &pl, int grid, cudaStream_t st) {
-#define V2_DISPATCH(CPT_)                                                         \
-    switch (a.p) {                                                                \
-        case 1: return v2_launch_t<1, CPT_>(a, pl.S, pl.tfirst, grid, pl.smem, st);          \
-        case 2: return v2_launch_t<2, CPT_>(a, pl.S, pl.tfirst, grid, pl.smem, st);          \
-        case 3: return v2_launch_t<3, CPT_>(a, pl.S, pl.tfirst, grid, pl.smem, st);          \
-        case 4: return v2_launch_t<4, CPT_>(a, pl.S, pl.tfirst, grid, pl.smem, st);          \
-        case 8: return v2_launch_t<8, CPT_>(a, pl.S, pl.tfirst, grid, pl.smem, st);          \
-        default: return cudaErrorInvalidValue;                                    \
+#define V2_DISPATCH(CPT_, TH_)                                                                 \
+    switch (a.p) {                                                                             \
+        case 1: return v2_launch_t<1, CPT_, TH_>(a, pl.S, pl.tfirst, grid, pl.smem, st);       \
+        case 2: return v2_launch_t<2, CPT_, TH_>(a, pl.S, pl.tfirst, grid, pl.smem, st);       \
+        case 3: return v2_launch_t<3, CPT_, TH_>(a, pl.S, pl.tfirst, grid, pl.smem, st);       \
+        case 4: return v2_launch_t<4, CPT_, TH_>(a, pl.S, pl.tfirst, grid, pl.smem, st);       \
+        case 8: return v2_launch_t<8, CPT_, TH_>(a, pl.S, pl.tfirst, grid, pl.smem, st);       \
+        default: return cudaErrorInvalidValue;                                                 \
     }
-    if (pl.cpt == 1) { V2_DISPATCH(1) }
-    if (pl.cpt == 2) { V2_DISPATCH(2) }
-    V2_DISPATCH(4)
+    if (pl.threads == 1024) { V2_DISPATCH(1, 1024) }
+    if (pl.cpt == 1) { V2_DISPATCH(1, 512) }
+    if (pl.cpt == 2) { V2_DISPATCH(2, 512) }
+    V2_DISPATCH(4, 256)
 #undef V2_DISPATCH
 }
 
