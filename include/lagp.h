@@ -198,7 +198,7 @@ lagp_status laGP_predict(int32_t B, int32_t n, int32_t p, const double *Xn, cons
  * laGP_exp_nonpos — the correlation kernel's exponential alone: y[i] = exp(x[i])
  * for x[i] <= 0 as the incremental local-design kernels evaluate it inside
  * K(x, x') = exp(-||x - x'||^2 / theta) (Gaussian correlation): a
- * 32-entry table of 2^(k/32) and a degree-6 polynomial, ~1 ulp; exp(x) = 0 for
+ * 16-entry table of 2^(k/16) and a degree-7 polynomial, ~1 ulp; exp(x) = 0 for
  * x < -708; NaN in, NaN out. x, y device arrays of n doubles (may alias).
  * Positive inputs are outside the contract (the kernels never form them).
  * Constraints: n >= 0.

@@ -172,8 +172,8 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t tbase = s_taddr + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)((65536 / TH) * (wid >> 2));
     __shared__ double zyv[2][LAGP_NMAX];  // z_j, y~_j of every append (a5)
-    __shared__ double s_exptab[32];        // 2^(k/32) for exp_nonpos_tab
-    if (threadIdx.x < 32) s_exptab[threadIdx.x] = c_exp2_32[threadIdx.x];
+    __shared__ double s_exptab[16];        // 2^(k/16) for exp_nonpos_tab
+    if (threadIdx.x < 16) s_exptab[threadIdx.x] = c_exp2_16[threadIdx.x];
 
     for (int64_t xi = blockIdx.x; xi < A.M; xi += gridDim.x) {
         const double rth = A.theta_vec ? 1.0 / A.theta_vec[xi] : A.rtheta;  // per-location theta (Fig 1 step 4)

@@ -13,8 +13,8 @@ constexpr int DIAG_THREADS = 256;
 
 // the table exponential of the incremental kernels, elementwise (laGP_exp_nonpos)
 __global__ void exp_nonpos_kernel(const double *__restrict__ x, double *__restrict__ y, int64_t n) {
-    __shared__ double tab[32];
-    if (threadIdx.x < 32) tab[threadIdx.x] = c_exp2_32[threadIdx.x];
+    __shared__ double tab[16];
+    if (threadIdx.x < 16) tab[threadIdx.x] = c_exp2_16[threadIdx.x];
     __syncthreads();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         y[i] = exp_nonpos_tab(x[i], tab);

@@ -62,39 +62,37 @@ __device__ __forceinline__ double exp_nonpos(double x) {
     return __longlong_as_double(__double_as_longlong(q) + ((long long)ni << 52));
 }
 
-// exp(x) for x <= 0 from a 32-entry table, ~1 ulp, branch-free, no FP64<->int
+// exp(x) for x <= 0 from a 16-entry table, ~1 ulp, branch-free, no FP64<->int
 // conversions (the hot-loop variant used by the incremental kernels):
-//   N = round(32 x / ln2) by the 1.5*2^52 shifter (t = fma(x, 32/ln2, S), N in the
-//   low bits of t), r = x - N ln2/32 (Cody-Waite, |r| <= ln2/64),
-//   e^r - 1 by its degree-6 Taylor polynomial (truncation < 4e-18),
-//   exp(x) = 2^m T[k] (1 + (e^r - 1)), N = 32 m + k, T[k] = 2^(k/32) (rounded).
-// x is clamped at -708 (2^m stays normal) and the result selected to 0 below it;
-// NaN propagates. `tab` points at the 32 table entries (shared memory).
-__constant__ double c_exp2_32[32] = {
-    1.0, 1.0218971486541166, 1.0442737824274138, 1.0671404006768237, 1.0905077326652577,
-    1.1143867425958924, 1.1387886347566916, 1.1637248587775775, 1.189207115002721, 1.215247359980469,
-    1.241857812073484, 1.2690509571917332, 1.2968395546510096, 1.3252366431597413, 1.3542555469368927,
-    1.383909881963832, 1.4142135623730951, 1.4451808069770467, 1.4768261459394993, 1.5091644275934228,
-    1.5422108254079407, 1.5759808451078865, 1.6104903319492543, 1.645755478153965, 1.681792830507429,
-    1.718619298122478, 1.7562521603732995, 1.7947090750031072, 1.8340080864093424, 1.8741676341103,
-    1.9152065613971474, 1.9571441241754002};
+//   N = round(16 x / ln2) by the 1.5*2^52 shifter (t = fma(x, 16/ln2, S), N in the
+//   low bits of t), r = x - N ln2/16 (Cody-Waite, |r| <= ln2/32),
+//   e^r - 1 by its degree-7 Taylor polynomial (truncation < 2e-18),
+//   exp(x) = 2^m T[k] (1 + (e^r - 1)), N = 16 m + k, T[k] = 2^(k/16) (rounded).
+// 16 entries = 16 distinct shared-memory bank pairs: a warp's table reads never
+// conflict (equal indices broadcast). x is clamped at -708 (2^m stays normal) and
+// the result selected to 0 below it; NaN propagates. `tab`: the 16 entries (shared).
+__constant__ double c_exp2_16[16] = {
+    1.0, 1.0442737824274138, 1.0905077326652577, 1.1387886347566916, 1.189207115002721, 1.241857812073484,
+    1.2968395546510096, 1.3542555469368927, 1.4142135623730951, 1.4768261459394993, 1.5422108254079407,
+    1.6104903319492543, 1.681792830507429, 1.7562521603732995, 1.8340080864093424, 1.9152065613971474};
 __device__ __forceinline__ double exp_nonpos_tab(double x, const double *tab) {
     const double xc = fmax(x, -708.0);
     const double shifter = 6755399441055744.0;  // 1.5 * 2^52
-    const double t = fma(xc, 46.16624130844683, shifter);  // 32 / ln2
+    const double t = fma(xc, 23.083120654223414, shifter);  // 16 / ln2
     const double nd = t - shifter;
     const int N = (int)(unsigned)__double2loint(t);
-    double r = fma(nd, -0.02166084938653512, xc);  // ln2_hi / 32 (32 significant bits)
-    r = fma(nd, -5.9631716539705866e-12, r);          // ln2_lo / 32
-    double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
+    double r = fma(nd, -0.04332169877307024, xc);  // ln2_hi / 16 (32 significant bits)
+    r = fma(nd, -1.1926343307941173e-11, r);       // ln2_lo / 16
+    double p = fma(r, 1.0 / 5040.0, 1.0 / 720.0);
+    p = fma(p, r, 1.0 / 120.0);
     p = fma(p, r, 1.0 / 24.0);
     p = fma(p, r, 1.0 / 6.0);
     p = fma(p, r, 0.5);
     p = fma(p, r, 1.0);
     const double pm1 = p * r;  // e^r - 1
-    const double T = tab[N & 31];
+    const double T = tab[N & 15];
     const double v0 = fma(T, pm1, T);
-    const double v = __longlong_as_double(__double_as_longlong(v0) + ((long long)(N >> 5) << 52));
+    const double v = __longlong_as_double(__double_as_longlong(v0) + ((long long)(N >> 4) << 52));
     return x < -708.0 ? 0.0 : (x == x ? v : x);
 }
 
