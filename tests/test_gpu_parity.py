@@ -323,3 +323,56 @@ def test_exp_nonpos_table_ulp(torch_dev, lagp):
     assert y[x == 0.0].tolist() == [1.0, 1.0]
     z = lagp.exp_nonpos(torch.tensor([-708.0001, -1e4, float("nan")], dtype=torch.float64, device=dev)).cpu().numpy()
     assert z[0] == 0.0 and z[1] == 0.0 and np.isnan(z[2])
+
+
+def _synthetic(seed, N, M, p):
+    rng = np.random.default_rng(seed)
+    X = rng.random((N, p))
+    Z = np.sin(4 * X).sum(1) + 0.5 * X[:, 0]
+    XX = rng.random((M, p))
+    return X, Z, XX
+
+
+@pytest.mark.parametrize("Nprime,p,n", [(1500, 2, 30), (4000, 8, 40), (8192, 2, 24), (2048, 3, 70)])
+def test_incremental_large_pools(torch_dev, lagp, Nprime, p, n):
+    """1024 < N' <= 8192: the 1024-thread incremental kernel with several
+    candidates per thread (the v2 kernel covers N' <= 1024)."""
+    torch, dev = torch_dev
+    X, Z, XX = _synthetic(Nprime + p, 40000, 6, p)
+    cfg = dict(X=X, Z=Z, XX=XX, d=0.02 * p, g=1e-4, n0=6, n=n, Nprime=Nprime)
+    g, o = run_both(torch, dev, lagp, cfg, form="incremental")
+    compare(g, o, 6, float(np.std(Z)), tau_for(p))
+
+
+@pytest.mark.parametrize("p", [1, 5, 7])
+@pytest.mark.parametrize("form", FORMS)
+def test_generic_dimension(torch_dev, lagp, p, form):
+    """p outside {2, 3, 4, 8}: the generic-p instantiations of the NN and design kernels."""
+    torch, dev = torch_dev
+    X, Z, XX = _synthetic(100 + p, 6000, 10, p)
+    cfg = dict(X=X, Z=Z, XX=XX, d=0.05 * p, g=1e-4, n0=4, n=30, Nprime=400)
+    g, o = run_both(torch, dev, lagp, cfg, form=form)
+    compare(g, o, 4, float(np.std(Z)), tau_for(p))
+
+
+@pytest.mark.parametrize("env", [{"LAGP_V2_CPT": "4"}, {"LAGP_V2_CPT": "1"}, {"LAGP_V2_TFIRST": "1"},
+                                 {"LAGP_V2_NOSTAGGER": "1"}, {"LAGP_INC_V1": "1"}, {"LAGP_NN_MMA": "1"}])
+def test_kernel_variants_agree(torch_dev, lagp, env):
+    """The A/B variants (CTA shapes, tier order, phase order, v1 kernel, TF32 NN
+    filter) against the oracle on the same C2 sample as the default path, with
+    n = 64 so the shared-memory, tensor-memory and slab tiers are all in use."""
+    import os
+
+    torch, dev = torch_dev
+    cfg = make_config("C2", M=24, N=20000, n=64)
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        g, o = run_both(torch, dev, lagp, cfg, form="incremental")
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    compare(g, o, cfg["n0"], float(np.std(cfg["Z"])), tau_for(8))

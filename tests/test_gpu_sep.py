@@ -40,7 +40,7 @@ CASES = [
 
 
 @pytest.mark.parametrize("name,M,N,theta,over", CASES)
-@pytest.mark.parametrize("form", ["explicit", "incremental"])
+@pytest.mark.parametrize("form", ["explicit", "explicit_dfma", "incremental"])
 def test_alc_batch_sep_vs_oracle(torch_dev, lagp, name, M, N, theta, over, form):
     torch, dev = torch_dev
     cfg = make_config(name, M=M, N=N, **over)
