@@ -98,25 +98,27 @@ __device__ bool mle_chol(const double *D, double *L, int n, double rth, double e
     return true;
 }
 
-// W = L^{-1} (lower) by forward substitution, one thread per column; then
-// A = W^T W (symmetric, both triangles).
+// W = L^{-1} (lower) by forward substitution, four lanes (a quad) per column: each
+// row's dot is split over the quad and combined by two quad shuffles, which cuts
+// the longest (column 0) dependent chain about 2-3x; then A = W^T W (symmetric,
+// both triangles). Every lane of the quad writes the same W[i][c], so its own later
+// reads of that entry need no synchronisation.
 __device__ void mle_inverse(const double *L, double *W, double *A, int n) {
     const int tid = threadIdx.x;
     // 1/L_ii first (keeps the divisions off the substitution chains)
     for (int i = tid; i < n; i += blockDim.x) A[i] = 1.0 / L[i * n + i];
     __syncthreads();
-    for (int c = tid; c < n; c += blockDim.x) {
-        for (int i = 0; i < c; i++) W[i * n + c] = 0.0;
+    const int sub = tid & 3;
+    const unsigned qmask = 0xfu << (tid & 28);
+    for (int c = tid >> 2; c < n; c += blockDim.x >> 2) {
+        for (int i = sub; i < c; i += 4) W[i * n + c] = 0.0;
         W[c * n + c] = A[c];
         for (int i = c + 1; i < n; i++) {
-            double s0 = 0.0, s1 = 0.0;
-            int t = c;
-            for (; t + 1 < i; t += 2) {
-                s0 = fma(L[i * n + t], W[t * n + c], s0);
-                s1 = fma(L[i * n + t + 1], W[(t + 1) * n + c], s1);
-            }
-            if (t < i) s0 = fma(L[i * n + t], W[t * n + c], s0);
-            W[i * n + c] = -(s0 + s1) * A[i];
+            double s = 0.0;
+            for (int t = c + sub; t < i; t += 4) s = fma(L[i * n + t], W[t * n + c], s);
+            s += __shfl_xor_sync(qmask, s, 1);
+            s += __shfl_xor_sync(qmask, s, 2);
+            W[i * n + c] = -s * A[i];
         }
     }
     __syncthreads();
@@ -172,11 +174,33 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, const double *D, doub
         L[e] = exp_nonpos(-q) * q;
     }
     __syncthreads();
-    for (int e = tid; e < n * n; e += blockDim.x) {
-        const int a = e / n, b = e - a * n;
-        double s = 0.0;
-        for (int t = 0; t < n; t++) s = fma(A[a * n + t], L[t * n + b], s);
-        W[e] = s;
+    // rows to warps, columns to lanes; two rows per warp pass and two accumulators
+    // per entry (four independent chains per thread)
+    {
+        const int lane = tid & 31, nw = blockDim.x >> 5;
+        for (int a = 2 * (tid >> 5); a < n; a += 2 * nw) {
+            const bool two = a + 1 < n;
+            for (int b = lane; b < n; b += 32) {
+                double s0 = 0.0, s1 = 0.0, u0 = 0.0, u1 = 0.0;
+                int t = 0;
+                for (; t + 1 < n; t += 2) {
+                    const double p0 = L[t * n + b], p1 = L[(t + 1) * n + b];
+                    s0 = fma(A[a * n + t], p0, s0);
+                    s1 = fma(A[a * n + t + 1], p1, s1);
+                    if (two) {
+                        u0 = fma(A[(a + 1) * n + t], p0, u0);
+                        u1 = fma(A[(a + 1) * n + t + 1], p1, u1);
+                    }
+                }
+                if (t < n) {
+                    const double p0 = L[t * n + b];
+                    s0 = fma(A[a * n + t], p0, s0);
+                    if (two) u0 = fma(A[(a + 1) * n + t], p0, u0);
+                }
+                W[a * n + b] = s0 + s1;
+                if (two) W[(a + 1) * n + b] = u0 + u1;
+            }
+        }
     }
     // v = P a (P symmetric)
     for (int a = tid; a < n; a += blockDim.x) {
