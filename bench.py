@@ -112,14 +112,32 @@ def dist_env():
     return world, rank, local
 
 
-def make_inputs(world):
+WORKLOADS = {
+    "C2": "C2: 8-d borehole, N=100000 LHS design, M=10000 LHS locations per GPU, n0=6 n=50 N'=1000",
+    "C3": "C3: 3-d LGBB-shaped grid, N=37908, M=500000 dense grid over all GPUs, n0=6 n=50 N'=1000",
+    "C4": "C4: 8-d borehole, N=M=1000000 LHS over all GPUs, n0=6 n=50 N'=1000 (the north_star target shape)",
+}
+
+
+def make_inputs(world, workload=WORKLOAD):
     from lagp_data import borehole, lhs, make_config
 
-    cfg = make_config(WORKLOAD)
-    if world > 1:  # weak scaling: a global LHS of world x M rows
+    cfg = make_config(workload)
+    if workload == "C2" and world > 1:  # weak scaling: a global LHS of world x M rows
         cfg["XX"] = lhs(cfg["XX"].shape[0] * world, cfg["X"].shape[1], 202)
     cfg["borehole"] = borehole
     return cfg
+
+
+def rank_rows(workload, M_total, rank, world):
+    """C2: weak scaling, 10,000 locations per rank; C3/C4: strong scaling, the config's
+    fixed predictive set split into contiguous shards."""
+    if workload == "C2":
+        return rank * 10_000, 10_000, 10_000 * world
+    import paper_1310_5182_b200 as lagp
+
+    lo, hi, _ = lagp.shard_bounds(M_total, rank, world)
+    return lo, hi - lo, M_total
 
 
 def cpu_baseline(cfg, budget_s=15.0, lo=0):
@@ -146,7 +164,7 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    cfg = make_inputs(1)
+    cfg = make_inputs(1, args.workload)
     import oracle
 
     cores = os.cpu_count() or 1
@@ -169,11 +187,12 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{WORKLOAD}: 8-d borehole N=100000 LHS, n0=6 n=50 N'=1000, d=q10 g=1e-4",
-                   "sample_locations_per_step": S},
+        "scaling": "weak" if args.workload == "C2" else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.workload] + ", d=q10 g=1e-4", "sample_locations_per_step": S},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": o["threads"], "kind": "oracle",
-                         "sample": f"{S} consecutive C2 locations per step (of 10000), OpenMP over locations"},
+                         "sample": f"{S} consecutive {args.workload} locations per step (of "
+                                   f"{cfg['XX'].shape[0]}), OpenMP over locations"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -203,6 +222,8 @@ def main():
                     help="formulation of the headline number")
     ap.add_argument("--compare", default="explicit",
                     help="comma list of other forms timed the same way and reported under 'forms' ('' = none)")
+    ap.add_argument("--workload", default=WORKLOAD, choices=sorted(WORKLOADS),
+                    help="C2 (default, BASELINE configs[1], weak scaling) or the full C3 / C4 shapes (strong)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-two-stage", action="store_true",
                     help="skip the Fig 1 two-stage (design, local MLE, design, MLE, predict) timing")
@@ -221,18 +242,18 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfg = make_inputs(world)
+    if args.workload != "C2":  # the big shapes: headline form only
+        args.compare, args.no_two_stage = "", True
+    cfg = make_inputs(world, args.workload)
     X = torch.from_numpy(cfg["X"]).to(dev)
     Z = torch.from_numpy(cfg["Z"]).to(dev)
-    M_rank = 10_000
-    lo = rank * M_rank
+    lo, M_rank, M_all = rank_rows(args.workload, cfg["XX"].shape[0], rank, world)
     XXr_np = np.ascontiguousarray(cfg["XX"][lo:lo + M_rank])
     XX = torch.from_numpy(XXr_np).to(dev)
     n0, n, Np, d, g = cfg["n0"], cfg["n"], cfg["Nprime"], cfg["d"], cfg["g"]
     p = cfg["X"].shape[1]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
-    M_all = M_rank * world
     nominal, meas = fp64_peak_tflops()
 
     def barrier():
@@ -355,8 +376,8 @@ def main():
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = M_all / (float(te[0]) / 1000.0)
-    h2d = (Xh.nbytes + Zh.nbytes + XXh.nbytes) * world
-    d2h = (M_rank * (n * 4 + 3 * 8 + 4)) * world
+    h2d = (Xh.nbytes + Zh.nbytes) * world + M_all * XXh.shape[1] * 8  # every rank: X, Z and its XX rows
+    d2h = M_all * (n * 4 + 3 * 8 + 4)
 
     if rank != 0:
         if world > 1:
@@ -375,10 +396,10 @@ def main():
             pass
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak" if args.workload == "C2" else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{WORKLOAD}: 8-d borehole, N=100000 LHS design, M=10000 LHS locations per GPU, "
-                               f"n0=6 n=50 N'=1000, d=q10={d:.4f} g=1e-4",
+        "config": {"workload": WORKLOADS[args.workload] + f", d=q10={d:.4f} g=1e-4",
                    "alc_form": args.form, "l2": "flushed (256 MiB write) before every timed step",
                    "parallelism": f"dp{world} (XX sharded, X/Z replicated)"},
         "alc_evals_per_sec": M_all * evals / (ms_step / 1000.0),
@@ -394,7 +415,8 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         o, S, el, used = cpu_baseline(cfg, budget_s=args.cpu_budget, lo=0)
         line["cpu_baseline"] = {"value": S / el, "unit": UNIT, "cores": used, "kind": "oracle",
-                                "sample": f"first {S} of the 10000 C2 locations, OpenMP over locations"}
+                                "sample": f"first {S} of the {M_rank} {args.workload} locations of rank 0, "
+                                          "OpenMP over locations"}
         gi = res["idx"][:S].cpu().numpy()
         line["sample_parity"] = {"locations": S, "identical_index_sequences": int((gi == o["idx"]).all(1).sum())}
         if two:
