@@ -140,6 +140,17 @@ def rank_rows(workload, M_total, rank, world):
     return lo, hi - lo, M_total
 
 
+def cpu_model():
+    """The host CPU model (SURVEY §8d asks for it beside the oracle timing)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(cfg, budget_s=15.0, lo=0):
     """The oracle as it stands, on all host cores, on a bounded sample of the
     workload's locations (consecutive rows of the rank-0 shard)."""
@@ -190,7 +201,7 @@ def run_reference(args):
         "scaling": "weak" if args.workload == "C2" else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": WORKLOADS[args.workload] + ", d=q10 g=1e-4", "sample_locations_per_step": S},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": o["threads"], "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": o["threads"], "kind": "oracle", "cpu": cpu_model(),
                          "sample": f"{S} consecutive {args.workload} locations per step (of "
                                    f"{cfg['XX'].shape[0]}), OpenMP over locations"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -414,7 +425,7 @@ def main():
     }
     if world == 1 and not args.no_cpu_baseline:
         o, S, el, used = cpu_baseline(cfg, budget_s=args.cpu_budget, lo=0)
-        line["cpu_baseline"] = {"value": S / el, "unit": UNIT, "cores": used, "kind": "oracle",
+        line["cpu_baseline"] = {"value": S / el, "unit": UNIT, "cores": used, "kind": "oracle", "cpu": cpu_model(),
                                 "sample": f"first {S} of the {M_rank} {args.workload} locations of rank 0, "
                                           "OpenMP over locations"}
         gi = res["idx"][:S].cpu().numpy()
