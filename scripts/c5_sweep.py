@@ -32,6 +32,7 @@ ap.add_argument("--ps", default="2,8")
 ap.add_argument("--forms", default="explicit,incremental")
 ap.add_argument("--target-ms", type=float, default=400.0)
 ap.add_argument("--sample", type=int, default=4)
+ap.add_argument("--min-m", type=int, default=512)
 ap.add_argument("--out", default=None)
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
@@ -61,6 +62,9 @@ for p in [int(x) for x in a.ps.split(",")]:
                 while r["timing"]["alc_ms"] < a.target_ms / 2 and M < 32768:
                     M = min(32768, M * 2 if r["timing"]["alc_ms"] > 0 else M * 4)
                     r = lagp.alc_batch(X, Z, XXall[:M], *args, form=form, timing=True)
+                # at least two locations per SM in flight: a grid narrower than the GPU
+                # understates the kernel (the slowest points calibrate to M = 64 otherwise)
+                M = max(M, a.min_m)
                 best = None
                 for _ in range(2):
                     r = lagp.alc_batch(X, Z, XXall[:M], *args, form=form, timing=True, gaps=True)
