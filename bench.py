@@ -414,6 +414,18 @@ def main():
                    "alc_form": args.form, "l2": "flushed (256 MiB write) before every timed step",
                    "parallelism": f"dp{world} (XX sharded, X/Z replicated)"},
         "alc_evals_per_sec": M_all * evals / (ms_step / 1000.0),
+        # the same numerator over the local-design kernel time (max over ranks),
+        # the NN stage and the whole step against the FP64 ALU peak (paper counts)
+        "alc_evals_per_sec_kernel": M_all * evals / (head["alc_ms"] / 1000.0),
+        "nn_roofline": {"work": "3p flop per (query, row) pair", "achieved_tflops":
+                        M_rank * cfg["X"].shape[0] * 3 * p / (head["nn_ms"] / 1000.0) / 1e12,
+                        "frac_fp64_peak": M_rank * cfg["X"].shape[0] * 3 * p / (head["nn_ms"] / 1000.0) / 1e12 / nominal,
+                        "note": "the filter runs in FP32x2 (and TF32 MMA for sparse pools); FP64 only on survivors"},
+        "end_to_end_paper_count": {
+            "frac_fp64_peak": (M_all * (alc_paper_flops_per_location(n0, n, Np) + cfg["X"].shape[0] * 3 * p)
+                               / (ms_step / 1000.0) / 1e12 / (world * nominal)),
+            "note": "(ALC paper count (N'-j)(2j^2+4j) + NN 3pN) per location / step time / (R x FP64 peak); "
+                    "above 1 with the incremental form, which does ~20x less arithmetic than the paper count"},
         "phase_ms_per_step": {"nn": head["nn_ms"], "local_design": head["alc_ms"]},
         "roofline": head["roofline"],
         "forms": others,
