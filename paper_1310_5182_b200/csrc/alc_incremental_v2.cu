@@ -18,18 +18,22 @@
 // needs only three running sums: mean = z^T y~, psi = ||y~||^2,
 // s2 = psi (1 + eta - ||z||^2) / n.
 //
-// B200 mapping (differences from alc_incremental.cu):
-//  * 512 threads, CPT = 1 or 2 candidates per thread (candidate c = tid + q*512):
-//    128 registers per thread hold R entries of w_c per candidate (R = 12..16),
-//    and the per-step broadcast reads of the winner's data are shared by CPT
-//    candidates.
-//  * Shared entries are stored in PAIRS (entry-major pairs of rows,
-//    double2 per (pair, candidate)): one LDS.128 per two entries of a column,
-//    the row stride is a compile-time constant (immediate offsets).
+// B200 mapping (differences from alc_incremental.cu; DESIGN.md §5.3b):
+//  * One persistent CTA per SM (the register file allows exactly one): 512 threads
+//    with CPT = 2 candidates per thread (N' <= 512: CPT = 1; A/B shapes 256 x 4 and
+//    1024 x 1), candidate c = tid + q*TH. The per-step broadcast reads of the
+//    winner's data are shared by a thread's CPT candidates.
+//  * Storage tiers of w_c: R entries in registers (R = 4 at p = 8, CPT = 2), then
+//    shared memory in PAIRS (entry-major pairs of rows, double2 per (pair,
+//    candidate): one LDS.128 per two entries, compile-time row stride), then tensor
+//    memory (tcgen05.ld/st on the thread's own lane row: 32 entries per candidate),
+//    then an L2-resident slab (pair layout) — n <= ~62 is on chip at N' = 1000.
 //  * One barrier per step: each warp's best candidate posts its whole record
-//    (key, x_c, 1/rho, z_j, y~_j, register entries) before the barrier; after
-//    it every warp reduces the 16 warp keys itself (redux.sync) and reads the
-//    winner's record — no second barrier, no separate publish phase.
+//    (key, x_c, s, cov, t, register and TMEM entries) before the barrier; after it
+//    every warp reduces the 16 warp keys itself (redux.sync), reads the winner's
+//    record and forms 1/rho = s^{-1/2} — no second barrier, no publish phase.
+//  * Warps w and w+4 (same SMSP) run the FP64-bound K(x_c, x*) and the
+//    shared-memory-bound dot in opposite orders; exp by a 16-entry table.
 //  * y~ is maintained per candidate (t_c) instead of a warp-0 dot per step.
 //  * Flags are accumulated per thread and reduced once per location.
 #include <cuda_runtime.h>
