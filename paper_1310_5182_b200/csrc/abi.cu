@@ -219,7 +219,7 @@ lagp_status alc_batch_impl(const double *X, int64_t N, int32_t p, const double *
     int host_counters[2] = {0, 0};
 
     LAGP_CUDA(ws.alloc((void **)&pool, (size_t)P.chunk * Nprime * sizeof(int32_t)));
-    LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(P.nn_grid, N, p, Nprime, false)));
+    LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(P.nn_grid, N, p, Nprime, false, P.chunk)));
     LAGP_CUDA(ws.alloc((void **)&cache, (size_t)P.alc_grid * P.cache_stride * sizeof(double)));
     // per-CTA slab: pool coordinates [p][Npad] (+ kappa and chosen flags for the DFMA kernel)
     LAGP_CUDA(ws.alloc((void **)&coords, (size_t)P.alc_grid * (p + 2) * P.Npad * sizeof(double)));
@@ -232,7 +232,7 @@ lagp_status alc_batch_impl(const double *X, int64_t N, int32_t p, const double *
     for (int64_t m0 = 0; m0 < M; m0 += P.chunk) {
         const int64_t mc = (M - m0) < P.chunk ? (M - m0) : P.chunk;
         if (timing) LAGP_CUDA(cudaEventRecord(ev[1], st));
-        LAGP_CUDA(lagp::launch_nn(X, N, p, XX + m0 * p, mc, Nprime, n0, false, pool, nullptr, nnws,
+        LAGP_CUDA(lagp::launch_nn(X, N, p, XX + m0 * p, mc, P.chunk, Nprime, n0, false, pool, nullptr, nnws,
                                   lagp::nn_grid(mc, P.sms, Nprime), counters + 1, st, m0 > 0, &launches));
         if (timing) LAGP_CUDA(cudaEventRecord(ev[2], st));
         lagp::AlcArgs a = design_args(P, X, N, p, Z, d, g, n0, n, Nprime);
@@ -443,7 +443,7 @@ lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *
     const MlePlan mp = plan_mle(P.chunk, n, p);
 
     LAGP_CUDA(ws.alloc((void **)&pool, (size_t)P.chunk * Nprime * sizeof(int32_t)));
-    LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(P.nn_grid, N, p, Nprime, false)));
+    LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(P.nn_grid, N, p, Nprime, false, P.chunk)));
     LAGP_CUDA(ws.alloc((void **)&cache, (size_t)P.alc_grid * P.cache_stride * sizeof(double)));
     LAGP_CUDA(ws.alloc((void **)&coords, (size_t)P.alc_grid * (p + 2) * P.Npad * sizeof(double)));
     LAGP_CUDA(ws.alloc((void **)&counters, 2 * sizeof(int)));
@@ -457,7 +457,7 @@ lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *
     for (int64_t m0 = 0; m0 < M; m0 += P.chunk) {
         const int64_t mc = (M - m0) < P.chunk ? (M - m0) : P.chunk;
         if (timing) LAGP_CUDA(cudaEventRecord(ev[1], st));
-        LAGP_CUDA(lagp::launch_nn(X, N, p, XX + m0 * p, mc, Nprime, n0, false, pool, nullptr, nnws,
+        LAGP_CUDA(lagp::launch_nn(X, N, p, XX + m0 * p, mc, P.chunk, Nprime, n0, false, pool, nullptr, nnws,
                                   lagp::nn_grid(mc, P.sms, Nprime), counters + 1, st, m0 > 0, &launches));
         if (timing) {
             LAGP_CUDA(cudaEventRecord(ev[2], st));
@@ -601,10 +601,10 @@ lagp_status laGP_nn_pool(const double *X, int64_t N, int32_t p, const double *XX
         void *nnws = nullptr;
         int *fb = nullptr;
         const int grid = lagp::nn_grid(M, num_sms(), Nprime);
-        LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(grid, N, p, Nprime, true)));
+        LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(grid, N, p, Nprime, true, M)));
         LAGP_CUDA(ws.alloc((void **)&fb, sizeof(int)));
         LAGP_CUDA(cudaMemsetAsync(fb, 0, sizeof(int), st));
-        LAGP_CUDA(lagp::launch_nn(X, N, p, XX, M, Nprime, Nprime, true, pool_out, d2_out, nnws, grid, fb, st, false,
+        LAGP_CUDA(lagp::launch_nn(X, N, p, XX, M, M, Nprime, Nprime, true, pool_out, d2_out, nnws, grid, fb, st, false,
                                   nullptr));
     cleanup:;
     }

@@ -9,10 +9,11 @@ namespace lagp {
 // nn.cu (row a1)
 // sorted = true: the whole pool ascending by (d^2, index) (laGP_nn_pool); false:
 // pool[0..n0) ascending, the rest of the N' nearest in any order (laGP_alc_batch).
-cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64_t M, int Nprime, int n0, bool sorted,
-                      int32_t *pool, double *d2, void *ws, int grid, int *fb, cudaStream_t st, bool prepared,
+// Mmax: the largest chunk of query locations a call with this workspace passes (M <= Mmax).
+cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64_t M, int64_t Mmax, int Nprime, int n0,
+                      bool sorted, int32_t *pool, double *d2, void *ws, int grid, int *fb, cudaStream_t st, bool prepared,
                       int *launches);
-size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime, bool sorted);
+size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime, bool sorted, int64_t Mmax);
 int nn_grid(int64_t M, int num_sms, int Nprime);
 
 // fused local-design kernels (rows a2-a5)

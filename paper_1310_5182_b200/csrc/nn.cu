@@ -52,6 +52,8 @@ struct NNSmem {
     int n0i[LAGP_NMAX];
     int wcnt[NN_THREADS / 32][NN_Q];    // filter appends per (warp segment, query)
     int ovf[NN_Q];                      // a warp segment overflowed
+    int nrng;                           // filter row ranges (in s.hist during the filter)
+    int qid[NN_Q];                      // the group's query indices (cell order)
 };
 
 __device__ __forceinline__ bool key_less(uint64_t ka, int ia, uint64_t kb, int ib) {
@@ -214,23 +216,49 @@ __device__ __forceinline__ double d_from_ordkey(unsigned long long k) {
 // per-dimension min / max of X (the prefilter's centre c = (min + max) / 2)
 __global__ void nn_bounds_kernel(const double *__restrict__ X, int64_t N, int p, unsigned long long *__restrict__ kmin,
                                  unsigned long long *__restrict__ kmax) {
-    for (int k = 0; k < p; k++) {
-        unsigned long long lo = ~0ull, hi = 0ull;
-        for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
-            const unsigned long long o = d_ordkey(X[r * p + k]);
-            lo = o < lo ? o : lo;
-            hi = o > hi ? o : hi;
-        }
+    // one pass over the rows; thread-strided over the flat array so the loads coalesce
+    // (element e belongs to dimension e % p; each thread's stride is a multiple of p
+    // when blockDim*gridDim % p == 0, else the dimension is recomputed)
+    __shared__ unsigned long long slo[LAGP_PMAX], shi[LAGP_PMAX];
+    if (threadIdx.x < LAGP_PMAX) {
+        slo[threadIdx.x] = ~0ull;
+        shi[threadIdx.x] = 0ull;
+    }
+    __syncthreads();
+    const int64_t tot = N * p, stride = (int64_t)gridDim.x * blockDim.x;
+    unsigned long long lo[LAGP_PMAX], hi[LAGP_PMAX];
+#pragma unroll
+    for (int k = 0; k < LAGP_PMAX; k++) {
+        lo[k] = ~0ull;
+        hi[k] = 0ull;
+    }
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += stride) {
+        const int k = (int)(e % p);
+        const unsigned long long o = d_ordkey(X[e]);
+#pragma unroll
+        for (int kk = 0; kk < LAGP_PMAX; kk++)
+            if (kk == k) {
+                lo[kk] = o < lo[kk] ? o : lo[kk];
+                hi[kk] = o > hi[kk] ? o : hi[kk];
+            }
+    }
+    for (int k = 0; k < p; k++) {  // warp reduction, then one shared atomic per warp
+        unsigned long long l = lo[k], h = hi[k];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
-            const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, off), b = __shfl_xor_sync(0xffffffffu, hi, off);
-            lo = a < lo ? a : lo;
-            hi = b > hi ? b : hi;
+            const unsigned long long a = __shfl_xor_sync(0xffffffffu, l, off), c = __shfl_xor_sync(0xffffffffu, h, off);
+            l = a < l ? a : l;
+            h = c > h ? c : h;
         }
         if ((threadIdx.x & 31) == 0) {
-            atomicMin(kmin + k, lo);
-            atomicMax(kmax + k, hi);
+            atomicMin(slo + k, l);
+            atomicMax(shi + k, h);
         }
+    }
+    __syncthreads();
+    if (threadIdx.x < p) {
+        atomicMin(kmin + threadIdx.x, slo[threadIdx.x]);
+        atomicMax(kmax + threadIdx.x, shi[threadIdx.x]);
     }
 }
 
@@ -240,23 +268,113 @@ __device__ __forceinline__ double nn_centre(const unsigned long long *kmin, cons
 
 // The prefilter works on x~ = x - c (distances are translation invariant): the
 // rounding margins scale with ||x~||^2 + ||q~||^2, smallest around the centre.
+//
+// Spatial cells ("cell pruning"): the bounding box of X is cut into
+// gx x gy cells on coordinates 0 and 1 (gy = 1 when p = 1) and the rows of the FP32
+// copy are stored cell by cell (row-major cell order; perm maps a stored position back
+// to the row of X); the queries of a chunk are ordered the same way, so the 16
+// queries of a group are spatial neighbours. Since d^2 >= (x_k - q_k)^2, a row can
+// pass the filter only if |x_k - q_k| <= sqrt(thr) on both cell coordinates: the
+// filter visits only the cells that meet the group's box (one margin cell on every
+// side absorbs the rounding of the cell arithmetic).
+__device__ __forceinline__ double nn_lo(const unsigned long long *kmin, int k) { return d_from_ordkey(kmin[k]); }
+__device__ __forceinline__ double nn_invw(const unsigned long long *kmin, const unsigned long long *kmax, int k, int G) {
+    const double w = d_from_ordkey(kmax[k]) - d_from_ordkey(kmin[k]);
+    return (G > 1 && w > 0.0 && w < INFINITY) ? (double)G / w : 0.0;
+}
+// cell of a coordinate, clamped to [0, G); NaN -> lo (a point) or hi (a box edge)
+__device__ __forceinline__ int nn_cell_lo(double v, double lo, double invw, int G) {
+    if (invw == 0.0) return 0;
+    const double t = (v - lo) * invw;
+    if (!(t >= 0.0)) return 0;
+    return t >= (double)G ? G - 1 : (int)t;
+}
+__device__ __forceinline__ int nn_cell_hi(double v, double lo, double invw, int G) {
+    if (invw == 0.0) return 0;
+    const double t = (v - lo) * invw;
+    if (!(t < (double)G)) return G - 1;
+    return t < 0.0 ? 0 : (int)t;
+}
+__device__ __forceinline__ int nn_cell_of(const double *x, int p, const unsigned long long *kmin,
+                                          const unsigned long long *kmax, int gx, int gy) {
+    const int cx = nn_cell_lo(x[0], nn_lo(kmin, 0), nn_invw(kmin, kmax, 0, gx), gx);
+    const int cy = (gy > 1 && p > 1) ? nn_cell_lo(x[1], nn_lo(kmin, 1), nn_invw(kmin, kmax, 1, gy), gy) : 0;
+    return cx * gy + cy;
+}
+
+// cell histogram of n points (rows of X, or a chunk of query locations)
+__global__ void nn_cell_hist_kernel(const double *__restrict__ X, int64_t n, int p, const unsigned long long *__restrict__ kmin,
+                                    const unsigned long long *__restrict__ kmax, int gx, int gy, int32_t *__restrict__ counts) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(counts + nn_cell_of(X + r * p, p, kmin, kmax, gx, gy), 1);
+}
+
+// exclusive scan of C <= 16384 cell counts by one block of 1024 threads:
+// start[0..C] (start[C] = n) and the scatter cursors cur[c] = start[c]
+__global__ void __launch_bounds__(1024) nn_cell_scan_kernel(const int32_t *__restrict__ counts, int C,
+                                                            int32_t *__restrict__ start, int32_t *__restrict__ cur) {
+    __shared__ int wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int per = (C + 1023) / 1024, c0 = tid * per;
+    int loc = 0;
+    for (int c = c0; c < c0 + per && c < C; c++) loc += counts[c];
+    int x = loc;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int v = wsum[lane];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, v, off);
+            if (lane >= off) v += y;
+        }
+        wsum[lane] = v;
+    }
+    __syncthreads();
+    int run = x - loc + (wid > 0 ? wsum[wid - 1] : 0);
+    for (int c = c0; c < c0 + per && c < C; c++) {
+        start[c] = run;
+        cur[c] = run;
+        run += counts[c];
+    }
+    if (tid == 1023) start[C] = run;
+}
+
+// query locations in cell order: qperm[position] = location
+__global__ void nn_cell_scatter_kernel(const double *__restrict__ XX, int64_t n, int p, const unsigned long long *__restrict__ kmin,
+                                       const unsigned long long *__restrict__ kmax, int gx, int gy, int32_t *__restrict__ cur,
+                                       int32_t *__restrict__ qperm) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        qperm[atomicAdd(cur + nn_cell_of(XX + r * p, p, kmin, kmax, gx, gy), 1)] = (int32_t)r;
+}
+
+// FP32 centred copy of X in cell order (perm[position] = row), its FP32 norms, and
+// B = max ||x~||^2 in FP64 (the margin's bound)
 __global__ void nn_prep_kernel(const double *__restrict__ X, int64_t N, int p, float *__restrict__ X32,
                                float *__restrict__ rn2f, unsigned long long *__restrict__ maxn2,
-                               const unsigned long long *__restrict__ kmin, const unsigned long long *__restrict__ kmax) {
+                               const unsigned long long *__restrict__ kmin, const unsigned long long *__restrict__ kmax,
+                               int gx, int gy, int32_t *__restrict__ cur, int32_t *__restrict__ perm) {
     double mx = 0.0;
     double c[LAGP_PMAX];
     for (int k = 0; k < p; k++) c[k] = nn_centre(kmin, kmax, k);
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t pos = atomicAdd(cur + nn_cell_of(X + r * p, p, kmin, kmax, gx, gy), 1);
+        perm[pos] = (int32_t)r;
         double n2 = 0.0;
         float f2 = 0.f;
         for (int k = 0; k < p; k++) {
             const double v = X[r * p + k] - c[k];
             const float vf = (float)v;
-            X32[r * p + k] = vf;
+            X32[pos * p + k] = vf;
             f2 = fmaf(vf, vf, f2);
             n2 = fma(v, v, n2);
         }
-        rn2f[r] = f2;
+        rn2f[pos] = f2;
         mx = fmax(mx, n2);
     }
 #pragma unroll
@@ -545,7 +663,9 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                const unsigned long long *maxn2_bits, const unsigned long long *__restrict__ kmin,
                const unsigned long long *__restrict__ kmax, int64_t N, int p, const double *__restrict__ XX, int64_t M, int Nprime, int n0, int bufcap,
                int sorted, int32_t *__restrict__ pool_out, double *__restrict__ d2_out, int32_t *__restrict__ bufc_ws,
-               uint64_t *__restrict__ bufk_ws, int32_t *__restrict__ bufi_ws, int *__restrict__ fallback_count) {
+               uint64_t *__restrict__ bufk_ws, int32_t *__restrict__ bufi_ws, int *__restrict__ fallback_count, int gx,
+               int gy, const int32_t *__restrict__ cstart, const int32_t *__restrict__ perm,
+               const int32_t *__restrict__ qperm) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     NNSmem &s = *reinterpret_cast<NNSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
@@ -560,7 +680,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
     const int r2 = (int)ceil(1.5 * (double)Nprime * (double)S2 / (double)N) + 12;
     int r1 = (int)ceil(4.0 * (double)r2 * (double)S1 / (double)S2) + 4;
     if (Nprime >= N) r1 = S1 + 1;
-    // per query: bufi = filter survivors in NN_THREADS/32 warp segments of segcap rows;
+    // per query: bufi = filter survivors (stored positions, cell order) in NN_THREADS/32 warp segments of segcap rows;
     // bufk/bufc = the exact survivors (key, row), compacted
     uint64_t *bufk = bufk_ws + (size_t)blockIdx.x * NN_Q * bufcap;
     int32_t *bufi = bufi_ws + (size_t)blockIdx.x * NN_Q * bufcap;
@@ -572,9 +692,11 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
     for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
         const int64_t q0 = grp * NN_Q;
         const int nq = (int)((M - q0) < NN_Q ? (M - q0) : NN_Q);
+        if (tid < NN_Q) s.qid[tid] = tid < nq ? (qperm ? qperm[q0 + tid] : (int32_t)(q0 + tid)) : 0;
+        __syncthreads();
         for (int e = tid; e < NN_Q * LAGP_PMAX; e += blockDim.x) {
             int q = e / LAGP_PMAX, k = e % LAGP_PMAX;
-            const double v = (q < nq && k < p) ? XX[(q0 + q) * p + k] : 0.0;
+            const double v = (q < nq && k < p) ? XX[(int64_t)s.qid[q] * p + k] : 0.0;
             const double vc = (q < nq && k < p) ? v - nn_centre(kmin, kmax, k) : 0.0;  // centred (prefilter)
             s.qx[q][k] = v;  // raw (exact keys)
             s.nqf[q][k] = -(float)vc;
@@ -683,6 +805,72 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
             unsigned act = 0;
             for (int q = 0; q < NN_Q; q++) act |= (s.state[q] == 0 ? 1u : 0u) << q;
             if (!act) break;
+            // the cells that meet the active queries' box |x_k - q_k| <= sqrt(thr), k = 0, 1,
+            // as maximal runs of stored rows (cell order is row-major: one run per cell column)
+            int *rng_a = reinterpret_cast<int *>(s.hist), *rng_b = rng_a + 128;
+            if (wid == 0) {
+                double lo0 = INFINITY, hi0 = -INFINITY, lo1 = INFINITY, hi1 = -INFINITY;
+                if (lane < NN_Q && s.state[lane] == 0) {
+                    const double r = sqrt((double)s.thrf[lane]);
+                    lo0 = s.qx[lane][0] - r;
+                    hi0 = s.qx[lane][0] + r;
+                    if (p > 1) {
+                        lo1 = s.qx[lane][1] - r;
+                        hi1 = s.qx[lane][1] + r;
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {  // fmin/fmax drop a NaN operand: NaN r -> whole axis below
+                    lo0 = fmin(lo0, __shfl_xor_sync(0xffffffffu, lo0, off));
+                    hi0 = fmax(hi0, __shfl_xor_sync(0xffffffffu, hi0, off));
+                    lo1 = fmin(lo1, __shfl_xor_sync(0xffffffffu, lo1, off));
+                    hi1 = fmax(hi1, __shfl_xor_sync(0xffffffffu, hi1, off));
+                }
+                bool anynan = false;
+                if (lane < NN_Q && s.state[lane] == 0) anynan = isnan(s.thrf[lane]) || isnan(s.qx[lane][0]) || (p > 1 && isnan(s.qx[lane][1]));
+                anynan = __any_sync(0xffffffffu, anynan);
+                int cx0 = 0, cx1 = gx - 1, cy0 = 0, cy1 = gy - 1;
+                if (!anynan) {
+                    const double l0 = nn_lo(kmin, 0), iw0 = nn_invw(kmin, kmax, 0, gx);
+                    cx0 = max(nn_cell_lo(lo0, l0, iw0, gx) - 1, 0);
+                    cx1 = min(nn_cell_hi(hi0, l0, iw0, gx) + 1, gx - 1);
+                    if (gy > 1) {
+                        const double l1 = nn_lo(kmin, 1), iw1 = nn_invw(kmin, kmax, 1, gy);
+                        cy0 = max(nn_cell_lo(lo1, l1, iw1, gy) - 1, 0);
+                        cy1 = min(nn_cell_hi(hi1, l1, iw1, gy) + 1, gy - 1);
+                    }
+                }
+                if (gy == 1) {  // one run
+                    if (lane == 0) {
+                        rng_a[0] = cstart[cx0];
+                        rng_b[0] = cstart[cx1 + 1];
+                        s.nrng = 1;
+                    }
+                } else {  // gx <= 128 columns: load the runs in parallel, merge adjacent ones
+                    for (int cx = cx0 + lane; cx <= cx1; cx += 32) {
+                        rng_a[cx - cx0] = cstart[cx * gy + cy0];
+                        rng_b[cx - cx0] = cstart[cx * gy + cy1 + 1];
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        int nr = 0;
+                        for (int i = 0; i <= cx1 - cx0; i++) {
+                            const int a = rng_a[i], b = rng_b[i];
+                            if (b <= a) continue;
+                            if (nr > 0 && rng_b[nr - 1] == a) {
+                                rng_b[nr - 1] = b;
+                            } else {
+                                rng_a[nr] = a;
+                                rng_b[nr] = b;
+                                nr++;
+                            }
+                        }
+                        s.nrng = nr;
+                    }
+                }
+            }
+            __syncthreads();
+            const int nrng = s.nrng;
             // 4 rows per thread per iteration: each query's coordinates are loaded
             // from shared memory once per 4 rows
             // (the loop bound is warp-uniform: the ballots below need whole warps)
@@ -709,7 +897,9 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 }
                 // 4 tiles (64 rows) per warp iteration: all loads issued before any MMA
                 constexpr int NT = 4;
-                for (int64_t rb = (int64_t)wid * 16 * NT; rb < N; rb += (int64_t)nw * 16 * NT) {
+                for (int ri = 0; ri < nrng; ri++) {
+                const int64_t ra = rng_a[ri], rend = rng_b[ri];
+                for (int64_t rb = ra + (int64_t)wid * 16 * NT; rb < rend; rb += (int64_t)nw * 16 * NT) {
                     float2 xa[NT], xb[NT];
                     float rnA[NT], rnB[NT];
 #pragma unroll
@@ -719,11 +909,11 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                         xb[u] = make_float2(0.f, 0.f);
                         rnA[u] = __int_as_float(0x7fc00000);
                         rnB[u] = __int_as_float(0x7fc00000);
-                        if (rA < N) {
+                        if (rA < rend) {
                             xa[u] = __ldg(reinterpret_cast<const float2 *>(X32 + rA * 8) + t);
                             rnA[u] = __ldg(rn2f + rA);
                         }
-                        if (rB < N) {
+                        if (rB < rend) {
                             xb[u] = __ldg(reinterpret_cast<const float2 *>(X32 + rB * 8) + t);
                             rnB[u] = __ldg(rn2f + rB);
                         }
@@ -761,15 +951,18 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                         }
                     }
                 }
+                }
             } else {
-                for (int64_t wbase = tid - lane; wbase < N; wbase += 4 * (int64_t)blockDim.x) {
+                for (int ri = 0; ri < nrng; ri++) {
+                const int64_t ra = rng_a[ri], rend = rng_b[ri];
+                for (int64_t wbase = ra + tid - lane; wbase < rend; wbase += 4 * (int64_t)blockDim.x) {
                     const int64_t base = wbase + lane;
                     float xf[4][P ? P : LAGP_PMAX];
                     float rn[4];
     #pragma unroll
                     for (int u = 0; u < 4; u++) {
                         const int64_t r = base + u * (int64_t)blockDim.x;
-                        if (r < N) {
+                        if (r < rend) {
                             load_row32<P>(X32, r, p, xf[u]);
                             rn[u] = __ldg(rn2f + r);
                         } else {
@@ -810,6 +1003,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                         }
                     }
                 }
+                }
             }
             if (lane < NN_Q) {
                 s.wcnt[wid][lane] = wcr;
@@ -838,7 +1032,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                     if (t < tot) {
                         int w = 0, off = t;
                         while (off >= s.wcnt[w][q]) { off -= s.wcnt[w][q]; w++; }
-                        r = bufi[q * bufcap + w * segcap + off];
+                        r = __ldg(perm + bufi[q * bufcap + w * segcap + off]);  // stored position -> row of X
                         double xr[P ? P : LAGP_PMAX];
                         load_row<P>(X, r, p, xr);
                         d2 = row_d2<P>(xr, s.qx[q], p);
@@ -889,7 +1083,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
         // ---- per-query exact selection and output
         for (int q = 0; q < nq; q++) {
             int c;
-            int32_t *po = pool_out + (q0 + q) * (int64_t)Nprime;
+            int32_t *po = pool_out + (int64_t)s.qid[q] * Nprime;
             uint64_t *qk = bufk + (size_t)q * bufcap;
             int32_t *qi = bufc + (size_t)q * bufcap;
             if (s.state[q] == 2) {
@@ -915,7 +1109,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 bitonic_sort(s, npow);
                 for (int t = tid; t < Nprime; t += blockDim.x) {
                     po[t] = s.idx[t];
-                    if (d2_out) d2_out[(q0 + q) * (int64_t)Nprime + t] = __longlong_as_double((long long)s.key[t]);
+                    if (d2_out) d2_out[(int64_t)s.qid[q] * Nprime + t] = __longlong_as_double((long long)s.key[t]);
                 }
                 __syncthreads();
             } else {
@@ -936,19 +1130,62 @@ static int nn_bufcap(int Nprime, bool sorted) {
     return c;
 }
 
+// Cell grid (see nn_cell_of): gx x gy cells on coordinates 0 and 1, ~64 rows per
+// cell; gx <= 128 when gy > 1 (the filter loads one run per cell column in parallel)
+static void nn_cells(int64_t N, int p, int *gx, int *gy) {
+    const char *ev = getenv("LAGP_NN_CELLS");  // A/B: 0 = one cell (no pruning)
+    if (ev && ev[0] == '0') {
+        *gx = 1;
+        *gy = 1;
+    } else if (p == 1) {
+        int64_t g = N / 64;
+        *gx = (int)(g < 1 ? 1 : (g > 16384 ? 16384 : g));
+        *gy = 1;
+    } else {
+        int g = (int)sqrt((double)N / 64.0);
+        g = g < 1 ? 1 : (g > 128 ? 128 : g);
+        *gx = g;
+        *gy = g;
+    }
+}
+
 // Workspace layout: [maxn2 bits, per-dimension min / max keys (512 B)] [X32: N*p floats] [rn2f: N floats]
+// [perm: N] [cell counts, starts (C+1), cursors] for the rows and again for the queries [qperm: Mmax]
 // [compacted rows] [survivor keys] [filter rows], the last three bufcap per query
-size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime, bool sorted) {
+struct NNLayout {
+    size_t x32, rn2f, perm, rcnt, rstart, rcur, qcnt, qstart, qcur, qperm, rest;
+    int gx, gy;
+};
+static inline size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
+static NNLayout nn_layout(int64_t N, int p, int64_t Mmax) {
+    NNLayout L;
+    nn_cells(N, p, &L.gx, &L.gy);
+    const size_t C = (size_t)L.gx * L.gy;
+    size_t o = 512;
+    L.x32 = o; o += al256((size_t)N * p * sizeof(float));
+    L.rn2f = o; o += al256((size_t)N * sizeof(float));
+    L.perm = o; o += al256((size_t)N * sizeof(int32_t));
+    L.rcnt = o; o += al256(C * sizeof(int32_t));
+    L.rstart = o; o += al256((C + 1) * sizeof(int32_t));
+    L.rcur = o; o += al256(C * sizeof(int32_t));
+    L.qcnt = o; o += al256(C * sizeof(int32_t));
+    L.qstart = o; o += al256((C + 1) * sizeof(int32_t));
+    L.qcur = o; o += al256(C * sizeof(int32_t));
+    L.qperm = o; o += al256((size_t)(Mmax > 0 ? Mmax : 1) * sizeof(int32_t));
+    L.rest = o;
+    return L;
+}
+size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime, bool sorted, int64_t Mmax) {
     const size_t bc = (size_t)nn_bufcap(Nprime, sorted);
-    return 512 + (((size_t)N * p * sizeof(float) + 255) & ~(size_t)255) + (((size_t)N * sizeof(float) + 255) & ~(size_t)255) +
-           (size_t)grid * NN_Q * bc * (sizeof(uint64_t) + 2 * sizeof(int32_t)) + 256;
+    return nn_layout(N, p, Mmax).rest + (size_t)grid * NN_Q * bc * (sizeof(uint64_t) + 2 * sizeof(int32_t)) + 256;
 }
 
 template <int P, bool MMA>
 static cudaError_t launch_nn_t(const double *X, const float *X32, const float *rn2f, const unsigned long long *mx,
                                const unsigned long long *kmin, const unsigned long long *kmax, int64_t N, int p,
                                const double *XX, int64_t M, int Nprime, int n0, int sorted, int32_t *pool, double *d2,
-                               char *w, int grid, int *fb, cudaStream_t st) {
+                               char *w, int grid, int *fb, cudaStream_t st, int gx, int gy, const int32_t *cstart,
+                               const int32_t *perm, const int32_t *qperm) {
     size_t smem = sizeof(NNSmem);
     cudaError_t e = cudaFuncSetAttribute(nn_pool_kernel<P, MMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -959,7 +1196,7 @@ static cudaError_t launch_nn_t(const double *X, const float *X32, const float *r
     w += (size_t)grid * NN_Q * bc * sizeof(uint64_t);
     int32_t *bi = (int32_t *)w;
     nn_pool_kernel<P, MMA><<<grid, NN_THREADS, smem, st>>>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, bc, sorted,
-                                                      pool, d2, bcmp, bk, bi, fb);
+                                                      pool, d2, bcmp, bk, bi, fb, gx, gy, cstart, perm, qperm);
     return cudaGetLastError();
 }
 
@@ -973,49 +1210,75 @@ int nn_grid(int64_t M, int num_sms, int Nprime) {
     return (int)(groups < g ? (groups > 0 ? groups : 1) : g);
 }
 
-// Two launches: the FP32 copy / max row norm (prep), then the pool kernel.
-// With prepared = true the prep results already in `ws` are reused (chunked calls).
-cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64_t M, int Nprime, int n0, bool sorted,
-                      int32_t *pool, double *d2, void *ws, int grid, int *fb, cudaStream_t st, bool prepared,
+// Launches: rows (first chunk only) = bounds, cell histogram, scan, FP32 copy in cell
+// order; queries (every chunk) = cell histogram, scan, scatter; then the pool kernel.
+// With prepared = true the row results already in `ws` are reused (chunked calls;
+// the layout is the same for every chunk: Mmax fixed by the caller).
+cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64_t M, int64_t Mmax, int Nprime, int n0,
+                      bool sorted, int32_t *pool, double *d2, void *ws, int grid, int *fb, cudaStream_t st, bool prepared,
                       int *launches) {
+    if (M > Mmax) return cudaErrorInvalidValue;
     char *w = (char *)ws;
+    const NNLayout L = nn_layout(N, p, Mmax);
+    const int C = L.gx * L.gy;
     unsigned long long *mx = (unsigned long long *)w;
     unsigned long long *kmin = mx + 1, *kmax = mx + 1 + LAGP_PMAX;  // 8 + 2*16*8 = 264 <= 512 B
-    float *X32 = (float *)(w + 512);
-    float *rn2f = (float *)(w + 512 + (((size_t)N * p * sizeof(float) + 255) & ~(size_t)255));
-    char *rest = (char *)rn2f + (((size_t)N * sizeof(float) + 255) & ~(size_t)255);
+    float *X32 = (float *)(w + L.x32);
+    float *rn2f = (float *)(w + L.rn2f);
+    int32_t *perm = (int32_t *)(w + L.perm), *rcnt = (int32_t *)(w + L.rcnt), *rstart = (int32_t *)(w + L.rstart),
+            *rcur = (int32_t *)(w + L.rcur), *qcnt = (int32_t *)(w + L.qcnt), *qstart = (int32_t *)(w + L.qstart),
+            *qcur = (int32_t *)(w + L.qcur), *qperm = (int32_t *)(w + L.qperm);
+    char *rest = w + L.rest;
+    cudaError_t e;
     if (!prepared) {
-        cudaError_t e = cudaMemsetAsync(mx, 0, sizeof(unsigned long long) * (1 + LAGP_PMAX), st);  // maxn2, kmin
+        e = cudaMemsetAsync(mx, 0, sizeof(unsigned long long) * (1 + LAGP_PMAX), st);  // maxn2, kmin
         if (e != cudaSuccess) return e;
         e = cudaMemsetAsync(kmin, 0xff, sizeof(unsigned long long) * LAGP_PMAX, st);
         if (e != cudaSuccess) return e;
         e = cudaMemsetAsync(kmax, 0, sizeof(unsigned long long) * LAGP_PMAX, st);
         if (e != cudaSuccess) return e;
+        e = cudaMemsetAsync(rcnt, 0, sizeof(int32_t) * C, st);
+        if (e != cudaSuccess) return e;
         int blocks = (int)((N + 255) / 256);
         if (blocks > 4096) blocks = 4096;
         nn_bounds_kernel<<<blocks < 592 ? blocks : 592, 256, 0, st>>>(X, N, p, kmin, kmax);
+        nn_cell_hist_kernel<<<blocks, 256, 0, st>>>(X, N, p, kmin, kmax, L.gx, L.gy, rcnt);
+        nn_cell_scan_kernel<<<1, 1024, 0, st>>>(rcnt, C, rstart, rcur);
+        nn_prep_kernel<<<blocks, 256, 0, st>>>(X, N, p, X32, rn2f, mx, kmin, kmax, L.gx, L.gy, rcur, perm);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        nn_prep_kernel<<<blocks, 256, 0, st>>>(X, N, p, X32, rn2f, mx, kmin, kmax);
+        if (launches) (*launches) += 4;
+    }
+    {
+        e = cudaMemsetAsync(qcnt, 0, sizeof(int32_t) * C, st);
+        if (e != cudaSuccess) return e;
+        int blocks = (int)((M + 255) / 256);
+        if (blocks > 4096) blocks = 4096;
+        if (blocks < 1) blocks = 1;
+        nn_cell_hist_kernel<<<blocks, 256, 0, st>>>(XX, M, p, kmin, kmax, L.gx, L.gy, qcnt);
+        nn_cell_scan_kernel<<<1, 1024, 0, st>>>(qcnt, C, qstart, qcur);
+        nn_cell_scatter_kernel<<<blocks, 256, 0, st>>>(XX, M, p, kmin, kmax, L.gx, L.gy, qcur, qperm);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        if (launches) (*launches) += 2;
+        if (launches) (*launches) += 3;
     }
     if (launches) (*launches)++;
+#define NN_ARGS X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st, L.gx, L.gy, rstart, perm, qperm
     switch (p) {
-        case 1: return launch_nn_t<1, false>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        case 2: return launch_nn_t<2, false>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        case 3: return launch_nn_t<3, false>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-        case 4: return launch_nn_t<4, false>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        case 1: return launch_nn_t<1, false>(NN_ARGS);
+        case 2: return launch_nn_t<2, false>(NN_ARGS);
+        case 3: return launch_nn_t<3, false>(NN_ARGS);
+        case 4: return launch_nn_t<4, false>(NN_ARGS);
         case 8: {
             // tensor-core filter when survivors are rare (~1.5 N'/N of the pairs pass)
             const char *ev = getenv("LAGP_NN_MMA");
             const bool mma = ev ? ev[0] == '1' : (double)Nprime <= 0.004 * (double)N;
-            if (mma) return launch_nn_t<8, true>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
-            return launch_nn_t<8, false>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+            if (mma) return launch_nn_t<8, true>(NN_ARGS);
+            return launch_nn_t<8, false>(NN_ARGS);
         }
-        default: return launch_nn_t<0, false>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st);
+        default: return launch_nn_t<0, false>(NN_ARGS);
     }
+#undef NN_ARGS
 }
 
 }  // namespace lagp

@@ -47,6 +47,41 @@ def test_nn_pool_bit_exact(torch_dev, lagp, name, M, N, Nprime):
         assert np.array_equal(d2[i], rd2)
 
 
+def _cell_cases():
+    """Inputs that stress the filter's spatial cells (nn.cu nn_cell_of): a constant
+    cell axis (zero-width box), half the rows in one tight cluster (one crowded cell),
+    queries far outside the bounding box of X, heavy exact ties on the cell axes,
+    and the 1-d grid."""
+    rng = np.random.default_rng(77)
+    out = []
+    X = rng.random((30000, 3)); X[:, 0] = 0.25                       # constant axis 0
+    out.append(("const_axis0", X, rng.random((40, 3))))
+    X = rng.random((30000, 2)); X[:15000] = 0.5 + 1e-7 * rng.standard_normal((15000, 2))  # one crowded cell
+    out.append(("cluster", X, np.vstack([rng.random((30, 2)), np.full((2, 2), 0.5)])))
+    X = rng.random((20000, 4))
+    out.append(("far_queries", X, np.vstack([rng.random((8, 4)) * 10 - 5, [[3.0, -2.0, 0.5, 0.5]]])))
+    X = np.floor(rng.random((25000, 2)) * 40) / 40                     # grid: exact ties everywhere
+    out.append(("ties_grid", X, np.floor(rng.random((24, 2)) * 40) / 40))
+    X = rng.random((50000, 1))
+    out.append(("p1", X, rng.random((20, 1))))
+    X = rng.standard_normal((40000, 5)) * [1e3, 1e-3, 1, 1, 1]         # very unequal axis scales
+    out.append(("scales", X, rng.standard_normal((20, 5)) * [1e3, 1e-3, 1, 1, 1]))
+    return out
+
+
+@pytest.mark.parametrize("case", range(6))
+@pytest.mark.parametrize("Nprime", [1, 700])
+def test_nn_pool_cells_bit_exact(torch_dev, lagp, case, Nprime):
+    torch, dev = torch_dev
+    name, X, XX = _cell_cases()[case]
+    pool, d2 = lagp.nn_pool(T(torch, dev, X), T(torch, dev, XX), Nprime, with_d2=True)
+    pool, d2 = pool.cpu().numpy(), d2.cpu().numpy()
+    for i in range(XX.shape[0]):
+        ref, rd2 = oracle.nn(X, XX[i], Nprime)
+        assert np.array_equal(pool[i], ref), (name, i, np.where(pool[i] != ref)[0][:5])
+        assert np.array_equal(d2[i], rd2), name
+
+
 def test_nn_pool_massive_ties_fallback(torch_dev, lagp):
     """Every row at the same distance -> threshold filter cannot split; the exact
     radix-select fallback must return the lowest indices."""
