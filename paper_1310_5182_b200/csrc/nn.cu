@@ -665,11 +665,11 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                int sorted, int32_t *__restrict__ pool_out, double *__restrict__ d2_out, int32_t *__restrict__ bufc_ws,
                uint64_t *__restrict__ bufk_ws, int32_t *__restrict__ bufi_ws, int *__restrict__ fallback_count, int gx,
                int gy, const int32_t *__restrict__ cstart, const int32_t *__restrict__ perm,
-               const int32_t *__restrict__ qperm) {
+               const int32_t *__restrict__ qperm, int qg) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     NNSmem &s = *reinterpret_cast<NNSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-    const int64_t ngroups = (M + NN_Q - 1) / NN_Q;
+    const int64_t ngroups = (M + qg - 1) / qg;  // qg = 8 or 16 query locations per group
     // sample sizes and target ranks (see the threshold phase)
     const int S1 = (int)(N < 1024 ? N : 1024);
     int64_t s2 = (int64_t)64 * N / (Nprime > 0 ? Nprime : 1);
@@ -690,8 +690,8 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
     const double u32 = 5.9604644775390625e-08;  // 2^-24, FP32 unit roundoff
 
     for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-        const int64_t q0 = grp * NN_Q;
-        const int nq = (int)((M - q0) < NN_Q ? (M - q0) : NN_Q);
+        const int64_t q0 = grp * qg;
+        const int nq = (int)((M - q0) < qg ? (M - q0) : qg);
         if (tid < NN_Q) s.qid[tid] = tid < nq ? (qperm ? qperm[q0 + tid] : (int32_t)(q0 + tid)) : 0;
         __syncthreads();
         for (int e = tid; e < NN_Q * LAGP_PMAX; e += blockDim.x) {
@@ -722,7 +722,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
         //     ~1.5 N' expected survivors under tau (relative spread ~1/sqrt(r2) = 10 %).
         {
             float *t1 = reinterpret_cast<float *>(s.key);  // NN_Q x 1024 floats (64 KB)
-            for (int e = tid; e < NN_Q * S1; e += blockDim.x) {
+            for (int e = tid; e < nq * S1; e += blockDim.x) {
                 const int q = e / S1, t = e - q * S1;
                 const int64_t r = (int64_t)t * N / S1;
                 float xf[P ? P : LAGP_PMAX];
@@ -731,7 +731,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
             }
             __syncthreads();
             for (int q = wid; q < NN_Q; q += nw) {
-                const float tq = (r1 > S1) ? INFINITY : warp_quantile(t1 + q * 1024, S1, r1, s.whist[wid]);
+                const float tq = (q >= nq || r1 > S1) ? INFINITY : warp_quantile(t1 + q * 1024, S1, r1, s.whist[wid]);
                 if (lane == 0) {
                     s.tau[q] = (double)tq;
                     s.state[q] = q < nq ? 0 : 1;
@@ -747,6 +747,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                     load_row32<P>(X32, r, p, xf);
 #pragma unroll
                     for (int q = 0; q < NN_Q; q++) {
+                        if (q >= nq) break;  // uniform
                         const float d2f = row_d2f<P>(xf, s.nqf[q], p);
                         const bool hit = d2f <= (float)s.tau[q];
                         const unsigned m = __ballot_sync(__activemask(), hit);
@@ -772,7 +773,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 if (tid < NN_Q) s.tau[tid] = INFINITY;  // N' close to N: every row
                 __syncthreads();
             } else {  // S2 == S1: T1 already has the target resolution
-                for (int q = wid; q < NN_Q; q += nw) {
+                for (int q = wid; q < nq; q += nw) {
                     const float tq = warp_quantile(t1 + q * 1024, S1, r2 <= S1 ? r2 : S1, s.whist[wid]);
                     if (lane == 0) s.tau[q] = (double)tq;
                 }
@@ -972,7 +973,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                         }
                     }
     #pragma unroll 1
-                    for (int q = 0; q < NN_Q; q++) {  // inactive queries have thr = NaN: no candidates
+                    for (int q = 0; q < nq; q++) {  // inactive queries have thr = NaN: no candidates
                         float qv[P ? P : LAGP_PMAX];
     #pragma unroll
                         for (int k = 0; k < (P ? P : LAGP_PMAX); k++) qv[k] = s.qf[q][k];
@@ -1185,7 +1186,7 @@ static cudaError_t launch_nn_t(const double *X, const float *X32, const float *r
                                const unsigned long long *kmin, const unsigned long long *kmax, int64_t N, int p,
                                const double *XX, int64_t M, int Nprime, int n0, int sorted, int32_t *pool, double *d2,
                                char *w, int grid, int *fb, cudaStream_t st, int gx, int gy, const int32_t *cstart,
-                               const int32_t *perm, const int32_t *qperm) {
+                               const int32_t *perm, const int32_t *qperm, int qg) {
     size_t smem = sizeof(NNSmem);
     cudaError_t e = cudaFuncSetAttribute(nn_pool_kernel<P, MMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1196,12 +1197,28 @@ static cudaError_t launch_nn_t(const double *X, const float *X32, const float *r
     w += (size_t)grid * NN_Q * bc * sizeof(uint64_t);
     int32_t *bi = (int32_t *)w;
     nn_pool_kernel<P, MMA><<<grid, NN_THREADS, smem, st>>>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, bc, sorted,
-                                                      pool, d2, bcmp, bk, bi, fb, gx, gy, cstart, perm, qperm);
+                                                      pool, d2, bcmp, bk, bi, fb, gx, gy, cstart, perm, qperm, qg);
     return cudaGetLastError();
 }
 
+// Query locations per group: 16 or 8. The tensor-core filter always takes 16 (its
+// MMAs cover 2 x 8 queries; one 8-query group would idle half of them: C4 909 vs
+// 776 ms). The FFMA2 filter takes 8 when p <= 4 (measured C3: 62.6 vs 67.0 ms) or
+// when 8-groups fill the last round of the grid better (C2: 625 16-groups on 296
+// CTAs = 2.1 rounds, 1250 8-groups = 4.2 rounds; 2.71 vs 3.02 ms).
+// LAGP_NN_Q=8|16 overrides.
+static int nn_group_size(int64_t M, int grid, int p, bool mma) {
+    const char *ev = getenv("LAGP_NN_Q");
+    if (ev && (ev[0] == '8' || ev[0] == '1')) return ev[0] == '8' ? 8 : 16;
+    if (mma) return 16;
+    if (p <= 4) return 8;
+    const double g16 = (double)((M + 15) / 16) / grid, g8 = (double)((M + 7) / 8) / grid;
+    const double eff16 = g16 / ceil(g16), eff8 = g8 / ceil(g8);
+    return eff8 > 1.05 * eff16 ? 8 : 16;
+}
+
 int nn_grid(int64_t M, int num_sms, int Nprime) {
-    int64_t groups = (M + NN_Q - 1) / NN_Q;
+    int64_t groups = (M + 7) / 8;  // 8-query groups at the smallest (nn_group_size)
     int64_t g = 2LL * num_sms;  // 2 CTAs/SM fit (~110 KB smem each)
     // keep the survivor buffers under ~2 GiB for large pools
     const int64_t per_cta = (int64_t)NN_Q * nn_bufcap(Nprime, false) * 16;
@@ -1263,7 +1280,10 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
         if (launches) (*launches) += 3;
     }
     if (launches) (*launches)++;
-#define NN_ARGS X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st, L.gx, L.gy, rstart, perm, qperm
+    const char *evm = getenv("LAGP_NN_MMA");
+    const bool mma = p == 8 && (evm ? evm[0] == '1' : (double)Nprime <= 0.004 * (double)N);
+    const int qg = nn_group_size(M, grid, p, mma);
+#define NN_ARGS X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st, L.gx, L.gy, rstart, perm, qperm, qg
     switch (p) {
         case 1: return launch_nn_t<1, false>(NN_ARGS);
         case 2: return launch_nn_t<2, false>(NN_ARGS);
@@ -1271,8 +1291,6 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
         case 4: return launch_nn_t<4, false>(NN_ARGS);
         case 8: {
             // tensor-core filter when survivors are rare (~1.5 N'/N of the pairs pass)
-            const char *ev = getenv("LAGP_NN_MMA");
-            const bool mma = ev ? ev[0] == '1' : (double)Nprime <= 0.004 * (double)N;
             if (mma) return launch_nn_t<8, true>(NN_ARGS);
             return launch_nn_t<8, false>(NN_ARGS);
         }
