@@ -741,22 +741,48 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
             __syncthreads();
             if (S2 > S1 && r2 <= S2) {
                 float *lst = reinterpret_cast<float *>(bufk);  // per query bufcap floats
-                for (int64_t t = tid; t < S2; t += blockDim.x) {
-                    const int64_t r = t * N / S2;
-                    float xf[P ? P : LAGP_PMAX];
-                    load_row32<P>(X32, r, p, xf);
+                const double step2 = (double)N / (double)S2;
+                // 4 sample rows per thread per pass, each query's coordinates read from
+                // shared memory once per 4 rows (as in the filter pass)
+                for (int64_t wb = (int64_t)wid * 128; wb < S2; wb += (int64_t)nw * 128) {
+                    float xf[4][P ? P : LAGP_PMAX];
+                    bool ok[4];
 #pragma unroll
-                    for (int q = 0; q < NN_Q; q++) {
-                        if (q >= nq) break;  // uniform
-                        const float d2f = row_d2f<P>(xf, s.nqf[q], p);
-                        const bool hit = d2f <= (float)s.tau[q];
-                        const unsigned m = __ballot_sync(__activemask(), hit);
-                        if (m) {  // one shared atomic per warp and query
-                            const int leader = __ffs(m) - 1;
+                    for (int u = 0; u < 4; u++) {
+                        const int64_t t = wb + 32 * u + lane;
+                        ok[u] = t < S2;
+                        if (ok[u]) {
+                            int64_t r = (int64_t)((double)t * step2);  // strided sample row (no 64-bit division)
+                            load_row32<P>(X32, r < N ? r : N - 1, p, xf[u]);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < (P ? P : LAGP_PMAX); k++) xf[u][k] = 0.f;
+                        }
+                    }
+#pragma unroll 1
+                    for (int q = 0; q < nq; q++) {
+                        float qv[P ? P : LAGP_PMAX];
+#pragma unroll
+                        for (int k = 0; k < (P ? P : LAGP_PMAX); k++) qv[k] = s.nqf[q][k];
+                        const float tq = (float)s.tau[q];
+                        float d2f[4];
+                        unsigned m[4];
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            d2f[u] = row_d2f<P>(xf[u], qv, p);
+                            m[u] = __ballot_sync(0xffffffffu, ok[u] && d2f[u] <= tq);
+                        }
+                        if (m[0] | m[1] | m[2] | m[3]) {  // one shared atomic per warp and query
                             int pos = 0;
-                            if (lane == leader) pos = atomicAdd(&s.cnt[q], __popc(m));
-                            pos = __shfl_sync(__activemask(), pos, leader) + __popc(m & ((1u << lane) - 1u));
-                            if (hit && pos < bufcap) lst[(size_t)q * bufcap + pos] = d2f;
+                            if (lane == 0) pos = atomicAdd(&s.cnt[q], __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]));
+                            pos = __shfl_sync(0xffffffffu, pos, 0);
+                            const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+                            for (int u = 0; u < 4; u++) {
+                                const int pu = pos + __popc(m[u] & lt);
+                                if (((m[u] >> lane) & 1u) && pu < bufcap) lst[(size_t)q * bufcap + pu] = d2f[u];
+                                pos += __popc(m[u]);
+                            }
                         }
                     }
                 }
