@@ -722,12 +722,13 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
         //     ~1.5 N' expected survivors under tau (relative spread ~1/sqrt(r2) = 10 %).
         {
             float *t1 = reinterpret_cast<float *>(s.key);  // NN_Q x 1024 floats (64 KB)
-            for (int e = tid; e < nq * S1; e += blockDim.x) {
-                const int q = e / S1, t = e - q * S1;
-                const int64_t r = (int64_t)t * N / S1;
+            const double step1 = (double)N / (double)S1;
+            for (int t = tid; t < S1; t += blockDim.x) {  // each sample row loaded once for all queries
+                int64_t r = (int64_t)((double)t * step1);
                 float xf[P ? P : LAGP_PMAX];
-                load_row32<P>(X32, r, p, xf);
-                t1[q * 1024 + t] = row_d2f<P>(xf, s.nqf[q], p);
+                load_row32<P>(X32, r < N ? r : N - 1, p, xf);
+#pragma unroll 1
+                for (int q = 0; q < nq; q++) t1[q * 1024 + t] = row_d2f<P>(xf, s.nqf[q], p);
             }
             __syncthreads();
             for (int q = wid; q < NN_Q; q += nw) {
