@@ -1285,7 +1285,8 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
         if (e != cudaSuccess) return e;
         int blocks = (int)((N + 255) / 256);
         if (blocks > 4096) blocks = 4096;
-        nn_bounds_kernel<<<blocks < 592 ? blocks : 592, 256, 0, st>>>(X, N, p, kmin, kmax);
+        // few blocks: every block ends in 2p same-address global atomics (592 blocks: 32 us)
+        nn_bounds_kernel<<<blocks < 148 ? blocks : 148, 256, 0, st>>>(X, N, p, kmin, kmax);
         nn_cell_hist_kernel<<<blocks, 256, 0, st>>>(X, N, p, kmin, kmax, L.gx, L.gy, rcnt);
         nn_cell_scan_kernel<<<1, 1024, 0, st>>>(rcnt, C, rstart, rcur);
         nn_prep_kernel<<<blocks, 256, 0, st>>>(X, N, p, X32, rn2f, mx, kmin, kmax, L.gx, L.gy, rcur, perm);
