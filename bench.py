@@ -183,7 +183,7 @@ def run_reference(args):
     t0 = time.perf_counter()
     oracle.alc_batch(cfg["X"], cfg["Z"], cfg["XX"][:1], *a, threads=1)
     t1 = time.perf_counter() - t0
-    per_step_budget = max(2.0, 90.0 / max(1, args.steps + args.warmup))
+    per_step_budget = max(min(2.0, args.ref_budget), args.ref_budget / max(1, args.steps + args.warmup))
     S = int(min(cfg["XX"].shape[0], max(cores, per_step_budget * cores / max(t1, 1e-4))))
     times = []
     for it in range(args.warmup + args.steps):
@@ -239,6 +239,8 @@ def main():
     ap.add_argument("--no-two-stage", action="store_true",
                     help="skip the Fig 1 two-stage (design, local MLE, design, MLE, predict) timing")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=90.0,
+                    help="--impl reference: host seconds for the whole warmup + timed run (bounded samples)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
