@@ -65,28 +65,76 @@ __device__ bool mle_chol(const double *D, double *L, int n, double rth, double e
     __shared__ int bad;
     if (tid == 0) bad = 0;
     __syncthreads();
-    // column k: every thread takes 1/sqrt(L_kk) itself; the trailing update uses the
-    // unscaled column times that factor, and column k is scaled one step later
-    // (no conflict: step k+1 touches columns >= k+1 only)
-    for (int k = 0; k < n; k++) {
+    // Two columns (k, k+1) per barrier. Every thread forms the pair's factors itself:
+    // 1/sqrt(L_kk), l_{k+1,k} = L_{k+1,k}/sqrt(L_kk), the updated pivot
+    // d = L_{k+1,k+1} - l_{k+1,k}^2 and 1/sqrt(d); each row then gets its two column
+    // values on the fly and the trailing block its rank-2 update. The arithmetic is
+    // the one-column-per-step right-looking order operation for operation (the same
+    // fmas, products and reciprocal square roots), so the factor is bitwise the same.
+    // The pair's columns are written one step later (no thread reads them then).
+    const int lane = tid & 31, nw = blockDim.x >> 5;
+    int kp = -1;
+    bool ptwo = false;
+    double prl = 0.0, pc10 = 0.0, prl2 = 0.0, pd2 = 0.0;
+    for (int k = 0; k < n; k += 2) {
+        const bool two = k + 1 < n;
         const double dkk = L[k * n + k];
         if (!(dkk > 0.0)) {
             if (tid == 0) bad = 1;
             break;  // uniform: every thread read the same pivot
         }
         const double rl = rsqrt_nr(dkk);  // 1/sqrt(L_kk), seed + Newton (dkk > 0 here)
-        if (k > 0) {  // scale column k-1 (its pivot is settled)
-            const double rp = rsqrt_nr(L[(k - 1) * n + (k - 1)]);
-            for (int i = k + tid; i < n; i += blockDim.x) L[i * n + (k - 1)] *= rp;
+        double c10 = 0.0, d2 = 0.0, rl2 = 0.0;
+        if (two) {
+            c10 = L[(k + 1) * n + k] * rl;
+            d2 = fma(-c10, c10, L[(k + 1) * n + (k + 1)]);
+            if (!(d2 > 0.0)) {
+                if (tid == 0) bad = 1;
+                break;  // uniform
+            }
+            rl2 = rsqrt_nr(d2);
+        }
+        if (kp >= 0) {  // the previous pair's columns, rows >= k
+            for (int i = k + tid; i < n; i += blockDim.x) {
+                const double lik = L[i * n + kp] * prl;
+                L[i * n + kp] = lik;
+                if (ptwo) L[i * n + kp + 1] = fma(-lik, pc10, L[i * n + kp + 1]) * prl2;
+            }
+            if (tid == 0 && ptwo) {
+                L[(kp + 1) * n + kp] = pc10;
+                L[(kp + 1) * n + kp + 1] = pd2;
+            }
         }
         // trailing update: rows to warps, columns to lanes (no index division)
-        const int lane = tid & 31, nw = blockDim.x >> 5;
-        for (int i = k + 1 + (tid >> 5); i < n; i += nw) {
-            const double li = L[i * n + k] * rl;
-            for (int jj = k + 1 + lane; jj <= i; jj += 32)
-                L[i * n + jj] = fma(-li, L[jj * n + k] * rl, L[i * n + jj]);
+        const int j0 = k + (two ? 2 : 1);
+        for (int i = j0 + (tid >> 5); i < n; i += nw) {
+            const double lik = L[i * n + k] * rl;
+            const double lik1 = two ? fma(-lik, c10, L[i * n + k + 1]) * rl2 : 0.0;
+            for (int jj = j0 + lane; jj <= i; jj += 32) {
+                const double ljk = L[jj * n + k] * rl;
+                double v = fma(-lik, ljk, L[i * n + jj]);
+                if (two) v = fma(-lik1, fma(-ljk, c10, L[jj * n + k + 1]) * rl2, v);
+                L[i * n + jj] = v;
+            }
         }
         __syncthreads();
+        kp = k;
+        ptwo = two;
+        prl = rl;
+        pc10 = c10;
+        prl2 = rl2;
+        pd2 = d2;
+    }
+    if (kp >= 0) {  // the last pair (after a failed pivot: the pair before it, harmless)
+        for (int i = kp + 2 + tid; i < n; i += blockDim.x) {
+            const double lik = L[i * n + kp] * prl;
+            L[i * n + kp] = lik;
+            if (ptwo) L[i * n + kp + 1] = fma(-lik, pc10, L[i * n + kp + 1]) * prl2;
+        }
+        if (tid == 0 && ptwo) {
+            L[(kp + 1) * n + kp] = pc10;
+            L[(kp + 1) * n + kp + 1] = pd2;
+        }
     }
     __syncthreads();
     if (bad) return false;
