@@ -162,8 +162,16 @@ __device__ void mle_inverse(const double *L, double *W, double *A, int n) {
         for (int i = sub; i < c; i += 4) W[i * n + c] = 0.0;
         W[c * n + c] = A[c];
         for (int i = c + 1; i < n; i++) {
-            double s = 0.0;
-            for (int t = c + sub; t < i; t += 4) s = fma(L[i * n + t], W[t * n + c], s);
+            // two accumulators, pointer steps (the column-0 chain is the critical path)
+            double s = 0.0, s1 = 0.0;
+            const double *pl = L + i * n + c + sub, *pw = W + (c + sub) * n + c;
+            int t = c + sub;
+            for (; t + 4 < i; t += 8, pl += 8, pw += 8 * n) {
+                s = fma(pl[0], pw[0], s);
+                s1 = fma(pl[4], pw[4 * n], s1);
+            }
+            if (t < i) s = fma(pl[0], pw[0], s);
+            s += s1;
             s += __shfl_xor_sync(qmask, s, 1);
             s += __shfl_xor_sync(qmask, s, 2);
             W[i * n + c] = -s * A[i];
@@ -174,8 +182,15 @@ __device__ void mle_inverse(const double *L, double *W, double *A, int n) {
     const int lane = tid & 31, nw = blockDim.x >> 5;
     for (int a = tid >> 5; a < n; a += nw)
         for (int b = lane; b <= a; b += 32) {
-            double s = 0.0;
-            for (int t = a; t < n; t++) s = fma(W[t * n + a], W[t * n + b], s);
+            double s = 0.0, s1 = 0.0;
+            const double *pa = W + a * n + a, *pb = W + a * n + b;
+            int t = a;
+            for (; t + 1 < n; t += 2, pa += 2 * n, pb += 2 * n) {
+                s = fma(pa[0], pb[0], s);
+                s1 = fma(pa[n], pb[n], s1);
+            }
+            if (t < n) s = fma(pa[0], pb[0], s);
+            s += s1;
             A[a * n + b] = s;
             A[b * n + a] = s;
         }
@@ -286,7 +301,7 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, const double *D, doub
     return r;
 }
 
-__global__ void __launch_bounds__(MLE_THREADS)
+__global__ void __launch_bounds__(MLE_THREADS, 2)
 mle_kernel(MleArgs A) {
     extern __shared__ __align__(16) double sm[];
     const int n = A.n, p = A.p;
