@@ -243,22 +243,23 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, const double *D, doub
         const int lane = tid & 31, nw = blockDim.x >> 5;
         for (int a = 2 * (tid >> 5); a < n; a += 2 * nw) {
             const bool two = a + 1 < n;
+            // the second row repeats the first when there is none (no branch in the loop)
+            const double *pa = A + a * n, *pa1 = A + (two ? a + 1 : a) * n;
             for (int b = lane; b < n; b += 32) {
                 double s0 = 0.0, s1 = 0.0, u0 = 0.0, u1 = 0.0;
+                const double *pl = L + b;
                 int t = 0;
-                for (; t + 1 < n; t += 2) {
-                    const double p0 = L[t * n + b], p1 = L[(t + 1) * n + b];
-                    s0 = fma(A[a * n + t], p0, s0);
-                    s1 = fma(A[a * n + t + 1], p1, s1);
-                    if (two) {
-                        u0 = fma(A[(a + 1) * n + t], p0, u0);
-                        u1 = fma(A[(a + 1) * n + t + 1], p1, u1);
-                    }
+                for (; t + 1 < n; t += 2, pl += 2 * n) {
+                    const double p0 = pl[0], p1 = pl[n];
+                    s0 = fma(pa[t], p0, s0);
+                    s1 = fma(pa[t + 1], p1, s1);
+                    u0 = fma(pa1[t], p0, u0);
+                    u1 = fma(pa1[t + 1], p1, u1);
                 }
                 if (t < n) {
-                    const double p0 = L[t * n + b];
-                    s0 = fma(A[a * n + t], p0, s0);
-                    if (two) u0 = fma(A[(a + 1) * n + t], p0, u0);
+                    const double p0 = pl[0];
+                    s0 = fma(pa[t], p0, s0);
+                    u0 = fma(pa1[t], p0, u0);
                 }
                 W[a * n + b] = s0 + s1;
                 if (two) W[(a + 1) * n + b] = u0 + u1;
