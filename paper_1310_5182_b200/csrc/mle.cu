@@ -156,12 +156,17 @@ __device__ void mle_inverse(const double *L, double *W, double *A, int n) {
     // 1/L_ii first (keeps the divisions off the substitution chains)
     for (int i = tid; i < n; i += blockDim.x) A[i] = 1.0 / L[i * n + i];
     __syncthreads();
+    // 2x2 block form: L = [L11 0; L21 L22] -> W11 = L11^-1 and W22 = L22^-1 by the
+    // substitution below at the same time (half the longest chain), then
+    // W21 = -W22 (L21 W11) by two short parallel products
+    const int h = n >= 24 ? n / 2 : n;
     const int sub = tid & 3;
     const unsigned qmask = 0xfu << (tid & 28);
     for (int c = tid >> 2; c < n; c += blockDim.x >> 2) {
         for (int i = sub; i < c; i += 4) W[i * n + c] = 0.0;
         W[c * n + c] = A[c];
-        for (int i = c + 1; i < n; i++) {
+        const int iend = c < h ? h : n;
+        for (int i = c + 1; i < iend; i++) {
             // two accumulators, pointer steps (the column-0 chain is the critical path)
             double s = 0.0, s1 = 0.0;
             const double *pl = L + i * n + c + sub, *pw = W + (c + sub) * n + c;
@@ -178,6 +183,36 @@ __device__ void mle_inverse(const double *L, double *W, double *A, int n) {
         }
     }
     __syncthreads();
+    if (h < n) {
+        // T = L21 W11 ((n-h) x h, in A's storage past the 1/L_ii entries; A is free until W^T W)
+        double *T = A + n;
+        const int m21 = (n - h) * h;
+        for (int e = tid; e < m21; e += blockDim.x) {
+            const int i = h + e / h, c = e - (i - h) * h;
+            double s0 = 0.0, s1 = 0.0;
+            int t = c;
+            for (; t + 1 < h; t += 2) {
+                s0 = fma(L[i * n + t], W[t * n + c], s0);
+                s1 = fma(L[i * n + t + 1], W[(t + 1) * n + c], s1);
+            }
+            if (t < h) s0 = fma(L[i * n + t], W[t * n + c], s0);
+            T[e] = s0 + s1;
+        }
+        __syncthreads();
+        // W21 = -W22 T
+        for (int e = tid; e < m21; e += blockDim.x) {
+            const int i = h + e / h, c = e - (i - h) * h;
+            double s0 = 0.0, s1 = 0.0;
+            int u = h;
+            for (; u + 1 <= i; u += 2) {
+                s0 = fma(W[i * n + u], T[(u - h) * h + c], s0);
+                s1 = fma(W[i * n + u + 1], T[(u + 1 - h) * h + c], s1);
+            }
+            if (u <= i) s0 = fma(W[i * n + u], T[(u - h) * h + c], s0);
+            W[i * n + c] = -(s0 + s1);
+        }
+        __syncthreads();
+    }
     // A = W^T W: rows a to warps, columns b <= a to lanes
     const int lane = tid & 31, nw = blockDim.x >> 5;
     for (int a = tid >> 5; a < n; a += nw)
