@@ -272,32 +272,28 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, const double *D, doub
         L[e] = exp_nonpos(-q) * q;
     }
     __syncthreads();
-    // rows to warps, columns to lanes; two rows per warp pass and two accumulators
-    // per entry (four independent chains per thread)
+    // T = A P on the FP64 tensor path (mma.sync m8n8k4 f64, SASS DMMA): 8x8 output tiles
+    // to warps, k in steps of 4, zero-padded past n. Fragments (PTX ISA): A a = A[g][k],
+    // B b = B[k][g], C {c0, c1} = C[g][2k], C[g][2k+1], with g = lane>>2, k = lane&3.
     {
         const int lane = tid & 31, nw = blockDim.x >> 5;
-        for (int a = 2 * (tid >> 5); a < n; a += 2 * nw) {
-            const bool two = a + 1 < n;
-            // the second row repeats the first when there is none (no branch in the loop)
-            const double *pa = A + a * n, *pa1 = A + (two ? a + 1 : a) * n;
-            for (int b = lane; b < n; b += 32) {
-                double s0 = 0.0, s1 = 0.0, u0 = 0.0, u1 = 0.0;
-                const double *pl = L + b;
-                int t = 0;
-                for (; t + 1 < n; t += 2, pl += 2 * n) {
-                    const double p0 = pl[0], p1 = pl[n];
-                    s0 = fma(pa[t], p0, s0);
-                    s1 = fma(pa[t + 1], p1, s1);
-                    u0 = fma(pa1[t], p0, u0);
-                    u1 = fma(pa1[t + 1], p1, u1);
-                }
-                if (t < n) {
-                    const double p0 = pl[0];
-                    s0 = fma(pa[t], p0, s0);
-                    u0 = fma(pa1[t], p0, u0);
-                }
-                W[a * n + b] = s0 + s1;
-                if (two) W[(a + 1) * n + b] = u0 + u1;
+        const int g = lane >> 2, q = lane & 3, nt = (n + 7) >> 3;
+        for (int tile = tid >> 5; tile < nt * nt; tile += nw) {
+            const int a0 = (tile / nt) * 8, b0 = (tile - (tile / nt) * nt) * 8;
+            const int ar = a0 + g, bc = b0 + g;
+            double c0 = 0.0, c1 = 0.0;
+            for (int kk = 0; kk < n; kk += 4) {
+                const int k = kk + q;
+                const double av = (ar < n && k < n) ? A[ar * n + k] : 0.0;
+                const double bv = (k < n && bc < n) ? L[k * n + bc] : 0.0;
+                asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                    : "+d"(c0), "+d"(c1)
+                    : "d"(av), "d"(bv));
+            }
+            const int cc = b0 + 2 * q;
+            if (ar < n) {
+                if (cc < n) W[ar * n + cc] = c0;
+                if (cc + 1 < n) W[ar * n + cc + 1] = c1;
             }
         }
     }
