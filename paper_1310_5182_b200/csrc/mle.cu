@@ -213,22 +213,38 @@ __device__ void mle_inverse(const double *L, double *W, double *A, int n) {
         }
         __syncthreads();
     }
-    // A = W^T W: rows a to warps, columns b <= a to lanes
-    const int lane = tid & 31, nw = blockDim.x >> 5;
-    for (int a = tid >> 5; a < n; a += nw)
-        for (int b = lane; b <= a; b += 32) {
-            double s = 0.0, s1 = 0.0;
-            const double *pa = W + a * n + a, *pb = W + a * n + b;
-            int t = a;
-            for (; t + 1 < n; t += 2, pa += 2 * n, pb += 2 * n) {
-                s = fma(pa[0], pb[0], s);
-                s1 = fma(pa[n], pb[n], s1);
+    // A = W^T W on the FP64 tensor path (mma.sync m8n8k4 f64): the lower 8x8 tiles to
+    // warps, mirrored; W is lower triangular, so tile (a0, b0) sums t >= max(a0, b0) only
+    {
+        const int lane = tid & 31, nw = blockDim.x >> 5;
+        const int g = lane >> 2, q = lane & 3, nt = (n + 7) >> 3;
+        for (int tile = tid >> 5; tile < nt * (nt + 1) / 2; tile += nw) {
+            int ti = 0;
+            while ((ti + 1) * (ti + 2) / 2 <= tile) ti++;  // lower-triangle tile (ti, tj)
+            const int tj = tile - ti * (ti + 1) / 2;
+            const int a0 = ti * 8, b0 = tj * 8, ar = a0 + g, bc = b0 + g;
+            double c0 = 0.0, c1 = 0.0;
+            for (int kk = a0 & ~3; kk < n; kk += 4) {
+                const int t = kk + q;
+                const double av = (ar < n && t < n) ? W[t * n + ar] : 0.0;
+                const double bv = (bc < n && t < n) ? W[t * n + bc] : 0.0;
+                asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                    : "+d"(c0), "+d"(c1)
+                    : "d"(av), "d"(bv));
             }
-            if (t < n) s = fma(pa[0], pb[0], s);
-            s += s1;
-            A[a * n + b] = s;
-            A[b * n + a] = s;
+            const int cc = b0 + 2 * q;
+            if (ar < n) {
+                if (cc < n && (ti != tj || cc <= ar)) {
+                    A[ar * n + cc] = c0;
+                    A[cc * n + ar] = c0;
+                }
+                if (cc + 1 < n && (ti != tj || cc + 1 <= ar)) {
+                    A[ar * n + cc + 1] = c1;
+                    A[(cc + 1) * n + ar] = c1;
+                }
+            }
         }
+    }
     __syncthreads();
 }
 
