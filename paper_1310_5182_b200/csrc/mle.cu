@@ -165,6 +165,7 @@ __device__ void mle_inverse(const double *L, double *W, double *A, int n) {
     for (int c = tid >> 2; c < n; c += blockDim.x >> 2) {
         for (int i = sub; i < c; i += 4) W[i * n + c] = 0.0;
         W[c * n + c] = A[c];
+        __syncwarp(qmask);  // every lane of the quad wrote the same values; order them for the reads
         const int iend = c < h ? h : n;
         for (int i = c + 1; i < iend; i++) {
             // two accumulators, pointer steps (the column-0 chain is the critical path)
@@ -180,6 +181,7 @@ __device__ void mle_inverse(const double *L, double *W, double *A, int n) {
             s += __shfl_xor_sync(qmask, s, 1);
             s += __shfl_xor_sync(qmask, s, 2);
             W[i * n + c] = -s * A[i];
+            __syncwarp(qmask);
         }
     }
     __syncthreads();
