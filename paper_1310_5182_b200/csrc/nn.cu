@@ -1236,7 +1236,10 @@ static cudaError_t launch_nn_t(const double *X, const float *X32, const float *r
 // LAGP_NN_Q=8|16 overrides.
 static int nn_group_size(int64_t M, int grid, int p, bool mma) {
     const char *ev = getenv("LAGP_NN_Q");
-    if (ev && (ev[0] == '8' || ev[0] == '1')) return ev[0] == '8' ? 8 : 16;
+    if (ev) {  // A/B: 4, 8 or 16 (the tensor-core filter needs 16)
+        const int v = atoi(ev);
+        if ((v == 4 || v == 8 || v == 16) && !(mma && v != 16)) return v;
+    }
     if (mma) return 16;
     if (p <= 4) return 8;
     const double g16 = (double)((M + 15) / 16) / grid, g8 = (double)((M + 7) / 8) / grid;
