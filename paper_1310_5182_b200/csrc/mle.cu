@@ -186,32 +186,50 @@ __device__ void mle_inverse(const double *L, double *W, double *A, int n) {
     }
     __syncthreads();
     if (h < n) {
-        // T = L21 W11 ((n-h) x h, in A's storage past the 1/L_ii entries; A is free until W^T W)
+        // T = L21 W11 ((n-h) x h, in A's storage past the 1/L_ii entries; A is free until
+        // W^T W), then W21 = -W22 T: both on the FP64 tensor path (mma.sync m8n8k4 f64,
+        // 8x8 tiles to warps; W11 and W22 are lower triangular, so T's tile (., b0) sums
+        // t >= b0 and W21's tile (a0, .) sums u <= a0 + 7)
         double *T = A + n;
-        const int m21 = (n - h) * h;
-        for (int e = tid; e < m21; e += blockDim.x) {
-            const int i = h + e / h, c = e - (i - h) * h;
-            double s0 = 0.0, s1 = 0.0;
-            int t = c;
-            for (; t + 1 < h; t += 2) {
-                s0 = fma(L[i * n + t], W[t * n + c], s0);
-                s1 = fma(L[i * n + t + 1], W[(t + 1) * n + c], s1);
+        const int lane = tid & 31, nw = blockDim.x >> 5, g = lane >> 2, q = lane & 3;
+        const int m1 = n - h, tr = (m1 + 7) >> 3, tc = (h + 7) >> 3;
+        for (int tile = tid >> 5; tile < tr * tc; tile += nw) {
+            const int r0 = (tile / tc) * 8, b0 = (tile - (tile / tc) * tc) * 8;
+            const int ar = r0 + g, bc = b0 + g;  // ar: row of L21 / T, bc: column of W11 / T
+            double c0 = 0.0, c1 = 0.0;
+            for (int kk = b0 & ~3; kk < h; kk += 4) {
+                const int t = kk + q;
+                const double av = (ar < m1 && t < h) ? L[(h + ar) * n + t] : 0.0;
+                const double bv = (bc < h && t < h) ? W[t * n + bc] : 0.0;
+                asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                    : "+d"(c0), "+d"(c1)
+                    : "d"(av), "d"(bv));
             }
-            if (t < h) s0 = fma(L[i * n + t], W[t * n + c], s0);
-            T[e] = s0 + s1;
+            const int cc = b0 + 2 * q;
+            if (ar < m1) {
+                if (cc < h) T[ar * h + cc] = c0;
+                if (cc + 1 < h) T[ar * h + cc + 1] = c1;
+            }
         }
         __syncthreads();
-        // W21 = -W22 T
-        for (int e = tid; e < m21; e += blockDim.x) {
-            const int i = h + e / h, c = e - (i - h) * h;
-            double s0 = 0.0, s1 = 0.0;
-            int u = h;
-            for (; u + 1 <= i; u += 2) {
-                s0 = fma(W[i * n + u], T[(u - h) * h + c], s0);
-                s1 = fma(W[i * n + u + 1], T[(u + 1 - h) * h + c], s1);
+        for (int tile = tid >> 5; tile < tr * tc; tile += nw) {
+            const int r0 = (tile / tc) * 8, b0 = (tile - (tile / tc) * tc) * 8;
+            const int ar = r0 + g, bc = b0 + g;  // ar: row of W22 / W21 (offset h), bc: column
+            const int kend = r0 + 8 < m1 ? r0 + 8 : m1;
+            double c0 = 0.0, c1 = 0.0;
+            for (int kk = 0; kk < kend; kk += 4) {
+                const int u = kk + q;  // column of W22 (offset h) = row of T
+                const double av = (ar < m1 && u < m1) ? W[(h + ar) * n + h + u] : 0.0;
+                const double bv = (bc < h && u < m1) ? T[u * h + bc] : 0.0;
+                asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                    : "+d"(c0), "+d"(c1)
+                    : "d"(av), "d"(bv));
             }
-            if (u <= i) s0 = fma(W[i * n + u], T[(u - h) * h + c], s0);
-            W[i * n + c] = -(s0 + s1);
+            const int cc = b0 + 2 * q;
+            if (ar < m1) {
+                if (cc < h) W[(h + ar) * n + cc] = -c0;
+                if (cc + 1 < h) W[(h + ar) * n + cc + 1] = -c1;
+            }
         }
         __syncthreads();
     }
