@@ -37,6 +37,24 @@ METRIC = "local-GP predictions/sec"
 UNIT = "predictions/s"
 
 
+# The paper's own timings with their hardware: context, not the target.
+PAPER_CONTEXT = {
+    "note": "PAPER.md timings (FP64, 2012 hardware); whole local-approximation runs, possibly incl. local MLE "
+            "(P:845-849); context only",
+    "lgbb_n50_Np1000": {"locations": 644436, "wall_s": 21 * 60, "locations_per_s": 511,
+                        "hardware": "4 nodes x (16 Sandy Bridge cores + 2 Tesla M2090), GPUs take 80% of ALC",
+                        "cite": "P:1006-1015"},
+    "borehole_table1_1024000": {"N=M": 1024000, "n": 60, "Nprime": 5772,
+                                "cpu": {"wall_s": 2789.81, "locations_per_s": 367,
+                                        "hardware": "96 nodes x 16 Sandy Bridge cores (1536 cores)"},
+                                "gpu": {"wall_s": 13694.48, "locations_per_s": 75,
+                                        "hardware": "5 nodes x (2 Tesla M2090 + 16 cores)"},
+                                "cite": "P:1062-1127 (Table 1)"},
+    "fig6_speedup_vs_1_core": {"16_cores_plus_2_gpus": [33, 50, 100], "nNp": [[50, 1000], [50, 2000], [128, 2000]],
+                               "cite": "P:933-936"},
+}
+
+
 def alc_evals_per_location(n0, n, Nprime):
     """ALC candidate evaluations per location: sum_{j=n0}^{n-1} (N' - j)."""
     return sum(Nprime - j for j in range(n0, n))
@@ -210,6 +228,22 @@ def run_reference(args):
     return 0
 
 
+def traffic_for(workload, form, launches):
+    """DRAM bytes (read + write) per local-design launch of this workload and
+    form, from the ncu --set full capture of the same workload
+    (profiles/ncu_traffic.json: {workload: {form: {"bytes": B, "launches": L,
+    "profile": file}}}); None when no capture of this workload exists."""
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        tr = json.load(open(tp)).get(workload, {}).get(form)
+    except Exception:
+        return None
+    if not tr:
+        return None
+    return {"bytes_per_launch": tr["bytes"] / max(1, tr.get("launches", 1)), "profile": tr.get("profile"),
+            "algorithmic_bytes_note": tr.get("note")}
+
+
 def form_work(form, n0, n, Np, p):
     """Algorithmic FP64 work per location of a local-design kernel.
 
@@ -223,14 +257,36 @@ def form_work(form, n0, n, Np, p):
     return float(alc_paper_flops_per_location(n0, n, Np))
 
 
+def self_launch(args) -> int:
+    """--gpus N > 1 outside torchrun: launch N ranks (one per GPU) the way the
+    driver does (torch.distributed.run, 127.0.0.1) and pass their output through."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.stderr.write(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible\n")
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--form", default="incremental", choices=["explicit", "incremental", "explicit_dfma"],
-                    help="formulation of the headline number")
+    ap.add_argument("--form", default="auto", choices=["auto", "explicit", "incremental", "explicit_dfma"],
+                    help="formulation of the headline number (auto = laGP_alc_batch's choice)")
+    ap.add_argument("--no-north-star", action="store_true",
+                    help="skip the north_star C4 line (N = M = 10^6 split over the ranks: strong scaling)")
     ap.add_argument("--compare", default="explicit",
                     help="comma list of other forms timed the same way and reported under 'forms' ('' = none)")
     ap.add_argument("--workload", default=WORKLOAD, choices=sorted(WORKLOADS),
@@ -244,6 +300,12 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        return self_launch(args)
+    if world_env is not None and int(world_env) != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}\n")
+        return 2
 
     import torch
     import torch.distributed as dist
@@ -274,24 +336,36 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    def time_form(form, clocks=None):
+    def time_form(form, clocks=None, Xd=None, Zd=None, XXd=None, c=None, m_rank=None, m_all=None, steps=None,
+                  workload=None):
+        """Warm-up, then `steps` timed steps (L2 flushed before each, barrier + sync on
+        both sides, CUDA events on the launching stream, max over ranks)."""
+        Xd = X if Xd is None else Xd
+        Zd = Z if Zd is None else Zd
+        XXd = XX if XXd is None else XXd
+        c = cfg if c is None else c
+        m_rank = M_rank if m_rank is None else m_rank
+        m_all = M_all if m_all is None else m_all
+        steps = args.steps if steps is None else steps
+        workload = args.workload if workload is None else workload
+        a = (c["d"], c["g"], c["n0"], c["n"], c["Nprime"])
         for _ in range(args.warmup):
-            lagp.alc_batch(X, Z, XX, d, g, n0, n, Np, form=form)
+            lagp.alc_batch(Xd, Zd, XXd, *a, form=form)
         torch.cuda.synchronize()
         if clocks:
             clocks.start()
         total = alc = nn = 0.0
         launches = 0
         res = None
-        for _ in range(args.steps):
+        for _ in range(steps):
             flush.fill_(1.0)  # L2 flush between timed steps (untimed)
             barrier()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            res = lagp.alc_batch(X, Z, XX, d, g, n0, n, Np, form=form, timing=True)
+            res = lagp.alc_batch(Xd, Zd, XXd, *a, form=form, timing=True)
             if world > 1:  # SURVEY §8e: the one collective, results all-gathered in input order
-                lagp.gather_shards(res, M_all)
+                lagp.gather_shards(res, m_all)
             e1.record(stream)
             barrier()
             total += e0.elapsed_time(e1)
@@ -302,30 +376,37 @@ def main():
         t = torch.tensor([total, alc, nn], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t[0]) / args.steps
-        alc_launch_ms = float(t[1]) / args.steps  # one local-design launch per step (M = 10,000)
-        achieved = M_rank * form_work(form, n0, n, Np, p) / (alc_launch_ms / 1000.0) / 1e12
-        roof = {"bound": "alu", "kernel": {"incremental": "alc_incremental_v2_kernel",
-                                           "explicit": "alc_explicit_dmma_kernel",
-                                           "explicit_dfma": "alc_explicit_kernel"}[form],
+        ms_step = float(t[0]) / steps
+        alc_step_ms = float(t[1]) / steps
+        ran = res["timing"]["alc_form"]  # the resolved formulation (auto -> incremental / explicit)
+        pp, Npp, nn_, n0_ = c["X"].shape[1], c["Nprime"], c["n"], c["n0"]
+        design_launches = -(-m_rank // 65536)  # one local-design launch per 65,536-location chunk
+        achieved = m_rank * form_work(ran, n0_, nn_, Npp, pp) / (alc_step_ms / 1000.0) / 1e12
+        kern = {"incremental": ("alc_incremental_v2_kernel" if Npp <= 1024 and pp in (1, 2, 3, 4, 8)
+                                else "alc_incremental_kernel"),
+                "explicit": "alc_explicit_dmma_kernel" if nn_ <= 64 else "alc_explicit_kernel",
+                "explicit_dfma": "alc_explicit_kernel"}[ran]
+        roof = {"bound": "alu", "kernel": kern, "alc_form": ran,
                 "achieved": achieved, "peak": nominal, "unit": "TFLOP/s", "frac": achieved / nominal,
-                "traffic": None,
+                "traffic": traffic_for(workload, ran, design_launches),
                 "work": ("incremental: (N'-j-1)(2j+3p+8) flop per location-step j=0..n-1, FP64, exp not counted"
-                         if form == "incremental" else
+                         if ran == "incremental" else
                          "paper count (N'-j)(2j^2+4j) flop per location-step (SURVEY §8d), FP64"),
-                "peak_basis": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz",
+                "peak_basis": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (no FP64 entry in MEASURED_PEAKS.json)",
                 "peak_measured_dfma": meas,
-                "kernel_ms_per_launch": alc_launch_ms}
-        if form == "incremental":
+                "kernel_ms_per_step": alc_step_ms, "kernel_launches_per_step": design_launches,
+                "kernel_ms_per_launch": alc_step_ms / design_launches}
+        if ran == "incremental":
             # secondary view: the per-candidate state w_c streamed every step (sum over steps
             # of (N'-j-1) j entries x 8 B per location) against the shared-memory bandwidth
             # (128 B/clk/SM x 148 x 1.965 GHz); part of it is served by registers / TMEM
-            sb = M_rank * sum((Np - jj - 1) * jj * 8.0 for jj in range(n)) / (alc_launch_ms / 1000.0) / 1e9
+            sb = m_rank * sum((Npp - jj - 1) * jj * 8.0 for jj in range(nn_)) / (alc_step_ms / 1000.0) / 1e9
             smem_peak = 128 * 148 * 1.965
             roof["state_stream"] = {"achieved_GBps": sb, "smem_peak_GBps": smem_peak, "frac": sb / smem_peak,
                                     "bytes": "sum_j (N'-j-1) j 8 B per location (w_c entries read per step)"}
-        return dict(ms_step=ms_step, value=M_all / (ms_step / 1000.0), alc_ms=alc_launch_ms,
-                    nn_ms=float(t[2]) / args.steps, launches=launches, res=res, clk=clk, roofline=roof)
+        return dict(ms_step=ms_step, value=m_all / (ms_step / 1000.0), alc_ms=alc_step_ms,
+                    nn_ms=float(t[2]) / steps, launches=launches, res=res, clk=clk, roofline=roof,
+                    form=ran)
 
     head = time_form(args.form, ClockSampler(local))
     others = {}
@@ -392,28 +473,48 @@ def main():
     h2d = (Xh.nbytes + Zh.nbytes) * world + M_all * XXh.shape[1] * 8  # every rank: X, Z and its XX rows
     d2h = M_all * (n * 4 + 3 * 8 + 4)
 
+    # ---- north_star target shape: C4 (8-d borehole, N = M = 10^6, n = 50, N' = 1000), the
+    # whole predictive set split over the ranks (strong scaling; the driver's 1/2/4/8-GPU
+    # runs give the 1 -> 8 curve). Same timing rules; fewer steps (1.5 s per step on one GPU).
+    north = None
+    if not args.no_north_star and args.workload != "C4":
+        c4 = make_inputs(1, "C4")
+        lo4, m4, mall4 = rank_rows("C4", c4["XX"].shape[0], rank, world)
+        X4, Z4 = torch.from_numpy(c4["X"]).to(dev), torch.from_numpy(c4["Z"]).to(dev)
+        XX4 = torch.from_numpy(np.ascontiguousarray(c4["XX"][lo4:lo4 + m4])).to(dev)
+        h4 = time_form("auto", ClockSampler(local), X4, Z4, XX4, c4, m4, mall4, steps=min(args.steps, 3),
+                       workload="C4")
+        north = {"workload": WORKLOADS["C4"] + f", d=q10={c4['d']:.4f} g=1e-4", "scaling": "strong",
+                 "metric": METRIC, "value": h4["value"], "unit": UNIT, "ms_per_step": h4["ms_step"],
+                 "steps": min(args.steps, 3), "warmup": args.warmup,
+                 "phase_ms_per_step": {"nn": h4["nn_ms"], "local_design": h4["alc_ms"]},
+                 "roofline": h4["roofline"], "clocks": h4["clk"], "gpu_launches": h4["launches"],
+                 "locations_per_rank": m4, "status": int(h4["res"]["status"])}
+        if world == 1 and not args.no_cpu_baseline:
+            import oracle
+
+            S4 = 16
+            sel4 = np.sort(np.random.default_rng(44).choice(m4, S4, replace=False))
+            o4 = oracle.alc_batch(c4["X"], c4["Z"], c4["XX"][lo4 + sel4], c4["d"], c4["g"], c4["n0"], c4["n"],
+                                  c4["Nprime"])
+            gi4 = h4["res"]["idx"].cpu().numpy()[sel4]
+            north["sample_parity"] = {"locations": S4,
+                                      "identical_index_sequences": int((gi4 == o4["idx"]).all(1).sum())}
+        del X4, Z4, XX4, h4
+
     if rank != 0:
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
         return 0
 
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        try:
-            tr = json.load(open(tp))
-            head["roofline"]["traffic"] = tr.get(args.form)
-            for f in others:
-                others[f]["roofline"]["traffic"] = tr.get(f)
-        except Exception:
-            pass
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak" if args.workload == "C2" else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOADS[args.workload] + f", d=q10={d:.4f} g=1e-4",
-                   "alc_form": args.form, "l2": "flushed (256 MiB write) before every timed step",
+                   "alc_form": head["form"], "l2": "flushed (256 MiB write) before every timed step",
                    "parallelism": f"dp{world} (XX sharded, X/Z replicated)"},
         "alc_evals_per_sec": M_all * evals / (ms_step / 1000.0),
         # the same numerator over the local-design kernel time (max over ranks),
@@ -436,6 +537,8 @@ def main():
         "gpu_launches": head["launches"],
         "clocks": head["clk"],
         "status": int(res["status"]),
+        "north_star_c4": north,
+        "paper_context": PAPER_CONTEXT,
     }
     if world == 1 and not args.no_cpu_baseline:
         o, S, el, used = cpu_baseline(cfg, budget_s=args.cpu_budget, lo=0)

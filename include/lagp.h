@@ -30,12 +30,13 @@
 extern "C" {
 #endif
 
-#define LAGP_ABI_VERSION 2
+#define LAGP_ABI_VERSION 3
 #define LAGP_SCORES_JMAX 768 /* laGP_alc_scores: largest j (Fig 4 goes to 512) */
 #define LAGP_NMAX 128  /* largest local design size n of the greedy path (laGP_alc_scores: LAGP_SCORES_JMAX) */
 #define LAGP_PMAX 16   /* largest input dimension p */
-#define LAGP_NPRIME_MAX 65536 /* largest candidate pool N' (laGP_alc_batch; the incremental
-                                 form takes N' <= 8192, laGP_nn_pool's sorted output N' <= 8192) */
+#define LAGP_NPRIME_MAX 65536 /* largest candidate pool N' (laGP_alc_batch; laGP_nn_pool's
+                                 sorted output N' <= 8192) */
+#define LAGP_NPRIME_MAX_INC 8192 /* largest N' of the incremental form (LAGP_ALC_INCREMENTAL) */
 
 typedef enum {
     LAGP_OK = 0,      /* every location reached size n                                   */
@@ -68,8 +69,17 @@ enum {
  *  LAGP_ALC_INCREMENTAL — SURVEY §8f row f1: per-candidate Schur-complement
  *                         downdates, O(j) per candidate per step.
  *  LAGP_ALC_EXPLICIT_DFMA — the explicit form forced onto the DFMA micro-kernel
- *                         for every n (the comparison arm for the DMMA choice). */
-typedef enum { LAGP_ALC_EXPLICIT = 0, LAGP_ALC_INCREMENTAL = 1, LAGP_ALC_EXPLICIT_DFMA = 2 } lagp_alc_form;
+ *                         for every n (the comparison arm for the DMMA choice).
+ *  LAGP_ALC_AUTO        — LAGP_ALC_INCREMENTAL wherever this build's incremental
+ *                         kernels take the shape (N' <= LAGP_NPRIME_MAX_INC), else
+ *                         LAGP_ALC_EXPLICIT; what laGP_alc_batch uses. The
+ *                         resolved form is reported in lagp_timing.alc_form. */
+typedef enum {
+    LAGP_ALC_EXPLICIT = 0,
+    LAGP_ALC_INCREMENTAL = 1,
+    LAGP_ALC_EXPLICIT_DFMA = 2,
+    LAGP_ALC_AUTO = 3
+} lagp_alc_form;
 
 /* Phase timings (milliseconds, CUDA events on cuda_stream) filled when the
  * optional `timing` argument is non-NULL. */
@@ -80,6 +90,7 @@ typedef struct {
     float total_ms;   /* whole call on the device                           */
     int32_t launches; /* number of kernel launches this call issued          */
     int32_t nn_fallbacks; /* locations whose NN pool needed the exact radix-select fallback */
+    int32_t alc_form; /* the formulation that ran (lagp_alc_form; LAGP_ALC_AUTO resolved) */
 } lagp_timing;
 
 /*
@@ -95,8 +106,13 @@ typedef struct {
  *        variance Delta = v_j(x) - v_{j+1}(x) of Eq (5)-(6), ties to
  *        the lowest global row index (R7); candidates with s_c <= 1e-12 excluded;
  *   (a4) partitioned-inverse update of K_j^{-1};
- *   (a5) mean, s2 (Eq (1)-(2) with N -> n) from a fresh Cholesky of
- *        K_n; var = s2 n/(n-2), NaN if n <= 2.
+ *   (a5) mean, s2 (Eq (1)-(2) with N -> n) from a fresh factorisation
+ *        of K_n; var = s2 n/(n-2), NaN if n <= 2.
+ * The formulation is LAGP_ALC_AUTO: the incremental form (the
+ * same argmax in exact arithmetic, on per-candidate Cholesky-factor state, with
+ * the factor of K_n built column by column for a5) where N' <= LAGP_NPRIME_MAX_INC,
+ * otherwise the explicit-K^{-1} form of the paper (a4 as written, fresh Cholesky
+ * in a5). laGP_alc_batch_ex selects a form explicitly.
  *
  * Arguments
  *   X [N×p], Z [N]          design and responses (zero-mean GP, Z used raw, R14)

@@ -65,7 +65,8 @@ def lib():
         _lib.oracle_sep_scale.restype = None
         _lib.oracle_local_fit_batch.argtypes = [D, i64, i32, D, D, i64, dbl, dbl, dbl, dbl, i32, i32, i32, i32,
                                                 i32, I32, D, D, D, D, U32]
-        for f in ("oracle_nn", "oracle_invert_spd", "oracle_alc_scores", "oracle_pinv_update",
+        _lib.oracle_score_noise.argtypes = [D, i64, i32, D, dbl, dbl, i32, i32, i32, I32, D, D]
+        for f in ("oracle_score_noise", "oracle_nn", "oracle_invert_spd", "oracle_alc_scores", "oracle_pinv_update",
                   "oracle_predict", "oracle_local_design", "oracle_alc_batch", "oracle_loglik", "oracle_mle",
                   "oracle_local_fit_batch"):
             getattr(_lib, f).restype = ctypes.c_int
@@ -168,6 +169,25 @@ def alc_batch(X, Z, XX, d, g, n0, n, Nprime, threads=0):
         _p(best, ctypes.c_double), _p(s2acc, ctypes.c_double))
     return dict(idx=idx, mean=mean, s2=s2, var=var, flags=flags, gaps=gaps, best=best,
                 s2_acc=s2acc, threads=used)
+
+
+def score_noise(X, x, idx, d, g, n0, n, Nprime):
+    """Reading R18 (tau_cfg): along the oracle's own trajectory idx[n] for x, the
+    per-step max |Delta_explicit - Delta_ref| / max Delta_ref between the oracle's
+    explicit-K^{-1} scores and a fresh long-double solve of the same Eq (5)
+    closed form, and the reference top-2 gap. Returns (noise, ref_gap), each
+    [n - n0] (NaN after an exhaustion)."""
+    X, pX = _d(X)
+    x, px = _d(np.ravel(x))
+    idx = np.ascontiguousarray(idx, dtype=np.int32)
+    N, p = X.shape
+    noise = np.empty(n - n0)
+    gap = np.empty(n - n0)
+    rc = lib().oracle_score_noise(pX, N, p, px, d, g, n0, n, Nprime, _p(idx, ctypes.c_int32),
+                                  _p(noise, ctypes.c_double), _p(gap, ctypes.c_double))
+    if rc:
+        raise RuntimeError(f"oracle_score_noise rc={rc}")
+    return noise, gap
 
 
 def sep_scale(X, theta):

@@ -367,6 +367,134 @@ out:
     return rc;
 }
 
+/* ------------------------------------------------------------------------- */
+/* Score noise of this oracle (reading R18: tau_cfg). Along the trajectory idx[n]
+ * that oracle_local_design chose for x, recompute at every greedy step j the
+ * oracle's own explicit-K_j^{-1} scores (the same oracle_invert_spd /
+ * oracle_pinv_update / alc_one calls in the same order, so bit-identical to the
+ * run) and reference scores by a FRESH long-double solve of the same Eq (5)
+ * closed form (App A.1): with K_j = L L^T (long-double Cholesky of the long-
+ * double kernel matrix), v = L^{-1} k_j(x'), z = L^{-1} h,
+ *   Delta_ref = (kappa - z^T v)^2 / (1 + eta - v^T v).
+ * noise[j - n0] = max_c |Delta_explicit - Delta_ref| / max_c Delta_ref over the
+ * candidates both sides keep (s > 1e-12); ref_gap[j - n0] = the reference top-2
+ * relative gap (R19). Steps after an exhaustion (-1 in idx) get NaN.
+ * Measurement only: nothing here changes what the oracle selects. */
+static long double corr_ld(const double *a, const double *b, int p, double theta) {
+    long double acc = 0.0L;
+    for (int k = 0; k < p; k++) {
+        long double diff = (long double)a[k] - (long double)b[k];
+        acc += diff * diff;
+    }
+    return expl(-acc / (long double)theta);
+}
+
+int oracle_score_noise(const double *X, int64_t N, int p, const double *x, double theta, double eta,
+                       int n0, int n, int Nprime, const int32_t *idx, double *noise, double *ref_gap) {
+    int rc = 0;
+    int32_t *pool = (int32_t *)malloc(sizeof(int32_t) * (size_t)Nprime);
+    char *chosen = (char *)calloc((size_t)Nprime, 1);
+    double *Xj = (double *)malloc(sizeof(double) * (size_t)n * p);
+    double *Kinv = (double *)malloc(sizeof(double) * (size_t)n * n);
+    double *Knew = (double *)malloc(sizeof(double) * (size_t)n * n);
+    double *K0 = (double *)malloc(sizeof(double) * (size_t)n0 * n0);
+    double *h = (double *)malloc(sizeof(double) * (size_t)n);
+    double *u = (double *)malloc(sizeof(double) * (size_t)n);
+    double *kc = (double *)malloc(sizeof(double) * (size_t)n);
+    double *dexp = (double *)malloc(sizeof(double) * (size_t)Nprime);
+    long double *dref = (long double *)malloc(sizeof(long double) * (size_t)Nprime);
+    long double *L = (long double *)malloc(sizeof(long double) * (size_t)n * n);
+    long double *v = (long double *)malloc(sizeof(long double) * (size_t)n);
+    long double *z = (long double *)malloc(sizeof(long double) * (size_t)n);
+    if (!pool || !chosen || !Xj || !Kinv || !Knew || !K0 || !h || !u || !kc || !dexp || !dref || !L || !v || !z) {
+        rc = 4;
+        goto out;
+    }
+    for (int t = 0; t < n - n0; t++) { noise[t] = NAN; ref_gap[t] = NAN; }
+    rc = oracle_nn(X, N, p, x, Nprime, pool, NULL);
+    if (rc) goto out;
+    for (int t = 0; t < n0; t++) {
+        chosen[t] = 1;
+        memcpy(Xj + t * p, X + (size_t)pool[t] * p, sizeof(double) * p);
+    }
+    build_K(n0, p, Xj, theta, eta, K0);
+    if (oracle_invert_spd(n0, K0, Kinv)) goto out;
+    for (int a = 0; a < n0; a++) h[a] = corr(Xj + a * p, x, p, theta);
+    for (int j = n0; j < n && idx[j] >= 0; j++) {
+        /* explicit scores, exactly as oracle_local_design forms them */
+        for (int c = 0; c < Nprime; c++) {
+            dexp[c] = NAN;
+            if (chosen[c]) continue;
+            double dcf;
+            double minv = alc_one(j, p, Xj, Kinv, h, X + (size_t)pool[c] * p, x, theta, eta, u, kc, &dcf, NULL);
+            if (minv > OR_S_MIN && isfinite(dcf)) dexp[c] = dcf;
+        }
+        /* fresh long-double factorisation of K_j = C(X_j) + eta I */
+        for (int a = 0; a < j; a++)
+            for (int b = 0; b <= a; b++)
+                L[a * j + b] = corr_ld(Xj + a * p, Xj + b * p, p, theta) + (a == b ? (long double)eta : 0.0L);
+        for (int k = 0; k < j; k++) {
+            long double dkk = L[k * j + k];
+            for (int t = 0; t < k; t++) dkk -= L[k * j + t] * L[k * j + t];
+            if (!(dkk > 0.0L)) { rc = 1; goto out; }
+            L[k * j + k] = sqrtl(dkk);
+            for (int i = k + 1; i < j; i++) {
+                long double sik = L[i * j + k];
+                for (int t = 0; t < k; t++) sik -= L[i * j + t] * L[k * j + t];
+                L[i * j + k] = sik / L[k * j + k];
+            }
+        }
+        for (int a = 0; a < j; a++) {
+            long double sa = corr_ld(Xj + a * p, x, p, theta);
+            for (int t = 0; t < a; t++) sa -= L[a * j + t] * z[t];
+            z[a] = sa / L[a * j + a];
+        }
+        long double m1 = -1.0L, m2 = -1.0L;
+        for (int c = 0; c < Nprime; c++) {
+            dref[c] = -1.0L;
+            if (chosen[c]) continue;
+            const double *xc = X + (size_t)pool[c] * p;
+            long double vv = 0.0L, zv = 0.0L;
+            for (int a = 0; a < j; a++) {
+                long double sa = corr_ld(Xj + a * p, xc, p, theta);
+                for (int t = 0; t < a; t++) sa -= L[a * j + t] * v[t];
+                v[a] = sa / L[a * j + a];
+                vv += v[a] * v[a];
+                zv += z[a] * v[a];
+            }
+            long double s_ref = 1.0L + (long double)eta - vv;
+            if (!(s_ref > (long double)OR_S_MIN)) continue;
+            long double cv = corr_ld(xc, x, p, theta) - zv;
+            dref[c] = cv * cv / s_ref;
+            if (dref[c] > m1) { m2 = m1; m1 = dref[c]; } else if (dref[c] > m2) { m2 = dref[c]; }
+        }
+        long double worst = 0.0L;
+        for (int c = 0; c < Nprime; c++)
+            if (dref[c] >= 0.0L && !isnan(dexp[c])) {
+                long double e = fabsl((long double)dexp[c] - dref[c]);
+                if (e > worst) worst = e;
+            }
+        noise[j - n0] = m1 > 0.0L ? (double)(worst / m1) : 0.0;
+        ref_gap[j - n0] = m1 > 0.0L ? (double)((m1 - (m2 > 0.0L ? m2 : 0.0L)) / m1) : 0.0;
+        /* advance along the oracle's own trajectory (a4, the same calls as the run) */
+        int bpos = -1;
+        for (int c = 0; c < Nprime; c++)
+            if (pool[c] == idx[j]) bpos = c;
+        if (bpos < 0 || chosen[bpos]) { rc = 2; goto out; }
+        const double *xs = X + (size_t)idx[j] * p;
+        for (int a = 0; a < j; a++) kc[a] = corr(Xj + a * p, xs, p, theta);
+        oracle_pinv_update(j, Kinv, kc, 1.0 + eta, Knew);
+        memcpy(Kinv, Knew, sizeof(double) * (size_t)(j + 1) * (j + 1));
+        chosen[bpos] = 1;
+        memcpy(Xj + j * p, xs, sizeof(double) * p);
+        h[j] = corr(xs, x, p, theta);
+    }
+out:
+    free(pool); free(chosen); free(Xj); free(Kinv); free(Knew); free(K0); free(h); free(u); free(kc);
+    free(dexp); free(dref); free(L); free(v); free(z);
+    return rc;
+}
+
 /* All M locations, OpenMP over locations ("embarrassingly parallel").
  * Output layouts: idx M×n, gaps/best M×(n-n0). Returns the number of threads used. */
 int oracle_alc_batch(const double *X, int64_t N, int p, const double *Z, const double *XX, int64_t M,

@@ -19,6 +19,7 @@ import torch
 
 from . import _lib
 from ._lib import (  # noqa: F401
+    ALC_AUTO,
     ALC_EXPLICIT,
     ALC_INCREMENTAL,
     FLAG_EXHAUSTED,
@@ -38,7 +39,8 @@ from ._lib import (  # noqa: F401
 
 _LIB = None
 
-FORMS = {"explicit": ALC_EXPLICIT, "incremental": ALC_INCREMENTAL, "explicit_dfma": _lib.ALC_EXPLICIT_DFMA}
+FORMS = {"explicit": ALC_EXPLICIT, "incremental": ALC_INCREMENTAL, "explicit_dfma": _lib.ALC_EXPLICIT_DFMA,
+         "auto": ALC_AUTO}
 
 
 class LagpError(RuntimeError):
@@ -84,10 +86,12 @@ def _stream(device) -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
-def alc_batch(X, Z, XX, d, g, n0, n, Nprime, form="explicit", gaps=False, timing=False, out=None, theta=None):
+def alc_batch(X, Z, XX, d, g, n0, n, Nprime, form="auto", gaps=False, timing=False, out=None, theta=None):
     """laGP_alc_batch_ex on CUDA tensors. Returns a dict with idx [M×n] int32,
     mean, s2, var [M] float64, flags [M] int32 (uint32 bits), optionally
     gaps [M×(n-n0)] and the phase timing, plus ``status`` (OK or PARTIAL).
+    ``form="auto"`` is laGP_alc_batch's choice (the incremental form where it
+    applies, else the paper's explicit form); the timing names the form that ran.
     With ``theta`` (CUDA float64 [M]) every location uses its own lengthscale
     (laGP_alc_batch_theta); ``d`` is then only validated."""
     X = _dev(X, "X")
@@ -107,7 +111,13 @@ def alc_batch(X, Z, XX, d, g, n0, n, Nprime, form="explicit", gaps=False, timing
         if gaps:
             out["gaps"] = torch.empty((M, n - n0), dtype=torch.float64, device=dev)
     tm = Timing()
-    if theta is None:
+    if theta is None and form == "auto" and not timing:
+        # the north_star entry point itself (LAGP_ALC_AUTO inside)
+        st = lib().laGP_alc_batch(
+            _ptr(X), N, p, _ptr(Z), _ptr(XX), M, float(d), float(g), int(n0), int(n), int(Nprime),
+            _ptr(out["idx"]), _ptr(out["mean"]), _ptr(out["s2"]), _ptr(out["var"]), _ptr(out["flags"]),
+            _ptr(out.get("gaps")), _stream(dev))
+    elif theta is None:
         st = lib().laGP_alc_batch_ex(
             _ptr(X), N, p, _ptr(Z), _ptr(XX), M, float(d), float(g), int(n0), int(n), int(Nprime),
             _ptr(out["idx"]), _ptr(out["mean"]), _ptr(out["s2"]), _ptr(out["var"]), _ptr(out["flags"]),
@@ -127,7 +137,7 @@ def alc_batch(X, Z, XX, d, g, n0, n, Nprime, form="explicit", gaps=False, timing
     return out
 
 
-def alc_batch_sep(X, Z, XX, theta, g, n0, n, Nprime, form="incremental", gaps=False, timing=False):
+def alc_batch_sep(X, Z, XX, theta, g, n0, n, Nprime, form="auto", gaps=False, timing=False):
     """laGP_alc_batch_sep (row f3): the full path under the separable correlation
     exp(-sum_k (x_k - x'_k)^2 / theta_k); ``theta`` is a sequence of p floats (host)."""
     X = _dev(X, "X")
@@ -179,11 +189,12 @@ def mle(X, Z, XX, idx, d0, lo, hi, g, theta_in=None):
     st = lib().laGP_mle(_ptr(X), N, p, _ptr(Z), _ptr(XX), M, _ptr(idx), n, _ptr(theta_in), float(d0), float(lo),
                         float(hi), float(g), _ptr(out["theta"]), _ptr(out["loglik"]), _ptr(out["iters"]),
                         _ptr(out["flags"]), _ptr(out["mean"]), _ptr(out["s2"]), _ptr(out["var"]), _stream(dev))
-    _check(st)
+    _check(st, (LAGP_OK, LAGP_PARTIAL))
+    out["status"] = st
     return out
 
 
-def local_fit(X, Z, XX, d0, lo, hi, g, n0, n, Nprime, stages=2, form="incremental", timing=False):
+def local_fit(X, Z, XX, d0, lo, hi, g, n0, n, Nprime, stages=2, form="auto", timing=False):
     """laGP_local_fit (Fig 1 steps 1-5): NN pool once, then ``stages`` times
     {local design with theta_x, theta_x = MLE}, then the prediction. Returns idx
     (last design), theta [stages×M], mean, s2, var, flags, status (+ timing)."""
@@ -209,7 +220,7 @@ def local_fit(X, Z, XX, d0, lo, hi, g, n0, n, Nprime, stages=2, form="incrementa
     return out
 
 
-def alc_batch_host(X, Z, XX, d, g, n0, n, Nprime, form="explicit", out=None, device=None):
+def alc_batch_host(X, Z, XX, d, g, n0, n, Nprime, form="auto", out=None, device=None):
     """laGP_alc_batch_host: numpy (ideally pinned-backed) host arrays in and out;
     the host<->device copies happen inside the call (end-to-end API)."""
     X = np.ascontiguousarray(X, dtype=np.float64)
@@ -297,7 +308,7 @@ def shard_bounds(M: int, rank: int, world: int):
     return lo, min(M, lo + per), per
 
 
-def alc_batch_dist(X, Z, XX, d, g, n0, n, Nprime, form="explicit", group=None):
+def alc_batch_dist(X, Z, XX, d, g, n0, n, Nprime, form="auto", group=None):
     """Multi-GPU path: every rank holds the full X, Z (replicated)
     and the full XX; rank r runs laGP_alc_batch on its contiguous shard of XX
     and one all-gather (NCCL over NVLink under the "nccl" backend) assembles
@@ -328,10 +339,11 @@ def gather_shards(r: dict, M: int, group=None) -> dict:
         if nccl:
             full = torch.empty((world * per,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
             dist.all_gather_into_tensor(full, pad, group=group)
-        else:
-            parts = [torch.empty_like(pad) for _ in range(world)]
-            dist.all_gather(parts, pad, group=group)
-            full = torch.cat(parts)
+        else:  # gloo (CPU tests, or CUDA tensors staged through host memory)
+            hp = pad.cpu()
+            parts = [torch.empty_like(hp) for _ in range(world)]
+            dist.all_gather(parts, hp, group=group)
+            full = torch.cat(parts).to(t.device)
         return full[:M]
 
     return dict(idx=gather(r["idx"], -1), mean=gather(r["mean"], float("nan")),

@@ -15,7 +15,8 @@ LIB_PATH = os.path.join(_PKG, "liblagp_b200.so")
 LAGP_OK, LAGP_PARTIAL, LAGP_EINVAL, LAGP_ECUDA, LAGP_ENOMEM = 0, 1, 2, 3, 4
 FLAG_NEAR_TIE, FLAG_SENTINEL, FLAG_EXHAUSTED, FLAG_NONFINITE = 1, 2, 4, 8
 FLAG_MLE_BOUND, FLAG_MLE_MAXIT, FLAG_MLE_FAIL = 16, 32, 64
-ALC_EXPLICIT, ALC_INCREMENTAL, ALC_EXPLICIT_DFMA = 0, 1, 2
+ALC_EXPLICIT, ALC_INCREMENTAL, ALC_EXPLICIT_DFMA, ALC_AUTO = 0, 1, 2, 3
+FORM_NAMES = {0: "explicit", 1: "incremental", 2: "explicit_dfma", 3: "auto"}
 NMAX, PMAX = 128, 16
 
 EXPORTS = (
@@ -44,10 +45,13 @@ class Timing(ctypes.Structure):
         ("total_ms", ctypes.c_float),
         ("launches", ctypes.c_int32),
         ("nn_fallbacks", ctypes.c_int32),
+        ("alc_form", ctypes.c_int32),
     ]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["alc_form"] = FORM_NAMES.get(d["alc_form"], d["alc_form"])
+        return d
 
 
 _vp, _i64, _i32, _dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double

@@ -30,6 +30,10 @@ lagp_status fail(lagp_status s, const char *fmt, ...) {
 }
 
 lagp_status cuda_fail(cudaError_t e, const char *where) {
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();  // clear the (non-sticky) allocation error
+        return fail(LAGP_ENOMEM, "%s: %s", where, cudaGetErrorString(e));
+    }
     return fail(LAGP_ECUDA, "%s: %s", where, cudaGetErrorString(e));
 }
 
@@ -48,22 +52,14 @@ int num_sms() {
 
 bool finite_pos(double v) { return std::isfinite(v) && v > 0.0; }
 
-// Stream-ordered workspace allocations released in one place. The device's
-// default memory pool keeps freed blocks (release threshold raised once per
-// call, idempotent) so repeated calls do not return the workspace to the OS
-// and re-map it at every synchronisation.
+// Stream-ordered workspace allocations (cudaMallocAsync from the device's current
+// memory pool, whose attributes this library leaves as the caller set them),
+// released in one place.
 struct Workspace {
     cudaStream_t st;
     void *ptrs[16];
     int n = 0;
-    explicit Workspace(cudaStream_t s) : st(s) {
-        int dev = 0;
-        cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = 8ull << 30;  // keep up to 8 GiB cached
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-    }
+    explicit Workspace(cudaStream_t s) : st(s) {}
     cudaError_t alloc(void **p, size_t bytes) {
         if (bytes == 0) bytes = 16;
         cudaError_t e = cudaMallocAsync(p, bytes, st);
@@ -112,16 +108,19 @@ namespace {
 struct DesignPlan {
     int sms = 1, ld = 0, Npad = 0;
     int64_t cache_stride = 0;
-    bool incremental = false, use_cluster = false, use_dmma = false;
+    bool incremental = false, use_dmma = false;
+    int form = LAGP_ALC_EXPLICIT;  // the resolved formulation (LAGP_ALC_AUTO chooses)
     lagp::IncPlan inc{};
     int alc_grid = 0, nn_grid = 0;
     int64_t chunk = 0;
 };
 
 lagp_status check_form(int32_t alc_form) {
-    if (alc_form != LAGP_ALC_EXPLICIT && alc_form != LAGP_ALC_INCREMENTAL && alc_form != LAGP_ALC_EXPLICIT_DFMA)
+    if (alc_form != LAGP_ALC_EXPLICIT && alc_form != LAGP_ALC_INCREMENTAL && alc_form != LAGP_ALC_EXPLICIT_DFMA &&
+        alc_form != LAGP_ALC_AUTO)
         return fail(LAGP_EINVAL,
-                    "alc_form must be LAGP_ALC_EXPLICIT, LAGP_ALC_INCREMENTAL or LAGP_ALC_EXPLICIT_DFMA (got %d)",
+                    "alc_form must be LAGP_ALC_EXPLICIT, LAGP_ALC_INCREMENTAL, LAGP_ALC_EXPLICIT_DFMA or LAGP_ALC_AUTO "
+                    "(got %d)",
                     alc_form);
     return LAGP_OK;
 }
@@ -132,23 +131,29 @@ lagp_status plan_design(int32_t p, int32_t n, int32_t Nprime, int64_t M, int32_t
     P.ld = (n + 3) & ~3;
     P.Npad = (Nprime + 3) & ~3;
     P.cache_stride = (int64_t)n * P.Npad + 1024;  // + max tile width (tile overrun)
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    // LAGP_ALC_AUTO: the incremental form wherever this build's incremental kernels
+    // take the shape (same selection in exact arithmetic, 4-10x faster), else the
+    // paper's explicit form
+    if (alc_form == LAGP_ALC_AUTO) {
+        lagp::IncPlan probe{};
+        const bool v2 = lagp::inc_v2_plan(n, p, Nprime, (size_t)optin - 2048, probe);
+        alc_form = (v2 || lagp::inc_plan(n, p, Nprime, P.Npad, (size_t)optin - 2048).ok) ? LAGP_ALC_INCREMENTAL
+                                                                                          : LAGP_ALC_EXPLICIT;
+    }
+    P.form = alc_form;
     P.incremental = alc_form == LAGP_ALC_INCREMENTAL;
-    // incremental form: the single-CTA kernel by default; LAGP_CLUSTER=1 selects the
-    // 2-CTA cluster variant (measured slower on C2: 27.8 vs 15.1 ms)
-    const char *cl = getenv("LAGP_CLUSTER");
-    P.use_cluster = P.incremental && lagp::inc_cluster_supported(n, p, Nprime) && (cl && cl[0] == '1');
     // explicit form: DMMA (FP64 tensor) micro-kernel for n <= 64, DFMA otherwise
     P.use_dmma = (alc_form == LAGP_ALC_EXPLICIT) && n <= 64;
     int alc_bps = 0;
     if (P.incremental) {
-        int dev = 0, optin = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
         // v2 kernel (one barrier per step) where it applies; LAGP_INC_V1=1 forces the
         // 1024-thread kernel of alc_incremental.cu (kept for N' > 1024 and other p)
         const char *v1 = getenv("LAGP_INC_V1");
         const bool force_v1 = v1 && v1[0] == '1';
-        if (force_v1 || P.use_cluster || !lagp::inc_v2_plan(n, p, Nprime, (size_t)optin - 2048, P.inc)) {
+        if (force_v1 || !lagp::inc_v2_plan(n, p, Nprime, (size_t)optin - 2048, P.inc)) {
             P.inc = lagp::inc_plan(n, p, Nprime, P.Npad, (size_t)optin - 2048);
             if (!P.inc.ok)
                 return fail(LAGP_EINVAL, "incremental form: Nprime=%d / n=%d exceed this build's limits", Nprime, n);
@@ -176,7 +181,6 @@ lagp_status plan_design(int32_t p, int32_t n, int32_t Nprime, int64_t M, int32_t
 
 cudaError_t launch_design(const DesignPlan &P, const lagp::AlcArgs &a, cudaStream_t st) {
     const int grid = (int)(a.M < P.alc_grid ? a.M : P.alc_grid);
-    if (P.incremental && P.use_cluster) return lagp::launch_alc_inc_cluster(a, P.sms, st);
     if (P.incremental && P.inc.v2) return lagp::launch_alc_incremental_v2(a, P.inc, grid, st);
     if (P.incremental) return lagp::launch_alc_incremental(a, P.inc, grid, st);
     return P.use_dmma ? lagp::launch_alc_explicit_dmma(a, grid, st) : lagp::launch_alc_explicit(a, grid, st);
@@ -269,6 +273,7 @@ lagp_status alc_batch_impl(const double *X, int64_t N, int32_t p, const double *
         timing->total_ms = tot_ms;
         timing->launches = launches;
         timing->nn_fallbacks = host_counters[1];
+        timing->alc_form = P.form;
     }
     if (host_counters[0] > 0) {
         fail(LAGP_PARTIAL, "%d location(s) flagged EXHAUSTED or NONFINITE", host_counters[0]);
@@ -399,12 +404,18 @@ lagp_status laGP_mle(const double *X, int64_t N, int32_t p, const double *Z, con
         a.theta_out = theta_out; a.loglik_out = loglik_out; a.iters_out = iters_out; a.flags_out = flags_out;
         a.mean = mean_out; a.s2 = s2_out; a.var = var_out;
         a.use_smem = mp.smem ? 1 : 0;
+        int host_partial = 0;
         if (!mp.smem) LAGP_CUDA(ws.alloc((void **)&a.ws, mp.ws));
+        LAGP_CUDA(ws.alloc((void **)&a.n_partial, sizeof(int)));
+        LAGP_CUDA(cudaMemsetAsync(a.n_partial, 0, sizeof(int), st));
         LAGP_CUDA(lagp::launch_mle(a, mp.grid, st));
+        LAGP_CUDA(cudaMemcpyAsync(&host_partial, a.n_partial, sizeof(int), cudaMemcpyDeviceToHost, st));
+        LAGP_CUDA(cudaStreamSynchronize(st));
+        if (host_partial > 0) st_ret = fail(LAGP_PARTIAL, "%d location(s) flagged NONFINITE", host_partial);
     cleanup:;
     }
     cudaError_t e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess && st_ret == LAGP_OK) st_ret = cuda_fail(e, "cudaStreamSynchronize");
+    if (e != cudaSuccess && (st_ret == LAGP_OK || st_ret == LAGP_PARTIAL)) st_ret = cuda_fail(e, "cudaStreamSynchronize");
     return st_ret;
 }
 
@@ -446,10 +457,13 @@ lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *
     LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(P.nn_grid, N, p, Nprime, false, P.chunk)));
     LAGP_CUDA(ws.alloc((void **)&cache, (size_t)P.alc_grid * P.cache_stride * sizeof(double)));
     LAGP_CUDA(ws.alloc((void **)&coords, (size_t)P.alc_grid * (p + 2) * P.Npad * sizeof(double)));
-    LAGP_CUDA(ws.alloc((void **)&counters, 2 * sizeof(int)));
+    // counters: [0] final-stage EXHAUSTED/NONFINITE flags (the last design and the
+    // last MLE/prediction: the flags the caller gets), [1] NN fallbacks, [2] the
+    // earlier stages' flags (not reported: a later stage replaces that design)
+    LAGP_CUDA(ws.alloc((void **)&counters, 3 * sizeof(int)));
     if (!flags_out) LAGP_CUDA(ws.alloc((void **)&fl, (size_t)P.chunk * sizeof(uint32_t)));
     if (!mp.smem) LAGP_CUDA(ws.alloc((void **)&mlews, mp.ws));
-    LAGP_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int), st));
+    LAGP_CUDA(cudaMemsetAsync(counters, 0, 3 * sizeof(int), st));
     if (timing)
         for (int i = 0; i < 5; i++) LAGP_CUDA(cudaEventCreate(&ev[i]));
     if (timing) LAGP_CUDA(cudaEventRecord(ev[0], st));
@@ -480,7 +494,7 @@ lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *
             a.flags = flc;
             a.gap_out = nullptr;
             a.cache = cache; a.coords = coords;
-            a.n_partial = counters;
+            a.n_partial = s == stages - 1 ? counters : counters + 2;
             LAGP_CUDA(launch_design(P, a, st));
             launches++;
             if (timing) LAGP_CUDA(cudaEventRecord(ev[3], st));
@@ -494,6 +508,7 @@ lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *
             ma.mean = mean_out + m0; ma.s2 = s2_out + m0; ma.var = var_out ? var_out + m0 : nullptr;
             ma.use_smem = mp.smem ? 1 : 0;
             ma.ws = mlews;
+            ma.n_partial = s == stages - 1 ? counters : counters + 2;
             const int mgrid = (int)(mc < mp.grid ? mc : mp.grid);
             LAGP_CUDA(lagp::launch_mle(ma, mgrid, st));
             launches++;
@@ -519,9 +534,10 @@ lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *
         timing->total_ms = tot_ms;
         timing->launches = launches;
         timing->nn_fallbacks = host_counters[1];
+        timing->alc_form = P.form;
     }
     if (host_counters[0] > 0) {
-        fail(LAGP_PARTIAL, "%d location-stage(s) flagged EXHAUSTED or NONFINITE", host_counters[0]);
+        fail(LAGP_PARTIAL, "%d final-stage flag(s) EXHAUSTED or NONFINITE", host_counters[0]);
         st_ret = LAGP_PARTIAL;
     }
 cleanup:
@@ -535,7 +551,7 @@ lagp_status laGP_alc_batch(const double *X, int64_t N, int32_t p, const double *
                            double *mean_out, double *s2_out, double *var_out, uint32_t *flags_out, double *gap_out,
                            void *cuda_stream) {
     return laGP_alc_batch_ex(X, N, p, Z, XX, M, d, g, n0, n, Nprime, idx_out, mean_out, s2_out, var_out, flags_out,
-                             gap_out, LAGP_ALC_EXPLICIT, nullptr, cuda_stream);
+                             gap_out, LAGP_ALC_AUTO, nullptr, cuda_stream);
 }
 
 lagp_status laGP_alc_batch_host(const double *X, int64_t N, int32_t p, const double *Z, const double *XX, int64_t M,

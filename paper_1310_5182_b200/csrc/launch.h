@@ -61,9 +61,6 @@ IncPlan inc_plan(int n, int p, int Nprime, int Npad, size_t smem_optin);
 // alc_incremental_v2.cu: one barrier per step, 512 threads, 1-2 candidates per thread
 bool inc_v2_plan(int n, int p, int Nprime, size_t smem_optin, IncPlan &pl);
 cudaError_t launch_alc_incremental_v2(const AlcArgs &a, const IncPlan &pl, int grid, cudaStream_t st);
-// alc_incremental_cluster.cu: 2-CTA cluster per location (N' <= 1024, n <= 64, p in {2,3,8})
-bool inc_cluster_supported(int n, int p, int Nprime);
-cudaError_t launch_alc_inc_cluster(const AlcArgs &a, int num_sms, cudaStream_t st);
 cudaError_t launch_alc_incremental(const AlcArgs &a, const IncPlan &pl, int grid, cudaStream_t st);
 int alc_explicit_dmma_blocks_per_sm(int n, int p, int Npad);
 
@@ -85,6 +82,7 @@ struct MleArgs {
     double *mean, *s2, *var;  // [M] (var nullable): prediction at theta-hat
     double *ws;             // per-CTA matrices when they do not fit in shared memory
     int use_smem;
+    int *n_partial;         // nullable: count of locations flagged NONFINITE
 };
 size_t mle_smem_bytes(int n, int p);
 size_t mle_ws_bytes(int grid, int n, int p, bool use_smem);

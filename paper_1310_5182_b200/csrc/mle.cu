@@ -136,8 +136,9 @@ __device__ bool mle_chol(const double *D, double *L, int n, double rth, double e
             L[(kp + 1) * n + kp + 1] = pd2;
         }
     }
-    __syncthreads();
-    if (bad) return false;
+    // every thread reads `bad` before any can leave the barrier, so the next call's
+    // reset (tid 0, before its own barrier) cannot race with these reads
+    if (__syncthreads_or(bad)) return false;
     // every column below the diagonal is scaled (column n-1 has no such entries);
     // the diagonal takes its square roots last
     for (int k = tid; k < n; k += blockDim.x) L[k * n + k] = sqrt(L[k * n + k]);
@@ -462,14 +463,18 @@ mle_kernel(MleArgs A) {
         if (tid == 0) {
             const double sc = psi_p * (1.0 + A.eta - hAh) / (double)m;
             const double vr = m > 2 ? sc * (double)m / (double)(m - 2) : __longlong_as_double(0x7ff8000000000000LL);
+            const double qnan = __longlong_as_double(0x7ff8000000000000LL);
             if (!fin.ok || !isfinite(mu) || !isfinite(sc)) fl |= LAGP_FLAG_NONFINITE;
             A.theta_out[xi] = theta_hat;
             if (A.loglik_out) A.loglik_out[xi] = cur.l;
             if (A.iters_out) A.iters_out[xi] = it;
             if (A.flags_out) A.flags_out[xi] |= fl;
-            if (A.mean) A.mean[xi] = mu;
-            if (A.s2) A.s2[xi] = sc;
-            if (A.var) A.var[xi] = vr;
+            // K not positive definite at the prediction's theta: no factor, no
+            // prediction (NaN, as oracle_predict reports it)
+            if (A.mean) A.mean[xi] = fin.ok ? mu : qnan;
+            if (A.s2) A.s2[xi] = fin.ok ? sc : qnan;
+            if (A.var) A.var[xi] = fin.ok ? vr : qnan;
+            if ((fl & LAGP_FLAG_NONFINITE) && A.n_partial) atomicAdd(A.n_partial, 1);
         }
         __syncthreads();
     }

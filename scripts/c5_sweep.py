@@ -82,14 +82,14 @@ for p in [int(x) for x in a.ps.split(",")]:
                            paper_count_tflops=M * alc_paper_flops_per_location(6, n, Np) / (tm["alc_ms"] / 1e3) / 1e12)
                 if a.sample > 0 and form == "incremental":
                     import oracle
-                    from parity import compare, tau_for
+                    from parity import check
 
                     sel = np.arange(a.sample)
                     g = {k: v.cpu().numpy()[sel] for k, v in best.items() if hasattr(v, "cpu")}
                     t0 = time.time()
                     o = oracle.alc_batch(base["X"], base["Z"], base["XX"][sel], *args)
                     try:
-                        pr = compare(g, o, 6, float(np.std(base["Z"])), tau_for(p))
+                        pr = check(g, o, dict(base, XX=base["XX"][sel], n0=6, n=n, Nprime=Np), form)
                         rec["parity"] = {"ok": True, "sampled": len(sel), "identical": pr["identical"],
                                          "explained": len(pr["explained"]), "max_rel_s2": pr["max_rel_s2"]}
                     except AssertionError as ex:

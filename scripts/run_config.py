@@ -71,7 +71,7 @@ rep = dict(config=a.config, form=a.form, N=int(cfg["X"].shape[0]), M=int(M), p=i
            input_generation_s=gen_s)
 if a.sample > 0:
     import oracle
-    from parity import compare, tau_for
+    from parity import check, golden_tau
 
     sel = np.sort(np.random.default_rng(11).choice(M, min(a.sample, M), replace=False))
     g = {k: v.cpu().numpy()[sel] for k, v in r.items() if hasattr(v, "cpu")}
@@ -80,7 +80,7 @@ if a.sample > 0:
     rep["oracle_s"] = time.time() - t0
     rep["oracle_threads"] = o["threads"]
     try:
-        pr = compare(g, o, cfg["n0"], float(np.std(cfg["Z"])), tau_for(p))
+        pr = check(g, o, dict(cfg, XX=cfg["XX"][sel]), a.form, label=f"run_config-{a.config}")
         rep["parity"] = {"ok": True, "sampled": int(len(sel)), "identical": pr["identical"],
                          "explained": pr["explained"], "max_rel_mean": pr["max_rel_mean"],
                          "max_rel_s2": pr["max_rel_s2"]}

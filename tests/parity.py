@@ -1,31 +1,99 @@
-"""Parity rules between the CUDA path and the oracle (readings R17/R18).
+"""Parity rules between the CUDA path and the oracle (readings R17/R18/R19).
 
-* Index sequences: bit-exact. A divergence is *explained* only if the oracle's
-  top-2 relative gap at the first divergent step is below ``tau`` (the FP64
-  score noise of the explicit-inverse formulation for that input shape, R18);
-  otherwise it is a failure. Explained divergences are counted and must stay
-  <= ``max_explained`` (fraction) of the locations.
+* tau_cfg (R18): the oracle's own measured score noise on the inputs at hand — the
+  max over (up to) 16 of the compared locations and over every greedy step of
+  |Delta_explicit - Delta_ref| / max Delta_ref, where Delta_explicit are the
+  oracle's explicit-K^{-1} scores along its own trajectory and Delta_ref a fresh
+  long-double solve of the same Eq (5) closed form (``oracle.score_noise``). For
+  the full-size named configurations it is also stored, with the script that
+  measured it, in tests/golden/tau_cfg.json (scripts/measure_tau.py).
+* The tolerance of a form (``tau_form``): two evaluations whose relative score
+  errors are e_o (oracle) and e_g (GPU) can disagree on the argmax only where the
+  top-2 gap is below 2 (e_o + e_g), and their per-step gaps differ by at most that.
+  The GPU's explicit forms have the oracle's error scale (the same algorithm in
+  another summation order: e_g = e_o), the incremental form works on the Cholesky
+  factor, 10^2-10^4 x less noisy (e_g << e_o):
+      tau_form = 4 tau_cfg (explicit, explicit_dfma),  2 tau_cfg (incremental).
+* Index sequences: bit-exact. A divergence is *explained* only if, at the first
+  divergent step, both sides report a near tie (gap < 1e-12) or the oracle's gap
+  is below tau_form; otherwise it is a failure. The incremental form must have no
+  explained divergence at all unless the caller allows it; the explicit forms at
+  most 1 % of the locations. Explained divergences are reported (warning + a JSON
+  line in gpurun_out/parity_log.jsonl).
 * mean: |dmu| <= 1e-8 * max(|mu_oracle|, std(Z));  s2 and var: |ds2| <= 1e-8 * s2_oracle
-  (north_star "1e-8 relative"), checked on every location whose sequence matches.
-* flags: EXHAUSTED / SENTINEL bits must agree on matching locations.
+  (north_star "1e-8 relative", R17), on every location whose sequence matches.
+* flags on matching locations: SENTINEL and EXHAUSTED equal; NEAR_TIE equal wherever
+  the oracle's smallest gap is not within tau_form of the 1e-12 threshold.
+* per-step gaps (R19) on matching locations: |gap_gpu - gap_oracle| <= tau_form + 1e-12,
+  NaN (steps after an exhaustion) at the same steps.
 """
 from __future__ import annotations
 
+import json
+import os
+import warnings
+
 import numpy as np
 
+import oracle
+
 REL = 1e-8
+TIE = 1e-12
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FACTOR = {"incremental": 2.0, "explicit": 4.0, "explicit_dfma": 4.0}
+FACTOR["auto"] = FACTOR["incremental"]
 
 
-def tau_for(p: int) -> float:
-    # explicit-K^{-1} score noise scale (~2e-5 (2-d), ~4e-5 (3-d grid), ~6e-8 (8-d))
-    return 2e-4 if p <= 3 else 1e-6
+def tau_cfg(cfg: dict, orc: dict, k: int = 16) -> float:
+    """R18: the oracle's measured score noise on (up to) k of the compared
+    locations of ``cfg`` (X, XX, d, g, n0, n, Nprime) along its own trajectories."""
+    M = orc["idx"].shape[0]
+    sel = np.linspace(0, M - 1, min(k, M)).astype(int) if M > 0 else []
+    worst = 0.0
+    for i in sorted(set(int(v) for v in sel)):
+        nz, _ = oracle.score_noise(cfg["X"], cfg["XX"][i], orc["idx"][i], cfg["d"], cfg["g"], cfg["n0"], cfg["n"],
+                                   cfg["Nprime"])
+        nz = nz[np.isfinite(nz)]
+        if nz.size:
+            worst = max(worst, float(nz.max()))
+    return max(worst, 2.0 ** -52)
 
 
-def compare(gpu: dict, orc: dict, n0: int, zstd: float, tau: float, max_explained: float = 0.01,
-            min_explained_allow: int = 1):
+def golden_tau(name: str) -> float:
+    """tau_cfg of a full-size named configuration (tests/golden/tau_cfg.json)."""
+    with open(os.path.join(ROOT, "tests", "golden", "tau_cfg.json")) as f:
+        return float(json.load(f)["configs"][name]["tau_cfg"])
+
+
+def tau_form(tau: float, form: str) -> float:
+    return FACTOR[form] * tau
+
+
+def _log(rec: dict):
+    path = os.environ.get("LAGP_PARITY_LOG", os.path.join(ROOT, "gpurun_out", "parity_log.jsonl"))
+    try:
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        with open(path, "a") as f:
+            f.write(json.dumps(rec) + "\n")
+    except OSError:
+        pass
+
+
+def compare(gpu: dict, orc: dict, n0: int, zstd: float, tau: float, form: str = "incremental",
+            max_explained: float | None = None, tie_only: bool = False, label: str = ""):
+    """Check the GPU result against the oracle (module docstring). ``tau`` is
+    tau_cfg; the form's tolerance is derived from it. ``max_explained``: allowed
+    fraction of explained divergences (default 0 for the incremental form, 1 %
+    otherwise). ``tie_only``: a divergence is explained only where both sides
+    report a gap below 1e-12. Returns a report dict."""
+    tf = tau_form(tau, form)
+    if max_explained is None:
+        max_explained = 0.0 if FACTOR[form] == FACTOR["incremental"] else 0.01
     idx_g = np.asarray(gpu["idx"])
     idx_o = np.asarray(orc["idx"])
     M, n = idx_o.shape
+    gaps_o = np.asarray(orc["gaps"])
+    gaps_g = np.asarray(gpu["gaps"]) if "gaps" in gpu else None
     same = (idx_g == idx_o).all(axis=1)
     explained, failures = [], []
     for i in np.where(~same)[0]:
@@ -33,18 +101,24 @@ def compare(gpu: dict, orc: dict, n0: int, zstd: float, tau: float, max_explaine
         if t < n0:
             failures.append((int(i), t, "NN part differs"))
             continue
-        gap = orc["gaps"][i, t - n0]
-        if gap < max(1e-12, tau):
-            explained.append((int(i), t, float(gap)))
+        go = float(gaps_o[i, t - n0])
+        gg = float(gaps_g[i, t - n0]) if gaps_g is not None else float("nan")
+        both_tie = go < TIE and gg < TIE
+        if both_tie or (not tie_only and go < tf):
+            explained.append((int(i), t, go, gg))
         else:
-            failures.append((int(i), t, f"oracle gap {gap:.3e} >= tau {tau:.1e}"))
+            failures.append((int(i), t, f"oracle gap {go:.3e}, gpu gap {gg:.3e} >= tau_form {tf:.2e}"))
     assert not failures, f"unexplained index divergences: {failures[:10]}"
-    allow = max(min_explained_allow, int(max_explained * M))
+    allow = int(np.floor(max_explained * M))
+    if explained:
+        warnings.warn(f"parity {label} {form}: {len(explained)} explained divergence(s) of {M}: {explained[:5]}")
+    _log(dict(label=label, form=form, M=int(M), identical=int(same.sum()), explained=len(explained),
+              detail=explained[:20], tau_cfg=tau, tau_form=tf))
     assert len(explained) <= allow, f"{len(explained)} explained divergences > {allow}: {explained[:10]}"
+    ok = same
     m_g, m_o = np.asarray(gpu["mean"]), orc["mean"]
     s_g, s_o = np.asarray(gpu["s2"]), orc["s2"]
     v_g, v_o = np.asarray(gpu["var"]), orc["var"]
-    ok = same
     dm = np.abs(m_g - m_o)[ok]
     lim_m = REL * np.maximum(np.abs(m_o[ok]), zstd)
     assert (dm <= lim_m).all(), f"mean off: max rel {np.max(dm / lim_m) * REL:.3e}"
@@ -54,8 +128,33 @@ def compare(gpu: dict, orc: dict, n0: int, zstd: float, tau: float, max_explaine
     assert (np.abs(v_g - v_o)[fin] <= REL * v_o[fin]).all()
     assert np.array_equal(np.isnan(v_g[ok]), np.isnan(v_o[ok]))
     fg = np.asarray(gpu["flags"]).astype(np.uint32)
+    fo = np.asarray(orc["flags"]).astype(np.uint32)
     for bit in (2, 4):  # SENTINEL, EXHAUSTED
-        assert np.array_equal(fg[ok] & bit, orc["flags"][ok] & bit), f"flag bit {bit} differs"
-    return dict(M=M, identical=int(same.sum()), explained=explained,
+        assert np.array_equal(fg[ok] & bit, fo[ok] & bit), f"flag bit {bit} differs"
+    # NEAR_TIE (bit 0): equal wherever the oracle's smallest gap is clear of the threshold
+    # by more than the form's noise
+    with np.errstate(invalid="ignore"):
+        gmin = np.where(np.isnan(gaps_o), np.inf, gaps_o).min(axis=1) if gaps_o.shape[1] else np.full(M, np.inf)
+    clear = ok & (gmin >= TIE + tf)
+    nt_diff = np.where(clear & ((fg & 1) != (fo & 1)))[0]
+    assert nt_diff.size == 0, f"NEAR_TIE differs at {nt_diff[:10].tolist()} (oracle min gaps {gmin[nt_diff[:5]]})"
+    max_gap_diff = None
+    if gaps_g is not None and gaps_o.shape[1]:
+        go, gg = gaps_o[ok], gaps_g[ok]
+        assert np.array_equal(np.isnan(go), np.isnan(gg)), "gap NaN pattern differs"
+        dg = np.abs(np.where(np.isnan(go), 0.0, go) - np.where(np.isnan(gg), 0.0, gg))
+        max_gap_diff = float(dg.max(initial=0.0))
+        assert max_gap_diff <= tf + TIE, f"per-step gap differs by {max_gap_diff:.3e} > tau_form {tf:.2e}"
+    return dict(M=M, identical=int(same.sum()), explained=explained, tau_cfg=tau, tau_form=tf,
+                near_tie=int((fo[ok] & 1).sum()), max_gap_diff=max_gap_diff,
                 max_rel_mean=float(np.max(dm / np.maximum(np.abs(m_o[ok]), zstd), initial=0.0)),
                 max_rel_s2=float(np.max(ds / s_o[ok], initial=0.0)))
+
+
+def check(gpu: dict, orc: dict, cfg: dict, form: str, tau: float | None = None, **kw):
+    """compare() with tau_cfg measured on these inputs (cfg's XX rows are the
+    compared locations) unless given, and zstd = std(Z)."""
+    if tau is None:
+        tau = tau_cfg(cfg, orc)
+    kw.setdefault("label", str(cfg.get("name", "")))
+    return compare(gpu, orc, cfg["n0"], float(np.std(cfg["Z"])), tau, form=form, **kw)

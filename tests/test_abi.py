@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(lagp):
     lib = lagp.lib()
     for s in declared_symbols():
         assert hasattr(lib, s), s
-    assert lagp.abi_version() == 2
+    assert lagp.abi_version() == 3
 
 
 def test_library_is_sm100a_only(lagp):

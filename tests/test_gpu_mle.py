@@ -11,7 +11,7 @@ import pytest
 
 import oracle
 from lagp_data import make_config
-from parity import compare, tau_for
+from parity import compare, tau_cfg, tau_form
 
 pytestmark = pytest.mark.gpu
 REL = 1e-8
@@ -75,12 +75,19 @@ def test_mle_exhausted_prefix_and_failure(torch_dev, lagp):
     X[idx[2, 1]] = X[idx[2, 0]]  # duplicate rows with eta = 0: K singular -> MLE_FAIL
     g = 0.0
     r = lagp.mle(T(torch, dev, X), T(torch, dev, Z), T(torch, dev, XX), T(torch, dev, idx), 0.3, 1e-3, 10.0, g)
-    r = {k: v.cpu().numpy() for k, v in r.items()}
+    assert r["status"] == lagp.LAGP_PARTIAL  # the failed location is flagged NONFINITE
+    r = {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in r.items()}
     th, lh, its, fl = oracle.mle(X[idx[1, :17]], Z[idx[1, :17]], 0.3, 1e-3, 10.0, g)
     assert abs(r["theta"][1] - th) <= REL * th
     assert r["flags"][2] & lagp.FLAG_MLE_FAIL
     assert r["theta"][2] == 0.3
     assert oracle.mle(X[idx[2]], Z[idx[2]], 0.3, 1e-3, 10.0, g)[3] & oracle.MLE_FLAG_FAIL
+    # K is singular at every theta: no prediction (NaN, as oracle_predict / oracle_local_fit report it)
+    assert r["flags"][2] & lagp.FLAG_NONFINITE
+    assert np.isnan(r["mean"][2]) and np.isnan(r["s2"][2]) and np.isnan(r["var"][2])
+    with pytest.raises(np.linalg.LinAlgError):
+        oracle.predict(X[idx[2]], Z[idx[2]], XX[2], 0.3, g)
+    assert np.isfinite(r["mean"][[0, 1, 3]]).all() and not (r["flags"][[0, 1, 3]] & lagp.FLAG_NONFINITE).any()
 
 
 @pytest.mark.parametrize("form", ["explicit", "incremental"])
@@ -95,7 +102,10 @@ def test_alc_batch_per_location_theta(torch_dev, lagp, form):
     rows = [oracle.alc_batch(cfg["X"], cfg["Z"], cfg["XX"][i:i + 1], th[i], cfg["g"], cfg["n0"], cfg["n"],
                              cfg["Nprime"]) for i in range(40)]
     o = {k: np.concatenate([rr[k] for rr in rows]) for k in ("idx", "mean", "s2", "var", "flags", "gaps")}
-    compare(g, o, cfg["n0"], float(np.std(cfg["Z"])), tau_for(2))
+    # R18 with each location's own theta: the oracle's score noise on 16 of the locations
+    tau = max(tau_cfg(dict(cfg, XX=cfg["XX"][i:i + 1], d=float(th[i])), {"idx": o["idx"][i:i + 1]})
+              for i in range(0, 40, 3))
+    compare(g, o, cfg["n0"], float(np.std(cfg["Z"])), tau, form=form, label="per-location-theta")
 
 
 @pytest.mark.parametrize(
@@ -108,7 +118,6 @@ def test_local_fit_vs_oracle(torch_dev, lagp, name, M, N, over, form):
     cfg = make_config(name, M=M, N=N, **over)
     d0 = cfg["d"]
     lo, hi = 1e-3 * d0, 10.0 * d0
-    p = cfg["X"].shape[1]
     args = (cfg["X"], cfg["Z"], cfg["XX"])
     for stages in (1, 2):
         r = lagp.local_fit(*(T(torch, dev, a) for a in args), d0, lo, hi, cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"],
@@ -121,7 +130,8 @@ def test_local_fit_vs_oracle(torch_dev, lagp, name, M, N, over, form):
             des = oracle.local_design(cfg["X"], cfg["Z"], cfg["XX"][i], th, cfg["g"], cfg["n0"], cfg["n"],
                                       cfg["Nprime"])
             t = int(np.argmax(g["idx"][i] != o["idx"][i]))
-            assert t >= cfg["n0"] and des["gaps"][t - cfg["n0"]] < max(1e-12, tau_for(p)), (i, t)
+            tau = tau_cfg(dict(cfg, XX=cfg["XX"][i:i + 1], d=float(th)), {"idx": des["idx"][None, :]})
+            assert t >= cfg["n0"] and des["gaps"][t - cfg["n0"]] < max(1e-12, tau_form(tau, form)), (i, t)
         assert (~same).sum() <= max(1, M // 50)
         dth = np.abs(g["theta"] - o["theta"])[:, same]
         assert (dth <= REL * o["theta"][:, same]).all(), np.max(dth / o["theta"][:, same])

@@ -5,7 +5,7 @@ import pytest
 
 import oracle
 from lagp_data import make_config
-from parity import compare, tau_for
+from parity import check, golden_tau
 
 pytestmark = pytest.mark.gpu
 
@@ -208,7 +208,7 @@ def test_alc_batch_vs_oracle(torch_dev, lagp, name, M, N, over, form):
     cfg = make_config(name, M=M, N=N, **over)
     g, o = run_both(torch, dev, lagp, cfg, form=form)
     p = cfg["X"].shape[1]
-    rep = compare(g, o, cfg["n0"], float(np.std(cfg["Z"])), tau_for(p))
+    rep = check(g, o, cfg, form)
     print(name, form, rep)
 
 
@@ -222,7 +222,7 @@ def test_large_pool_explicit(torch_dev, lagp, form):
     torch, dev = torch_dev
     cfg = make_config("C5_2d", M=3, Nprime=12000, n=20)
     g, o = run_both(torch, dev, lagp, cfg, form=form)
-    compare(g, o, cfg["n0"], float(np.std(cfg["Z"])), tau_for(2))
+    check(g, o, cfg, form)
 
 
 def test_incremental_rejects_large_pool(torch_dev, lagp):
@@ -327,7 +327,7 @@ def test_full_size_C2_sampled(torch_dev, lagp, form):
     sel = np.sort(np.random.default_rng(7).choice(cfg["XX"].shape[0], 48, replace=False))
     g = {k: v.cpu().numpy()[sel] for k, v in r.items() if hasattr(v, "cpu")}
     o = oracle.alc_batch(cfg["X"], cfg["Z"], cfg["XX"][sel], cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"])
-    compare(g, o, cfg["n0"], float(np.std(cfg["Z"])), tau_for(8))
+    check(g, o, cfg, form, tau=golden_tau("C2"))
     # properties at every location: indices distinct and in range, s2 > 0
     idx = r["idx"].cpu().numpy()
     assert (idx >= 0).all() and (idx < cfg["X"].shape[0]).all()
@@ -376,7 +376,7 @@ def test_incremental_large_pools(torch_dev, lagp, Nprime, p, n):
     X, Z, XX = _synthetic(Nprime + p, 40000, 6, p)
     cfg = dict(X=X, Z=Z, XX=XX, d=0.02 * p, g=1e-4, n0=6, n=n, Nprime=Nprime)
     g, o = run_both(torch, dev, lagp, cfg, form="incremental")
-    compare(g, o, 6, float(np.std(Z)), tau_for(p))
+    check(g, o, cfg, "incremental")
 
 
 @pytest.mark.parametrize("p", [1, 5, 7])
@@ -387,15 +387,18 @@ def test_generic_dimension(torch_dev, lagp, p, form):
     X, Z, XX = _synthetic(100 + p, 6000, 10, p)
     cfg = dict(X=X, Z=Z, XX=XX, d=0.05 * p, g=1e-4, n0=4, n=30, Nprime=400)
     g, o = run_both(torch, dev, lagp, cfg, form=form)
-    compare(g, o, 4, float(np.std(Z)), tau_for(p))
+    check(g, o, cfg, form)
 
 
 @pytest.mark.parametrize("env", [{"LAGP_V2_CPT": "4"}, {"LAGP_V2_CPT": "1"}, {"LAGP_V2_TFIRST": "1"},
-                                 {"LAGP_V2_NOSTAGGER": "1"}, {"LAGP_INC_V1": "1"}, {"LAGP_NN_MMA": "1"}])
+                                 {"LAGP_V2_NOSTAGGER": "1"}, {"LAGP_INC_V1": "1"}, {"LAGP_NN_MMA": "1"},
+                                 {"LAGP_NN_MMA": "0"}, {"LAGP_NN_CELLS": "0"}, {"LAGP_NN_Q": "4"},
+                                 {"LAGP_NN_Q": "8"}, {"LAGP_NN_Q": "16"}])
 def test_kernel_variants_agree(torch_dev, lagp, env):
-    """The A/B variants (CTA shapes, tier order, phase order, v1 kernel, TF32 NN
-    filter) against the oracle on the same C2 sample as the default path, with
-    n = 64 so the shared-memory, tensor-memory and slab tiers are all in use."""
+    """Every A/B switch of the library (CTA shapes, tier order, phase order, v1
+    kernel; NN: TF32 filter on/off, no spatial cells, 4/8/16-query groups) against
+    the oracle on the same C2 sample as the default path, with n = 64 so the
+    shared-memory, tensor-memory and slab tiers are all in use."""
     import os
 
     torch, dev = torch_dev
@@ -410,4 +413,38 @@ def test_kernel_variants_agree(torch_dev, lagp, env):
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
-    compare(g, o, cfg["n0"], float(np.std(cfg["Z"])), tau_for(8))
+    check(g, o, cfg, "incremental")
+
+
+def test_north_star_entry_point(torch_dev, lagp):
+    """laGP_alc_batch itself — the north_star signature, called through ctypes
+    with device data and every output — against the oracle; it resolves to the
+    incremental form (LAGP_ALC_AUTO), which lagp_timing reports; pools beyond the
+    incremental kernels resolve to the paper's explicit form."""
+    import ctypes
+
+    torch, dev = torch_dev
+    cfg = make_config("C2", M=64, N=20000)
+    X, Z, XX = (T(torch, dev, cfg[k]) for k in ("X", "Z", "XX"))
+    M, n, n0 = XX.shape[0], cfg["n"], cfg["n0"]
+    out = dict(idx=torch.empty((M, n), dtype=torch.int32, device=dev),
+               mean=torch.empty(M, dtype=torch.float64, device=dev), s2=torch.empty(M, dtype=torch.float64, device=dev),
+               var=torch.empty(M, dtype=torch.float64, device=dev), flags=torch.empty(M, dtype=torch.int32, device=dev),
+               gaps=torch.empty((M, n - n0), dtype=torch.float64, device=dev))
+    vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    st = lagp.lib().laGP_alc_batch(vp(X), X.shape[0], X.shape[1], vp(Z), vp(XX), M, cfg["d"], cfg["g"], n0, n,
+                                   cfg["Nprime"], vp(out["idx"]), vp(out["mean"]), vp(out["s2"]), vp(out["var"]),
+                                   vp(out["flags"]), vp(out["gaps"]),
+                                   ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+    assert st == lagp.LAGP_OK, lagp.last_error()
+    g = {k: v.cpu().numpy() for k, v in out.items()}
+    o = oracle.alc_batch(cfg["X"], cfg["Z"], cfg["XX"], cfg["d"], cfg["g"], n0, n, cfg["Nprime"])
+    rep = check(g, o, cfg, "incremental", label="laGP_alc_batch")
+    assert rep["identical"] == M
+    r = lagp.alc_batch(X, Z, XX[:4], cfg["d"], cfg["g"], n0, n, cfg["Nprime"], timing=True)
+    assert r["timing"]["alc_form"] == "incremental"
+    assert torch.equal(r["idx"], out["idx"][:4])
+    big = make_config("C5_2d", M=2, Nprime=12000, n=20)
+    rb = lagp.alc_batch(*(T(torch, dev, big[k]) for k in ("X", "Z", "XX")), big["d"], big["g"], big["n0"], big["n"],
+                        big["Nprime"], timing=True)
+    assert rb["timing"]["alc_form"] == "explicit"

@@ -7,7 +7,7 @@ import pytest
 
 import oracle
 from lagp_data import make_config
-from parity import compare, tau_for
+from parity import check
 
 pytestmark = pytest.mark.gpu
 
@@ -49,6 +49,8 @@ def test_alc_batch_sep_vs_oracle(torch_dev, lagp, name, M, N, theta, over, form)
                            cfg["n"], cfg["Nprime"], form=form, gaps=True)
     g = {k: v.cpu().numpy() for k, v in r.items() if hasattr(v, "cpu")}
     o = oracle.alc_batch_sep(X, Z, XX, theta, cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"])
-    rep = compare(g, o, cfg["n0"], float(np.std(Z)), tau_for(X.shape[1]))
+    # R18 on the rescaled inputs the oracle ran on (isotropic with d = 1, reading R23)
+    scaled = dict(cfg, X=oracle.sep_scale(X, theta), XX=oracle.sep_scale(XX, theta), d=1.0)
+    rep = check(g, o, scaled, form, label=f"sep-{name}")
     print(name, form, rep)
 

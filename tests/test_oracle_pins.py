@@ -386,6 +386,7 @@ def test_worked_example_WA():
     assert r["idx"].tolist() == gold["idx"]
     for v, ref, rt in zip(r["best"], gold["best_delta"], gold["best_delta_rtol"]):
         assert abs(v - ref) <= rt * ref
+    assert np.allclose(r["gaps"], gold["gaps"], rtol=0, atol=1e-8)
     assert abs(r["mean"] - gold["mean"]) <= 1e-13
     assert abs(r["s2"] - gold["s2"]) <= 1e-10 * gold["s2"]
     assert abs(r["var"] - gold["var"]) <= 1e-10 * gold["var"]
@@ -402,6 +403,21 @@ def test_worked_example_WB():
     assert oracle.nn(X, x, 8)[0].tolist() == gold["nn8"]
     assert abs(r["mean"] - gold["mean"]) <= 1e-12
     assert abs(r["s2"] - gold["s2"]) <= 1e-10 * gold["s2"]
+    assert abs(r["var"] - gold["var"]) <= 1e-10 * gold["var"]
+    # the greedy steps' best reductions and top-2 gaps (explicit-inverse noise: eps * cond)
+    assert np.allclose(r["best"], gold["best_delta"], rtol=1e-8, atol=0)
+    assert np.allclose(r["gaps"], gold["gaps"], rtol=0, atol=1e-8)
+
+
+def test_worked_examples_regenerate():
+    """tests/golden/worked_examples.json is what scripts/golden_worked_examples.py
+    (60-digit decimal brute force, no oracle import) produces."""
+    import subprocess
+    import sys
+
+    script = os.path.join(os.path.dirname(os.path.dirname(__file__)), "scripts", "golden_worked_examples.py")
+    r = subprocess.run([sys.executable, script, "--check"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
 
 
 # --------------------------------------------- degenerate cases (R12, S:269)
@@ -434,3 +450,36 @@ def test_sentinel_skips_duplicate_but_continues():
     assert r["flags"] & oracle.FLAG_SENTINEL
     assert not r["flags"] & oracle.FLAG_EXHAUSTED
     assert 1 not in r["idx"].tolist()
+
+
+def test_score_noise_reference_pinned_to_decimal_brute_force():
+    """oracle.score_noise (reading R18's tau_cfg): its long-double fresh-solve
+    reference reproduces the 60-digit brute-force top-2 gaps of W-A and W-B, and
+    its noise bounds the explicit-inverse error of the oracle's own best scores."""
+    gold = json.load(open(GOLDEN))
+    X = (np.arange(11) / 10.0)[:, None]
+    Y = np.sin(2 * math.pi * X[:, 0])
+    rng = np.random.default_rng(42)
+    XB = rng.random((30, 2))
+    xb = rng.random(2)
+    YB = np.sin(5 * XB[:, 0]) + np.cos(3 * XB[:, 1])
+    for key, (XS, YS, x, d, n0, n, Np) in {"W-A": (X, Y, np.array([0.43]), 0.1, 2, 5, 11),
+                                            "W-B": (XB, YB, xb, 0.05, 3, 8, 30)}.items():
+        r = oracle.local_design(XS, YS, x, d, 1e-4, n0, n, Np)
+        noise, ref_gap = oracle.score_noise(XS, x, r["idx"], d, 1e-4, n0, n, Np)
+        assert np.allclose(ref_gap, gold[key]["gaps"], rtol=0, atol=1e-12), key
+        err = np.abs(r["best"] - np.array(gold[key]["best_delta"])) / np.array(gold[key]["best_delta"])
+        assert (err <= noise * (1 + 1e-6) + 1e-15).all(), (key, err, noise)
+        assert (noise > 0).all() and (noise < 1e-6).all()
+
+
+def test_score_noise_small_when_well_conditioned():
+    """With a large nugget K_j is well conditioned (kappa <= 1 + j/g, App A.6):
+    the explicit-inverse scores agree with the fresh long-double solve to ~1e-13."""
+    rng = np.random.default_rng(9)
+    X = rng.random((200, 3))
+    x = rng.random(3)
+    r = oracle.local_design(X, np.zeros(200), x, 0.3, 0.5, 4, 20, 120)
+    noise, gap = oracle.score_noise(X, x, r["idx"], 0.3, 0.5, 4, 20, 120)
+    assert noise.max() < 1e-12
+    assert np.allclose(gap, r["gaps"], rtol=0, atol=1e-12)
