@@ -11,9 +11,12 @@
  *    tensors), row-major, FP64 unless noted; indices are 0-based int32.
  *    laGP_alc_batch_host is the one exception (HOST pointers, see below).
  *  - The caller owns every input and output buffer. The library owns only a
- *    per-call workspace, allocated stream-ordered (cudaMallocAsync) and freed
- *    before return. No global mutable state except the thread-local error
- *    string returned by lagp_last_error().
+ *    per-call workspace, allocated stream-ordered from the library's own memory
+ *    pool (one cudaMemPool per device, created on first use; the device's default
+ *    pool is not touched) and freed back to that pool before return. The pool
+ *    keeps up to 4 GiB of freed workspace mapped so that repeated calls do not
+ *    re-map it; lagp_release_workspace() returns it to the driver. Other global
+ *    state: the pool handles and the thread-local error string (lagp_last_error).
  *  - Work is enqueued on `cuda_stream` (a cudaStream_t; NULL = legacy default
  *    stream) and the call synchronises that stream before returning, so a
  *    status can report per-location outcomes. Reentrant on distinct streams.
@@ -301,6 +304,10 @@ lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *
                            double g, int32_t n0, int32_t n, int32_t Nprime, int32_t stages, int32_t alc_form,
                            int32_t *idx_out, double *theta_out, double *mean_out, double *s2_out,
                            double *var_out, uint32_t *flags_out, lagp_timing *timing, void *cuda_stream);
+
+/* Return the current device's cached workspace memory (the library's pool) to
+ * the driver; synchronises the device. LAGP_OK or LAGP_ECUDA. */
+lagp_status lagp_release_workspace(void);
 
 /* Thread-local message for the last non-OK status of this thread. */
 const char *lagp_last_error(void);

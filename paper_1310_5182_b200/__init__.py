@@ -64,6 +64,12 @@ def abi_version() -> int:
     return lib().lagp_abi_version()
 
 
+def release_workspace():
+    """lagp_release_workspace: return the library's cached workspace memory on the
+    current device to the driver."""
+    _check(lib().lagp_release_workspace())
+
+
 def _check(st: int, ok=(LAGP_OK,)):
     if st not in ok:
         raise LagpError(st, last_error())

@@ -32,6 +32,7 @@ EXPORTS = (
     "laGP_local_fit",
     "laGP_exp_nonpos",
     "laGP_alc_batch_sep",
+    "lagp_release_workspace",
     "lagp_last_error",
     "lagp_abi_version",
 )
@@ -81,6 +82,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.laGP_alc_batch_sep.argtypes = [_vp, _i64, _i32, _vp, _vp, _i64, ctypes.POINTER(ctypes.c_double), _dbl,
                                        _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
                                        ctypes.POINTER(Timing), _vp]
+    lib.lagp_release_workspace.argtypes = []
     for f in EXPORTS[:-2]:
         getattr(lib, f).restype = ctypes.c_int
     lib.lagp_last_error.argtypes = []

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 
 #include "lagp_internal.cuh"
@@ -52,9 +53,42 @@ int num_sms() {
 
 bool finite_pos(double v) { return std::isfinite(v) && v > 0.0; }
 
-// Stream-ordered workspace allocations (cudaMallocAsync from the device's current
-// memory pool, whose attributes this library leaves as the caller set them),
-// released in one place.
+// The library's own stream-ordered memory pool, one per device, created on first
+// use: per-call workspaces come from it (cudaMallocFromPoolAsync) and go back to it
+// at the end of the call. Its release threshold (LAGP_POOL_KEEP bytes) keeps the
+// memory of repeated calls mapped instead of returning it to the driver at every
+// synchronisation (re-mapping it cost ~7 ms per C2 call); the device's default
+// pool, which other libraries (e.g. PyTorch) may use, is left untouched.
+// lagp_release_workspace() returns the cached memory to the driver.
+constexpr uint64_t LAGP_POOL_KEEP = 4ull << 30;
+constexpr int LAGP_MAX_DEVICES = 64;
+cudaMemPool_t g_pool[LAGP_MAX_DEVICES] = {};
+std::mutex g_pool_mu;
+
+cudaError_t lib_pool(cudaMemPool_t *out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= LAGP_MAX_DEVICES) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (!g_pool[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pool;
+        e = cudaMemPoolCreate(&pool, &props);
+        if (e != cudaSuccess) return e;
+        uint64_t keep = LAGP_POOL_KEEP;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        g_pool[dev] = pool;
+    }
+    *out = g_pool[dev];
+    return cudaSuccess;
+}
+
+// Stream-ordered workspace allocations released in one place.
 struct Workspace {
     cudaStream_t st;
     void *ptrs[16];
@@ -62,7 +96,10 @@ struct Workspace {
     explicit Workspace(cudaStream_t s) : st(s) {}
     cudaError_t alloc(void **p, size_t bytes) {
         if (bytes == 0) bytes = 16;
-        cudaError_t e = cudaMallocAsync(p, bytes, st);
+        cudaMemPool_t pool;
+        cudaError_t e = lib_pool(&pool);
+        if (e != cudaSuccess) return e;
+        e = cudaMallocFromPoolAsync(p, bytes, pool, st);
         if (e == cudaSuccess) ptrs[n++] = *p;
         return e;
     }
@@ -98,6 +135,14 @@ lagp_status check_batch_args(const double *X, int64_t N, int32_t p, const double
 extern "C" {
 
 const char *lagp_last_error(void) { return g_err.c_str(); }
+
+lagp_status lagp_release_workspace(void) {
+    cudaMemPool_t pool;
+    cudaError_t e = lib_pool(&pool);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemPoolTrimTo(pool, 0);
+    return e == cudaSuccess ? LAGP_OK : cuda_fail(e, "lagp_release_workspace");
+}
 int lagp_abi_version(void) { return LAGP_ABI_VERSION; }
 
 }  // extern "C"

@@ -62,7 +62,8 @@ def test_fullsize_sampled_parity(torch_dev, lagp, name, form, sample):
     sel = np.sort(np.random.default_rng(11).choice(M, sample, replace=False))
     g = {k: v.cpu().numpy()[sel] for k, v in r.items() if hasattr(v, "cpu")}
     o = oracle.alc_batch(X, Z, XX[sel], cfg["d"], cfg["g"], cfg["n0"], n, cfg["Nprime"])
-    rep = check(g, o, cfg, form, tau=golden_tau(name), label=f"fullsize-{name}")
+    rep = check(g, o, dict(cfg, XX=XX[sel]), form, tau=golden_tau(name), label=f"fullsize-{name}",
+                **({"max_explained": 0.0} if form == "incremental" else {}))
     print(name, form, rep)
     if name == "C3":
         # the grid's exact distance ties: 32 of the locations the GPU flags NEAR_TIE,
@@ -73,7 +74,12 @@ def test_fullsize_sampled_parity(torch_dev, lagp, name, form, sample):
         sel = np.sort(np.random.default_rng(12).choice(nt, min(32, nt.size), replace=False))
         g = {k: v.cpu().numpy()[sel] for k, v in r.items() if hasattr(v, "cpu")}
         o = oracle.alc_batch(X, Z, XX[sel], cfg["d"], cfg["g"], cfg["n0"], n, cfg["Nprime"])
-        rep = check(g, o, cfg, form, tau=golden_tau(name), tie_only=True, max_explained=1.0,
+        rep = check(g, o, dict(cfg, XX=XX[sel]), form, tau=golden_tau(name), tie_only=True, max_explained=1.0,
                     label="fullsize-C3-near-tie")
-        assert (o["flags"] & 1).sum() >= len(sel) // 2, "the oracle sees the near ties too"
+        # the long-double reference sees the ties too (the explicit-inverse oracle's own
+        # gaps at an exact tie are noise, ~1e-8 here)
+        from parity import noise_matrix
+
+        _, ref_gap = noise_matrix(dict(cfg, XX=XX[sel]), o, with_ref_gap=True)
+        assert (np.nanmin(ref_gap, axis=1) < 1e-12).sum() >= len(sel) // 2
         print("C3 near-tie sample", rep)

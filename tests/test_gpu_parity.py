@@ -208,7 +208,9 @@ def test_alc_batch_vs_oracle(torch_dev, lagp, name, M, N, over, form):
     cfg = make_config(name, M=M, N=N, **over)
     g, o = run_both(torch, dev, lagp, cfg, form=form)
     p = cfg["X"].shape[1]
-    rep = check(g, o, cfg, form)
+    # the incremental form on the named workloads: no divergence at all
+    strict = form == "incremental" and not over and N is None and name in ("C1", "C2", "C3", "C3j", "C4")
+    rep = check(g, o, cfg, form, **({"max_explained": 0.0} if strict else {}))
     print(name, form, rep)
 
 
@@ -327,7 +329,8 @@ def test_full_size_C2_sampled(torch_dev, lagp, form):
     sel = np.sort(np.random.default_rng(7).choice(cfg["XX"].shape[0], 48, replace=False))
     g = {k: v.cpu().numpy()[sel] for k, v in r.items() if hasattr(v, "cpu")}
     o = oracle.alc_batch(cfg["X"], cfg["Z"], cfg["XX"][sel], cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"])
-    check(g, o, cfg, form, tau=golden_tau("C2"))
+    check(g, o, dict(cfg, XX=cfg["XX"][sel]), form, tau=golden_tau("C2"),
+          **({"max_explained": 0.0} if form == "incremental" else {}))
     # properties at every location: indices distinct and in range, s2 > 0
     idx = r["idx"].cpu().numpy()
     assert (idx >= 0).all() and (idx < cfg["X"].shape[0]).all()
