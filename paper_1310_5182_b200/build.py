@@ -28,31 +28,70 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+OBJ = os.path.join(ROOT, "build", "obj")
+
+
+def _headers():
+    return (glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
+            + [os.path.join(ROOT, "include", "lagp.h")])
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
-    deps.append(os.path.join(ROOT, "include", "lagp.h"))
-    return any(os.path.getmtime(f) > t for f in deps)
+    return any(os.path.getmtime(f) > t for f in sources() + _headers())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not (force or _stale()):
-        return LIB
+def _nvcc() -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
     if os.path.exists("/usr/local/cuda/bin/nvcc") and nvcc == "nvcc":
         nvcc = "/usr/local/cuda/bin/nvcc"
-    cmd = [nvcc, *NVCC_FLAGS, "-shared", "-o", LIB + ".tmp", *sources()]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    return nvcc
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """One object per .cu (compiled in parallel, reused while it is newer than its
+    source and every header), then one shared-library link."""
+    if not (force or _stale()):
+        return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
+    nvcc = _nvcc()
+    os.makedirs(OBJ, exist_ok=True)
+    th = max([os.path.getmtime(f) for f in _headers()] + [0.0])
+
+    def compile_one(src):
+        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(th, os.path.getmtime(src)):
+            return obj, "", 0
+        r = subprocess.run([nvcc, *NVCC_FLAGS, "-c", "-o", obj + ".tmp", src], capture_output=True, text=True)
+        if r.returncode == 0:
+            with open(obj + ".ptxas", "w") as f:
+                f.write(r.stderr)
+            os.replace(obj + ".tmp", obj)
+        return obj, r.stdout + r.stderr, r.returncode
+
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        res = list(ex.map(compile_one, sources()))
+    bad = [out for _, out, rc in res if rc != 0]
+    if bad:
+        sys.stderr.write("\n".join(bad))
+        raise RuntimeError("nvcc failed building liblagp_b200.so")
+    objs = [o for o, _, _ in res]
+    r = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+                        "-o", LIB + ".tmp", *objs], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building liblagp_b200.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking liblagp_b200.so")
     os.replace(LIB + ".tmp", LIB)
-    with open(os.path.join(PKG, "ptxas_report.txt"), "w") as f:
-        f.write(r.stderr)
+    report = "".join(out for _, out, _ in res)
+    if verbose:
+        sys.stderr.write(report)
+    with open(os.path.join(PKG, "ptxas_report.txt"), "w") as f:  # ptxas -v of every object
+        for o in objs:
+            if os.path.exists(o + ".ptxas"):
+                f.write(open(o + ".ptxas").read())
     return LIB
 
 
