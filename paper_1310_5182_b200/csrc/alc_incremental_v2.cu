@@ -39,6 +39,8 @@
 #include <cuda_runtime.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "block_ops.cuh"
 #include "launch.h"
 
@@ -61,22 +63,22 @@ struct V2T {
     static constexpr int value = (65536 / TH) / 2 / CPT;
 };
 
-// warp post record (doubles): key | gidx,pos | key2 | - | x[8] | rrho z y - | w[R] | w[TMEM part]
+// warp post record (doubles): key | gidx,pos | key2 | - | x[8] | s cov t - | w[R]
 enum { RK = 0, RI = 1, RK2 = 2, RX = 4, RRHO = 12, RZN = 13, RYN = 14, RW = 16 };
-__host__ __device__ constexpr int v2_rec(int R, int T) { return RW + R + T; }
+__host__ __device__ constexpr int v2_rec(int R) { return RW + R; }
 
 // ---- tensor memory as per-thread storage (tcgen05; thread-private lane rows)
-__device__ __forceinline__ void tm_ld8(uint32_t taddr, double (&v)[4]) {
-    uint32_t r[8];
+// 2E columns (E doubles) of this thread's row; tm_wait_ld() before using r
+template <int E>
+__device__ __forceinline__ void tm_ld(uint32_t taddr, uint32_t (&r)[2 * E]);
+template <>
+__device__ __forceinline__ void tm_ld<4>(uint32_t taddr, uint32_t (&r)[8]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                  : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int k = 0; k < 4; k++) v[k] = __hiloint2double((int)r[2 * k + 1], (int)r[2 * k]);
 }
-// 16 columns (8 doubles) of this thread's row; tm_wait_ld() before using r
-__device__ __forceinline__ void tm_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+template <>
+__device__ __forceinline__ void tm_ld<8>(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
         "%15}, [%16];\n"
@@ -85,14 +87,44 @@ __device__ __forceinline__ void tm_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         : "r"(taddr));
 }
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ double tm_d(const uint32_t (&r)[16], int k) {
+template <int N2>
+__device__ __forceinline__ double tm_d(const uint32_t (&r)[N2], int k) {
     return __hiloint2double((int)r[2 * k + 1], (int)r[2 * k]);
 }
 __device__ __forceinline__ void tm_st1(uint32_t taddr, double v) {
     const uint32_t lo = (uint32_t)__double2loint(v), hi = (uint32_t)__double2hiint(v);
     asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(taddr), "r"(lo), "r"(hi) : "memory");
 }
+// 16 zero columns (8 entries) of this thread's row
+__device__ __forceinline__ void tm_zero16(uint32_t taddr) {
+    const uint32_t z = 0;
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+        "%1};\n" ::"r"(taddr),
+        "r"(z)
+        : "memory");
+}
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// ---- mbarrier (CTA scope): the winner warp's tensor-memory entries are published
+// after the step barrier by that warp alone; the other warps wait only when they
+// reach their tensor-memory dot
+__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(b)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n}" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n @!p bra "
+        "WAIT_%=;\n}" ::"r"((uint32_t)__cvta_generic_to_shared(b)),
+        "r"(parity)
+        : "memory");
+}
 
 __device__ __forceinline__ double fast_div_pos(double a, double b) {
     // a / b for finite b > 0 (not tiny): reciprocal seed, one Newton step, then
@@ -105,8 +137,6 @@ __device__ __forceinline__ double fast_div_pos(double a, double b) {
     const double res = fma(-b, q, a);
     return fma(res, r, q);
 }
-
-
 
 #ifdef LAGP_V2_PROF
 // clock probes of thread 0 on its first location (profiling builds only)
@@ -139,38 +169,42 @@ __device__ volatile double g_v2_sink;
     } while (0)
 #endif
 
+// mode bits: 1 = shared memory before tensor memory (A/B), 2 = no phase stagger (A/B)
 template <int P, int CPT, int TH>
 __global__ void __launch_bounds__(TH, 1)
-alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
+alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
     constexpr int R = V2R<P, CPT, TH>::value;
-    constexpr int V2_THREADS = TH;
-    constexpr int V2_NW = TH / 32;
-    constexpr int NPC = V2_THREADS * CPT;  // columns (candidates) per pair row
-    constexpr int T = V2T<CPT, TH>::value;  // entries [R+S, R+S+T) in tensor memory
-    constexpr int REC = v2_rec(R, T);
-    constexpr int RT = RW + R;              // record offset of the TMEM entries
+    constexpr int NW = TH / 32;
+    constexpr int NPC = TH * CPT;           // columns (candidates) per pair row
+    constexpr int T = V2T<CPT, TH>::value;  // entries per candidate in tensor memory (multiple of 8)
+    constexpr int REC = v2_rec(R);
+    constexpr int TMC = CPT >= 2 ? 4 : 8;  // tensor-memory entries per load in the dot
+    static_assert(T % 8 == 0 && REC % 2 == 0, "tier sizes");
     extern __shared__ __align__(16) double sm[];
-    double2 *wsm2 = reinterpret_cast<double2 *>(sm);          // [S/2][NPC] pairs of entries [R, R+S)
-    double *post = sm + (size_t)S * NPC;                      // [2][NW][REC]
+    double2 *wsm2 = reinterpret_cast<double2 *>(sm);  // [S/2][NPC] pairs of shared-memory entries
+    double *post = sm + (size_t)S * NPC;              // [2][NW][REC]
+    double *wtm = post + 2 * NW * REC;                // [T] the winner's tensor-memory entries (this step)
     const int n = A.n, Np = A.Nprime, n0 = A.n0;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     // entry tiers of w_c: registers [0, R), tensor memory [T0, T1), shared memory
-    // [S0, S1), L2 slab [G0, n); tfirst puts tensor memory before shared memory
-    const int T0 = (tfirst & 1) ? R : R + S, T1 = T0 + T;
-    const int S0 = (tfirst & 1) ? R + T : R, S1 = S0 + S;
+    // [S0, S1), L2 slab [G0, n); mode bit 1 puts shared memory first
+    const int T0 = (mode & 1) ? R + S : R, T1 = T0 + T;
+    const int S0 = (mode & 1) ? R : R + T, S1 = S0 + S;
     const int G0 = R + S + T;
     const int G = n - n0;
     const double eta = A.eta;
-    double2 *gw2 = reinterpret_cast<double2 *>(A.cache + (size_t)blockIdx.x * A.cache_stride);  // [(a-RST)/2][NPC]
+    double2 *gw2 = reinterpret_cast<double2 *>(A.cache + (size_t)blockIdx.x * A.cache_stride);  // [(a-G0)/2][NPC]
     __shared__ double xq[8];
     __shared__ uint32_t s_taddr;
+    __shared__ uint64_t s_mbar;
     // all 512 TMEM columns (one CTA per SM); warp w owns lanes 32(w%4).. and columns
-    // 128(w/4).. : candidate slot q's entry e at column 2(qT + e)
+    // (65536/TH)(w/4).. : candidate slot q's entry e at column 2(qT + e)
     if (wid == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
             (uint32_t)__cvta_generic_to_shared(&s_taddr)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
+    if (tid == 32) mbar_init(&s_mbar, 1);
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
@@ -178,13 +212,14 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
     __shared__ double zyv[2][LAGP_NMAX];  // z_j, y~_j of every append (a5)
     __shared__ double s_exptab[16];        // 2^(k/16) for exp_nonpos_tab
     if (threadIdx.x < 16) s_exptab[threadIdx.x] = c_exp2_16[threadIdx.x];
+    uint32_t mph = 0;  // parity of the next winner-TMEM publication
 
     for (int64_t xi = blockIdx.x; xi < A.M; xi += gridDim.x) {
         const double rth = A.theta_vec ? 1.0 / A.theta_vec[xi] : A.rtheta;  // per-location theta (Fig 1 step 4)
         const int32_t *pool = A.pool + xi * (int64_t)Np;
         int32_t *idx = A.idx_out + xi * (int64_t)n;
         if (tid < P) xq[tid] = A.XX[xi * P + tid];
-        for (int t = tid; t < n; t += V2_THREADS) idx[t] = (t < n0) ? pool[t] : -1;
+        for (int t = tid; t < n; t += TH) idx[t] = (t < n0) ? pool[t] : -1;
         __syncthreads();
 
         // ---- per-candidate state
@@ -194,9 +229,10 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
         bool chosen[CPT];
         int gidx[CPT];
         uint32_t fl = 0;
+        bool in_range = true;  // every pool d^2 to x finite and d^2/theta <= 175
 #pragma unroll
         for (int q = 0; q < CPT; q++) {
-            const int c = tid + q * V2_THREADS;
+            const int c = tid + q * TH;
             const bool valid = c < Np;
             chosen[q] = !valid;  // padding columns never compete
             gidx[q] = valid ? pool[c] : 0x7fffffff - c;  // unique keys for the warp argmax
@@ -207,33 +243,29 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
                 const double diff = __dsub_rn(xc[q][k], xq[k]);
                 d2 = __fma_rn(diff, diff, d2);
             }
+            if (valid && !(d2 * rth <= 175.0)) in_range = false;
             s[q] = 1.0 + eta;
             cov[q] = valid ? exp_nonpos_tab(-d2 * rth, s_exptab) : 0.0;  // kappa_c (z is empty at j = 0)
             tc[q] = valid ? A.Z[gidx[q]] : 0.0;             // y_c (y~ is empty at j = 0)
 #pragma unroll
             for (int a = 0; a < R; a++) wr[q][a] = 0.0;
+#pragma unroll
+            for (int e = 0; e < T; e += 8) tm_zero16(tbase + 2 * (q * T + e));  // unwritten entries read as 0
         }
+        tm_wait_st();
+        // pairwise: d^2(x_c, x*) <= 2 d^2(x_c, x) + 2 d^2(x*, x), so every K(x_c, x*) of
+        // this location has argument >= -700: the exp needs no range or NaN guard
+        const bool fast = __syncthreads_and(in_range);
         bool near_tie = false, exhausted = false;
 
         int j = 0;
         for (; j < n; j++) {
             V2_PROBE(0, (double)j);
             const int par = j & 1;
-            double *pst = post + par * (V2_NW * REC);
+            double *pst = post + par * (NW * REC);
             const double *rec;
             if (j < n0) {
                 // forced NN append (a2): pool position j (thread j, q = 0; j < n <= LAGP_NMAX <= TH)
-                // posts to slot 0; its TMEM entries through a load by its whole warp
-                if (j > T0 && wid == (j >> 5)) {
-                    const int mt = (j < T1 ? j : T1) - T0;
-                    for (int e = 0; e < mt; e += 4) {
-                        double v[4];
-                        tm_ld8(tbase + 2 * e, v);
-                        if (tid == j)
-#pragma unroll
-                            for (int k = 0; k < 4; k++) pst[RT + e + k] = e + k < mt ? v[k] : 0.0;
-                    }
-                }
                 if (tid == j) {
                     double *r = pst;
 #pragma unroll
@@ -291,33 +323,18 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
                 const unsigned long long sk = wl ? k2 : kb;
                 const unsigned sh = __reduce_max_sync(0xffffffffu, (unsigned)(sk >> 32));
                 const unsigned sl = __reduce_max_sync(0xffffffffu, (unsigned)(sk >> 32) == sh ? (unsigned)sk : 0u);
-                if (j > T0) {  // the warp winner's TMEM entries: a warp-collective load of its slot
-                    const int wlane = __ffs(__ballot_sync(0xffffffffu, wl)) - 1;
-                    const int qsel = __shfl_sync(0xffffffffu, qb, wlane);
-                    const int mt = (j < T1 ? j : T1) - T0;
-                    double *r = pst + wid * REC + RT;
-                    for (int e = 0; e < mt; e += 4) {
-                        double v[4];
-                        tm_ld8(tbase + 2 * (qsel * T + e), v);
-                        if (wl)
-#pragma unroll
-                            for (int k = 0; k < 4; k++) r[e + k] = e + k < mt ? v[k] : 0.0;
-                    }
-                }
                 if (wl) {
                     double *r = pst + wid * REC;
-                    reinterpret_cast<unsigned long long *>(r)[RK] = kb;
-                    reinterpret_cast<unsigned long long *>(r)[RI] =
-                        ((unsigned long long)(unsigned)(tid + qb * V2_THREADS) << 32) | (unsigned)gb;
+                    reinterpret_cast<ulonglong2 *>(r)[0] =
+                        make_ulonglong2(kb, ((unsigned long long)(unsigned)(tid + qb * TH) << 32) | (unsigned)gb);
                     reinterpret_cast<unsigned long long *>(r)[RK2] = ((unsigned long long)sh << 32) | sl;
 #pragma unroll
                     for (int q = 0; q < CPT; q++) {
                         if (q == qb) {
 #pragma unroll
                             for (int k = 0; k < P; k++) r[RX + k] = xc[q][k];
-                            r[RRHO] = s[q];  // raw s, cov, t: the readers scale by 1/sqrt(s)
-                            r[RZN] = cov[q];
-                            r[RYN] = tc[q];
+                            *reinterpret_cast<double2 *>(r + RRHO) = make_double2(s[q], cov[q]);
+                            r[RYN] = tc[q];  // raw s, cov, t: the readers scale by 1/sqrt(s)
 #pragma unroll
                             for (int a = 0; a < R; a += 2)
                                 *reinterpret_cast<double2 *>(r + RW + a) = make_double2(wr[q][a], wr[q][a + 1]);
@@ -329,9 +346,10 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
                 // every warp: argmax over the warp posts
                 unsigned long long pk = 0;
                 unsigned pg = 0xffffffffu;
-                if (lane < V2_NW) {
-                    pk = reinterpret_cast<const unsigned long long *>(pst + lane * REC)[RK];
-                    pg = (unsigned)reinterpret_cast<const unsigned long long *>(pst + lane * REC)[RI];
+                if (lane < NW) {
+                    const ulonglong2 kv = reinterpret_cast<const ulonglong2 *>(pst + lane * REC)[0];
+                    pk = kv.x;
+                    pg = (unsigned)kv.y;
                 }
                 const unsigned ph = (unsigned)(pk >> 32), pl = (unsigned)pk;
                 const unsigned qh = __reduce_max_sync(0xffffffffu, ph);
@@ -345,7 +363,7 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
                 const int W = __ffs(__ballot_sync(0xffffffffu, ptie && pg == qi)) - 1;
                 rec = pst + W * REC;
                 V2_PROBE(3, (double)W);
-                if (wid == V2_NW - 1) {  // top-2 gap: max(winner warp's second, other warps' best)
+                if (wid == NW - 1) {  // top-2 gap: max(winner warp's second, other warps' best)
                     const unsigned long long v =
                         lane == W ? reinterpret_cast<const unsigned long long *>(pst + lane * REC)[RK2] : pk;
                     const unsigned vh = __reduce_max_sync(0xffffffffu, (unsigned)(v >> 32));
@@ -367,25 +385,41 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
             const int cstar = (int)(ri >> 32);
 #pragma unroll
             for (int q = 0; q < CPT; q++)
-                if (cstar == tid + q * V2_THREADS) chosen[q] = true;
+                if (cstar == tid + q * TH) chosen[q] = true;
+            // the winner's tensor-memory entries [T0, j): its warp loads them (warp-collective)
+            // and publishes them in wtm; entries of a chunk beyond j are 0 on both sides
+            const int mt = j <= T0 ? 0 : (j < T1 ? j : T1) - T0;
+            if (mt > 0 && wid == ((cstar & (TH - 1)) >> 5)) {
+                const int qs = cstar / TH, wlane = cstar & 31;
+                for (int e = 0; e < mt; e += 8) {
+                    uint32_t r[16];
+                    tm_ld<8>(tbase + 2 * (qs * T + e), r);
+                    tm_wait_ld();
+                    if (lane == wlane) {
+#pragma unroll
+                        for (int k = 0; k < 8; k += 2)
+                            *reinterpret_cast<double2 *>(wtm + e + k) = make_double2(tm_d(r, k), tm_d(r, k + 1));
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_mbar);
+            }
             // 1/rho = s*^{-1/2} (off the posting lanes' path: every thread forms it)
             const double rrho = rsqrt_nr(rec[RRHO]), znew = rec[RZN] * rrho, ynew = rec[RYN] * rrho;
             V2_PROBE(4, rrho);
-            if (tid == V2_THREADS - 1) {  // a5 state (summed once at the end)
+            if (tid == TH - 1) {  // a5 state (summed once at the end)
                 zyv[0][j] = znew;
                 zyv[1][j] = ynew;
             }
 
             // Two phases per candidate: K(x_c, x*) (FP64 pipe) and the dot w_{c*}^T w_c
-            // (shared-memory / L2 bandwidth). Odd warps run them in the opposite order,
-            // so the two units are busy at the same time across the CTA.
+            // (shared / tensor memory). Warps w and w+4 (same SMSP) run them in opposite
+            // orders, so the two units are busy at the same time.
             double kx[CPT];
             double acc[CPT][2];
 #pragma unroll
             for (int q = 0; q < CPT; q++) acc[q][0] = acc[q][1] = 0.0;
-            // K(x_c, x*) first: branch-free, so the CPT chains interleave and overlap
-            // the slab loads below
-            auto kx_phase = [&]() {
+            auto kx_phase = [&](auto fastc) {
                 double d2[CPT][2];  // two partial sums: half the dependent-chain depth
 #pragma unroll
                 for (int q = 0; q < CPT; q++) d2[q][0] = d2[q][1] = 0.0;
@@ -399,124 +433,147 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
                     }
                 }
 #pragma unroll
-                for (int q = 0; q < CPT; q++) kx[q] = exp_nonpos_tab(-(d2[q][0] + d2[q][1]) * rth, s_exptab);
+                for (int q = 0; q < CPT; q++) {
+                    const double xa = -(d2[q][0] + d2[q][1]) * rth;
+                    if constexpr (decltype(fastc)::value)
+                        kx[q] = exp_nonpos_tab_inrange(xa, s_exptab);
+                    else
+                        kx[q] = exp_nonpos_tab(xa, s_exptab);
+                }
+            };
+            auto kx_any = [&]() {
+                if (fast)
+                    kx_phase(std::true_type{});
+                else
+                    kx_phase(std::false_type{});
             };
             auto dot_phase = [&]() {
-            // tensor-memory entries [T0, min(j, T1)): own rows by tcgen05.ld, the
-            // winner's from its record
-            if (j > T0) {
-                const int mt = (j < T1 ? j : T1) - T0;
-                for (int e = 0; e < mt; e += 4) {
-                    const double2 w01 = *reinterpret_cast<const double2 *>(rec + RT + e);
-                    const double2 w23 = *reinterpret_cast<const double2 *>(rec + RT + e + 2);
+                // register entries (entries >= j are 0 on both sides)
+#pragma unroll
+                for (int a = 0; a < R; a += 2) {
+                    const double2 wv = *reinterpret_cast<const double2 *>(rec + RW + a);
 #pragma unroll
                     for (int q = 0; q < CPT; q++) {
-                        double v[4];
-                        tm_ld8(tbase + 2 * (q * T + e), v);
-                        // entries >= mt of this chunk are stale on both sides: masked to 0
-                        acc[q][0] = fma(w01.x, v[0], acc[q][0]);
-                        acc[q][1] = fma(w01.y, e + 1 < mt ? v[1] : 0.0, acc[q][1]);
-                        acc[q][0] = fma(w23.x, e + 2 < mt ? v[2] : 0.0, acc[q][0]);
-                        acc[q][1] = fma(w23.y, e + 3 < mt ? v[3] : 0.0, acc[q][1]);
+                        acc[q][0] = fma(wv.x, wr[q][a], acc[q][0]);
+                        acc[q][1] = fma(wv.y, wr[q][a + 1], acc[q][1]);
                     }
                 }
-            }
-            // slab entries [G0, j) (L2-resident), two pairs per iteration
-            if (j > G0) {
-                const int m = j - G0;
-                const double2 *gwin = gw2 + cstar;
-                const double2 *gown = gw2 + tid;
-                const int np = m >> 1;
+                // shared entries [S0, min(j, S1)): one LDS.128 per two entries of a column
+                if (j > S0) {
+                    const int m = (j < S1 ? j : S1) - S0;
+                    const double2 *swin = wsm2 + cstar;
+                    const double2 *sown = wsm2 + tid;
+                    const int np = m >> 1;
 #pragma unroll 2
-                for (int pr = 0; pr < np; pr++) {
-                    const double2 wv = *gwin;
+                    for (int pr = 0; pr < np; pr++) {
+                        const double2 wv = *swin;
 #pragma unroll
-                    for (int q = 0; q < CPT; q++) {
-                        const double2 o = gown[q * V2_THREADS];
-                        acc[q][0] = fma(wv.x, o.x, acc[q][0]);
-                        acc[q][1] = fma(wv.y, o.y, acc[q][1]);
+                        for (int q = 0; q < CPT; q++) {
+                            const double2 o = sown[q * TH];
+                            acc[q][0] = fma(wv.x, o.x, acc[q][0]);
+                            acc[q][1] = fma(wv.y, o.y, acc[q][1]);
+                        }
+                        swin += NPC;
+                        sown += NPC;
                     }
-                    gwin += NPC;
-                    gown += NPC;
-                }
-                if (m & 1) {
-                    const double wv = reinterpret_cast<const double *>(gwin)[0];
+                    if (m & 1) {
+                        const double wv = reinterpret_cast<const double *>(swin)[0];
 #pragma unroll
-                    for (int q = 0; q < CPT; q++)
-                        acc[q][0] = fma(wv, reinterpret_cast<const double *>(gown + q * V2_THREADS)[0], acc[q][0]);
+                        for (int q = 0; q < CPT; q++)
+                            acc[q][0] = fma(wv, reinterpret_cast<const double *>(sown + q * TH)[0], acc[q][0]);
+                    }
                 }
-            }
-            // register entries (entries >= j are 0 on both sides)
-#pragma unroll
-            for (int a = 0; a < R; a += 2) {
-                const double2 wv = *reinterpret_cast<const double2 *>(rec + RW + a);
-#pragma unroll
-                for (int q = 0; q < CPT; q++) {
-                    acc[q][0] = fma(wv.x, wr[q][a], acc[q][0]);
-                    acc[q][1] = fma(wv.y, wr[q][a + 1], acc[q][1]);
-                }
-            }
-            // shared entries [S0, min(j, S1)): one LDS.128 per two entries of a column
-            if (j > S0) {
-                const int m = (j < S1 ? j : S1) - S0;
-                const double2 *swin = wsm2 + cstar;
-                const double2 *sown = wsm2 + tid;
-                const int np = m >> 1;
+                // slab entries [G0, j) (L2-resident), two pairs per iteration
+                if (j > G0) {
+                    const int m = j - G0;
+                    const double2 *gwin = gw2 + cstar;
+                    const double2 *gown = gw2 + tid;
+                    const int np = m >> 1;
 #pragma unroll 2
-                for (int pr = 0; pr < np; pr++) {
-                    const double2 wv = *swin;
+                    for (int pr = 0; pr < np; pr++) {
+                        const double2 wv = *gwin;
 #pragma unroll
-                    for (int q = 0; q < CPT; q++) {
-                        const double2 o = sown[q * V2_THREADS];
-                        acc[q][0] = fma(wv.x, o.x, acc[q][0]);
-                        acc[q][1] = fma(wv.y, o.y, acc[q][1]);
+                        for (int q = 0; q < CPT; q++) {
+                            const double2 o = gown[q * TH];
+                            acc[q][0] = fma(wv.x, o.x, acc[q][0]);
+                            acc[q][1] = fma(wv.y, o.y, acc[q][1]);
+                        }
+                        gwin += NPC;
+                        gown += NPC;
                     }
-                    swin += NPC;
-                    sown += NPC;
-                }
-                if (m & 1) {
-                    const double wv = reinterpret_cast<const double *>(swin)[0];
+                    if (m & 1) {
+                        const double wv = reinterpret_cast<const double *>(gwin)[0];
 #pragma unroll
-                    for (int q = 0; q < CPT; q++)
-                        acc[q][0] = fma(wv, reinterpret_cast<const double *>(sown + q * V2_THREADS)[0], acc[q][0]);
+                        for (int q = 0; q < CPT; q++)
+                            acc[q][0] = fma(wv, reinterpret_cast<const double *>(gown + q * TH)[0], acc[q][0]);
+                    }
                 }
-            }
+                // tensor-memory entries [T0, T0 + mt): own rows by tcgen05.ld (8 entries per
+                // load), the winner's from wtm once its warp has published them
+                if (mt > 0) {
+                    mbar_wait(&s_mbar, mph);
+                    for (int e = 0; e < mt; e += TMC) {
+                        uint32_t r[CPT][2 * TMC];
+#pragma unroll
+                        for (int q = 0; q < CPT; q++) tm_ld<TMC>(tbase + 2 * (q * T + e), r[q]);
+                        tm_wait_ld();
+#pragma unroll
+                        for (int k = 0; k < TMC; k += 2) {
+                            const double2 wv = *reinterpret_cast<const double2 *>(wtm + e + k);
+#pragma unroll
+                            for (int q = 0; q < CPT; q++) {
+                                acc[q][0] = fma(wv.x, tm_d(r[q], k), acc[q][0]);
+                                acc[q][1] = fma(wv.y, tm_d(r[q], k + 1), acc[q][1]);
+                            }
+                        }
+                    }
+                }
             };
-            if ((tfirst & 2) ? false : ((wid >> 2) & 1)) {  // warps w and w+4 share an SMSP: opposite orders
+            if ((mode & 2) ? false : ((wid >> 2) & 1)) {  // warps w and w+4 share an SMSP: opposite orders
                 dot_phase();
-                kx_phase();
+                kx_any();
             } else {
-                kx_phase();
+                kx_any();
                 V2_PROBE(5, kx[0]);
                 dot_phase();
                 V2_PROBE(6, acc[0][0] + acc[0][1]);
             }
+            if (mt > 0) mph ^= 1u;
+            double wn[CPT];
 #pragma unroll
-            for (int q = 0; q < CPT; q++) {
-                const int c = tid + q * V2_THREADS;
-                const double wn = (kx[q] - (acc[q][0] + acc[q][1])) * rrho;
-                if (j < R) {
+            for (int q = 0; q < CPT; q++) wn[q] = (kx[q] - (acc[q][0] + acc[q][1])) * rrho;
+            // store entry j of every column in its tier (the tier is uniform per step)
+            if (j < R) {
+#pragma unroll
+                for (int q = 0; q < CPT; q++)
 #pragma unroll
                     for (int b = 0; b < R; b++)
-                        if (b == j) wr[q][b] = wn;
-                } else if (j >= S0 && j < S1) {
-                    reinterpret_cast<double *>(wsm2 + ((j - S0) >> 1) * NPC + c)[(j - S0) & 1] = wn;
-                } else if (j >= T0 && j < T1) {
-                    tm_st1(tbase + 2 * (q * T + (j - T0)), wn);
-                } else {
-                    reinterpret_cast<double *>(gw2 + ((j - G0) >> 1) * NPC + c)[(j - G0) & 1] = wn;
-                }
-                s[q] = fma(-wn, wn, s[q]);
-                cov[q] = fma(-znew, wn, cov[q]);
-                tc[q] = fma(-ynew, wn, tc[q]);
+                        if (b == j) wr[q][b] = wn[q];
+            } else if (j >= T0 && j < T1) {
+#pragma unroll
+                for (int q = 0; q < CPT; q++) tm_st1(tbase + 2 * (q * T + (j - T0)), wn[q]);
+                tm_wait_st();  // this step's stores land before the next reads
+            } else if (j >= S0 && j < S1) {
+                double *dst = reinterpret_cast<double *>(wsm2 + ((j - S0) >> 1) * NPC + tid) + ((j - S0) & 1);
+#pragma unroll
+                for (int q = 0; q < CPT; q++) dst[2 * q * TH] = wn[q];
+            } else {
+                double *dst = reinterpret_cast<double *>(gw2 + ((j - G0) >> 1) * NPC + tid) + ((j - G0) & 1);
+#pragma unroll
+                for (int q = 0; q < CPT; q++) dst[2 * q * TH] = wn[q];
             }
-            if (j >= T0 && j < T1) tm_wait_st();  // this step's TMEM stores land before the next reads
+#pragma unroll
+            for (int q = 0; q < CPT; q++) {
+                s[q] = fma(-wn[q], wn[q], s[q]);
+                cov[q] = fma(-znew, wn[q], cov[q]);
+                tc[q] = fma(-ynew, wn[q], tc[q]);
+            }
         }
 
         // ---- flags and a5: mean = z^T y~, psi = ||y~||^2, s2 = psi (1 + eta - ||z||^2) / j
         const bool any_sent = __syncthreads_or((fl & LAGP_FLAG_SENTINEL) != 0);
         const bool any_nonf = __syncthreads_or((fl & LAGP_FLAG_NONFINITE) != 0);
-        if (wid == V2_NW - 1) {  // the warp holding near_tie (its lane 0)
+        if (wid == NW - 1) {  // the warp holding near_tie (its lane 0)
             double mu = 0.0, psi = 0.0, zz = 0.0;
             for (int a = lane; a < j; a += 32) {
                 mu = fma(zyv[0][a], zyv[1][a], mu);
@@ -554,11 +611,11 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int tfirst) {
 
 // ---------------------------------------------------------------- host side
 template <int P, int CPT, int TH>
-static cudaError_t v2_launch_t(const AlcArgs &a, int S, int tfirst, int grid, size_t smem, cudaStream_t st) {
+static cudaError_t v2_launch_t(const AlcArgs &a, int S, int mode, int grid, size_t smem, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(alc_incremental_v2_kernel<P, CPT, TH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    alc_incremental_v2_kernel<P, CPT, TH><<<grid, TH, smem, st>>>(a, S, tfirst);
+    alc_incremental_v2_kernel<P, CPT, TH><<<grid, TH, smem, st>>>(a, S, mode);
     return cudaGetLastError();
 }
 
@@ -589,20 +646,22 @@ bool inc_v2_plan(int n, int p, int Nprime, size_t smem_optin, IncPlan &pl) {
     if (R < 0) return false;
     const int npc = th * cpt;
     const int T = (65536 / th) / 2 / cpt;
-    const size_t fixed = (size_t)2 * (th / 32) * v2_rec(R, T) * sizeof(double);
+    int mode = 0;
+    const char *sf = getenv("LAGP_V2_SFIRST");  // A/B: 1 = shared memory before tensor memory
+    if (sf && sf[0] == '1') mode |= 1;
+    const char *ns = getenv("LAGP_V2_NOSTAGGER");  // A/B: every warp runs K(x_c,x*) before the dot
+    if (ns && ns[0] == '1') mode |= 2;
+    const size_t fixed = ((size_t)2 * (th / 32) * v2_rec(R) + T) * sizeof(double);
     if (smem_optin < fixed + 2048) return false;
     const size_t pair_bytes = (size_t)npc * 2 * sizeof(double);
     int S = 2 * (int)((smem_optin - fixed - 2048) / pair_bytes);
-    const int need = n - R > 0 ? n - R : 0;
+    const int need = n - R - ((mode & 1) ? 0 : T) > 0 ? n - R - ((mode & 1) ? 0 : T) : 0;
     const int need2 = (need + 1) & ~1;
     if (S > need2) S = need2;
     pl = IncPlan{};
     pl.ok = true;
     pl.v2 = true;
-    const char *tf = getenv("LAGP_V2_TFIRST");  // A/B: 1 = tensor memory before shared memory
-    pl.tfirst = (tf && tf[0] == '1') ? 1 : 0;  // measured: TMEM after shared memory is faster
-    const char *ns = getenv("LAGP_V2_NOSTAGGER");  // A/B: every warp runs K(x_c,x*) before the dot
-    if (ns && ns[0] == '1') pl.tfirst |= 2;
+    pl.tfirst = mode;
     pl.cpt = cpt;
     pl.threads = th;
     pl.R = R;

@@ -95,6 +95,27 @@ __device__ __forceinline__ double exp_nonpos_tab(double x, const double *tab) {
     const double v = __longlong_as_double(__double_as_longlong(v0) + ((long long)(N >> 4) << 52));
     return x < -708.0 ? 0.0 : (x == x ? v : x);
 }
+// The same for a finite x in [-708, 0] (the caller proves the range): no clamp, no
+// NaN or underflow select, the 2^m scaling added to the high word only. Bitwise
+// equal to exp_nonpos_tab on that domain.
+__device__ __forceinline__ double exp_nonpos_tab_inrange(double x, const double *tab) {
+    const double shifter = 6755399441055744.0;  // 1.5 * 2^52
+    const double t = fma(x, 23.083120654223414, shifter);  // 16 / ln2
+    const double nd = t - shifter;
+    const int N = (int)(unsigned)__double2loint(t);
+    double r = fma(nd, -0.04332169877307024, x);  // ln2_hi / 16
+    r = fma(nd, -1.1926343307941173e-11, r);      // ln2_lo / 16
+    double p = fma(r, 1.0 / 5040.0, 1.0 / 720.0);
+    p = fma(p, r, 1.0 / 120.0);
+    p = fma(p, r, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    const double pm1 = p * r;  // e^r - 1
+    const double T = tab[N & 15];
+    const double v0 = fma(T, pm1, T);
+    return __hiloint2double(__double2hiint(v0) + ((N >> 4) << 20), __double2loint(v0));
+}
 
 // s^{-1/2} for s > 0: reciprocal-square-root seed and two Newton steps
 // (r <- r + r(1 - s r^2)/2); s <= 0 gives NaN (a non-PD append, flagged NONFINITE)

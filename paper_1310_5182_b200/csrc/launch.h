@@ -54,7 +54,7 @@ struct IncPlan {
     size_t smem;         // dynamic shared memory bytes
     bool v2;             // alc_incremental_v2.cu (N' <= 1024, p in {1,2,3,4,8})
     int64_t cache_doubles;  // per-CTA slab doubles (v2)
-    int tfirst;             // v2: bit 0 tensor-memory entries before the shared-memory ones, bit 1 no stagger
+    int tfirst;             // v2 mode: bit 0 shared-memory entries before the tensor-memory ones, bit 1 no stagger
     int threads;            // v2: threads per CTA
 };
 IncPlan inc_plan(int n, int p, int Nprime, int Npad, size_t smem_optin);
