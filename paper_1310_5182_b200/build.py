@@ -50,22 +50,23 @@ def _nvcc() -> str:
     return nvcc
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB, obj_dir: str = OBJ) -> str:
     """One object per .cu (compiled in parallel, reused while it is newer than its
-    source and every header), then one shared-library link."""
-    if not (force or _stale()):
+    source and every header), then one shared-library link. `defines` / `lib` /
+    `obj_dir`: experiment builds (e.g. -DLAGP_V2_PROF into liblagp_b200_prof.so)."""
+    if lib == LIB and not (force or _stale()):
         return LIB
     from concurrent.futures import ThreadPoolExecutor
 
     nvcc = _nvcc()
-    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(obj_dir, exist_ok=True)
     th = max([os.path.getmtime(f) for f in _headers()] + [0.0])
 
     def compile_one(src):
-        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
         if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(th, os.path.getmtime(src)):
             return obj, "", 0
-        r = subprocess.run([nvcc, *NVCC_FLAGS, "-c", "-o", obj + ".tmp", src], capture_output=True, text=True)
+        r = subprocess.run([nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", "-o", obj + ".tmp", src], capture_output=True, text=True)
         if r.returncode == 0:
             with open(obj + ".ptxas", "w") as f:
                 f.write(r.stderr)
@@ -80,11 +81,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building liblagp_b200.so")
     objs = [o for o, _, _ in res]
     r = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
-                        "-o", LIB + ".tmp", *objs], capture_output=True, text=True)
+                        "-o", lib + ".tmp", *objs], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed linking liblagp_b200.so")
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(lib + ".tmp", lib)
+    if lib != LIB:
+        return lib
     report = "".join(out for _, out, _ in res)
     if verbose:
         sys.stderr.write(report)
@@ -96,5 +99,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    if "--prof" in sys.argv:  # clock-probe build of the incremental kernel (scripts/v2_probe.py)
+        print(build(force=True, defines=["LAGP_V2_PROF"], lib=os.path.join(PKG, "liblagp_b200_prof.so"),
+                    obj_dir=os.path.join(ROOT, "build", "obj_prof")))
+    else:
+        build(force="--force" in sys.argv, verbose=True)
+        print(LIB)

@@ -50,10 +50,16 @@ namespace lagp {
 // 512 x 2 (default), 256 x 4 or 1024 x 1 (A/B, LAGP_V2_CPT=4|1)
 
 // register entries per candidate for (P, CPT, TH)
+#ifndef LAGP_V2_STAG_EXPR
+#define LAGP_V2_STAG_EXPR ((mode & 2) ? false : ((wid >> 2) & 1))
+#endif
+#ifndef LAGP_V2R_C4
+#define LAGP_V2R_C4 6
+#endif
 template <int P, int CPT, int TH>
 struct V2R {
     static constexpr int value =
-        (TH == 1024) ? 2 : (CPT == 1) ? 16 : (CPT == 2 ? (P <= 4 ? 8 : 4) : (P <= 4 ? 8 : 6));
+        (TH == 1024) ? 2 : (CPT == 1) ? 16 : (CPT == 2 ? (P <= 4 ? 8 : 4) : (P <= 4 ? 8 : LAGP_V2R_C4));
 };
 
 // TMEM entries per candidate: each thread owns 256 KB / TH of tensor memory (its warp's
@@ -63,8 +69,8 @@ struct V2T {
     static constexpr int value = (65536 / TH) / 2 / CPT;
 };
 
-// warp post record (doubles): key | gidx,pos | key2 | - | x[8] | s cov t - | w[R]
-enum { RK = 0, RI = 1, RK2 = 2, RX = 4, RRHO = 12, RZN = 13, RYN = 14, RW = 16 };
+// warp post record (doubles): key | gidx,pos | key2 | - | x-x_ref[8] | s cov t |x-x_ref|^2/theta | w[R]
+enum { RK = 0, RI = 1, RK2 = 2, RX = 4, RRHO = 12, RZN = 13, RYN = 14, RAC = 15, RW = 16 };
 __host__ __device__ constexpr int v2_rec(int R) { return RW + R; }
 
 // ---- tensor memory as per-thread storage (tcgen05; thread-private lane rows)
@@ -106,26 +112,6 @@ __device__ __forceinline__ void tm_zero16(uint32_t taddr) {
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// ---- mbarrier (CTA scope): the winner warp's tensor-memory entries are published
-// after the step barrier by that warp alone; the other warps wait only when they
-// reach their tensor-memory dot
-__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(b)), "r"(count)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
-    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n}" ::"r"(
-                     (uint32_t)__cvta_generic_to_shared(b))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n @!p bra "
-        "WAIT_%=;\n}" ::"r"((uint32_t)__cvta_generic_to_shared(b)),
-        "r"(parity)
-        : "memory");
-}
-
 __device__ __forceinline__ double fast_div_pos(double a, double b) {
     // a / b for finite b > 0 (not tiny): reciprocal seed, one Newton step, then
     // one residual correction of the quotient (no special-case path)
@@ -139,33 +125,21 @@ __device__ __forceinline__ double fast_div_pos(double a, double b) {
 }
 
 #ifdef LAGP_V2_PROF
-// clock probes of thread 0 on its first location (profiling builds only)
-__device__ long long g_v2_prof[160][8];
-__device__ long long g_v2_arrive[160][32];  // per warp: clock when its lane 0 reaches the step barrier
-#define V2_ARRIVE()                                                                             \
-    do {                                                                                        \
-        if (lane == 0 && xi == blockIdx.x && blockIdx.x == 0 && j < 160) {                      \
-            long long t_;                                                                       \
-            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_)::"memory");                        \
-            g_v2_arrive[j][wid] = t_;                                                           \
-        }                                                                                       \
-    } while (0)
-__device__ volatile double g_v2_sink;
-#define V2_PROBE(k, v)                                                              \
+// clock probes (profiling builds only): lane 0 of every warp of CTA 0 on its first
+// location, event k of step j: g_v2_ev[j][warp][k]
+#define V2_NEV 12
+__device__ long long g_v2_ev[128][32][V2_NEV];
+#define V2_EV(k)                                                                    \
     do {                                                                            \
-        if (tid == 0 && xi == blockIdx.x && blockIdx.x == 0 && j < 160) {           \
-            g_v2_sink = (v);                                                        \
+        if (lane == 0 && xi == blockIdx.x && blockIdx.x == 0 && j < 128) {          \
             long long t_;                                                           \
             asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_)::"memory");            \
-            g_v2_prof[j][k] = t_;                                                   \
+            g_v2_ev[j][wid][k] = t_;                                                \
         }                                                                           \
     } while (0)
 #else
-#define V2_PROBE(k, v) \
-    do {               \
-    } while (0)
-#define V2_ARRIVE() \
-    do {            \
+#define V2_EV(k) \
+    do {         \
     } while (0)
 #endif
 
@@ -184,6 +158,9 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
     double2 *wsm2 = reinterpret_cast<double2 *>(sm);  // [S/2][NPC] pairs of shared-memory entries
     double *post = sm + (size_t)S * NPC;              // [2][NW][REC]
     double *wtm = post + 2 * NW * REC;                // [T] the winner's tensor-memory entries (this step)
+    // [n][NW + 1] per greedy step: every warp's best key and the winner warp's second
+    // best (top-2 gaps and the near-tie flag, formed once per location)
+    unsigned long long *glog = reinterpret_cast<unsigned long long *>(wtm + T);
     const int n = A.n, Np = A.Nprime, n0 = A.n0;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     // entry tiers of w_c: registers [0, R), tensor memory [T0, T1), shared memory
@@ -196,7 +173,7 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
     double2 *gw2 = reinterpret_cast<double2 *>(A.cache + (size_t)blockIdx.x * A.cache_stride);  // [(a-G0)/2][NPC]
     __shared__ double xq[8];
     __shared__ uint32_t s_taddr;
-    __shared__ uint64_t s_mbar;
+    __shared__ volatile int s_pub;  // sequence number of the last winner-TMEM publication
     // all 512 TMEM columns (one CTA per SM); warp w owns lanes 32(w%4).. and columns
     // (65536/TH)(w/4).. : candidate slot q's entry e at column 2(qT + e)
     if (wid == 0) {
@@ -204,7 +181,7 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
             (uint32_t)__cvta_generic_to_shared(&s_taddr)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
-    if (tid == 32) mbar_init(&s_mbar, 1);
+    if (tid == 32) s_pub = -1;
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
@@ -212,7 +189,7 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
     __shared__ double zyv[2][LAGP_NMAX];  // z_j, y~_j of every append (a5)
     __shared__ double s_exptab[16];        // 2^(k/16) for exp_nonpos_tab
     if (threadIdx.x < 16) s_exptab[threadIdx.x] = c_exp2_16[threadIdx.x];
-    uint32_t mph = 0;  // parity of the next winner-TMEM publication
+    int pubseq = 0;  // sequence number of the next winner-TMEM publication (uniform)
 
     for (int64_t xi = blockIdx.x; xi < A.M; xi += gridDim.x) {
         const double rth = A.theta_vec ? 1.0 / A.theta_vec[xi] : A.rtheta;  // per-location theta (Fig 1 step 4)
@@ -223,7 +200,8 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
         __syncthreads();
 
         // ---- per-candidate state
-        double xc[CPT][P];
+        double xc[CPT][P];  // x_c - x (offsets from the reference location)
+        double ac[CPT];     // |x_c - x|^2 / theta
         double s[CPT], cov[CPT], tc[CPT];
         double wr[CPT][R];
         bool chosen[CPT];
@@ -239,13 +217,14 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
             double d2 = 0.0;
 #pragma unroll
             for (int k = 0; k < P; k++) {
-                xc[q][k] = valid ? A.X[(int64_t)gidx[q] * P + k] : 0.0;
-                const double diff = __dsub_rn(xc[q][k], xq[k]);
+                const double diff = __dsub_rn(valid ? A.X[(int64_t)gidx[q] * P + k] : xq[k], xq[k]);
+                xc[q][k] = diff;
                 d2 = __fma_rn(diff, diff, d2);
             }
-            if (valid && !(d2 * rth <= 175.0)) in_range = false;
+            ac[q] = d2 * rth;
+            if (valid && !(ac[q] <= 175.0)) in_range = false;
             s[q] = 1.0 + eta;
-            cov[q] = valid ? exp_nonpos_tab(-d2 * rth, s_exptab) : 0.0;  // kappa_c (z is empty at j = 0)
+            cov[q] = valid ? exp_nonpos_tab(-ac[q], s_exptab) : 0.0;  // kappa_c (z is empty at j = 0)
             tc[q] = valid ? A.Z[gidx[q]] : 0.0;             // y_c (y~ is empty at j = 0)
 #pragma unroll
             for (int a = 0; a < R; a++) wr[q][a] = 0.0;
@@ -256,14 +235,15 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
         // pairwise: d^2(x_c, x*) <= 2 d^2(x_c, x) + 2 d^2(x*, x), so every K(x_c, x*) of
         // this location has argument >= -700: the exp needs no range or NaN guard
         const bool fast = __syncthreads_and(in_range);
-        bool near_tie = false, exhausted = false;
+        bool exhausted = false;
 
         int j = 0;
         for (; j < n; j++) {
-            V2_PROBE(0, (double)j);
+            V2_EV(0);
             const int par = j & 1;
             double *pst = post + par * (NW * REC);
             const double *rec;
+            unsigned long long sk2 = ~0ull;  // the winner warp's per-lane second-best candidates
             if (j < n0) {
                 // forced NN append (a2): pool position j (thread j, q = 0; j < n <= LAGP_NMAX <= TH)
                 if (tid == j) {
@@ -273,6 +253,7 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
                     r[RRHO] = s[0];  // raw s, cov, t: the readers scale by 1/sqrt(s)
                     r[RZN] = cov[0];
                     r[RYN] = tc[0];
+                    r[RAC] = ac[0];
 #pragma unroll
                     for (int a = 0; a < R; a += 2)
                         *reinterpret_cast<double2 *>(r + RW + a) = make_double2(wr[0][a], wr[0][a + 1]);
@@ -310,7 +291,7 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
                     gb = b ? gidx[q] : gb;
                     qb = b ? q : qb;
                 }
-                V2_PROBE(1, (double)kb);
+                V2_EV(1);
                 // warp argmax on (key desc, gidx asc) with 32-bit redux
                 const unsigned hi = (unsigned)(kb >> 32), lo = (unsigned)kb;
                 const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
@@ -318,30 +299,25 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
                 const bool tie = hi == mh && lo == ml;
                 const unsigned mi = __reduce_min_sync(0xffffffffu, tie ? (unsigned)gb : 0xffffffffu);
                 const bool wl = tie && (unsigned)gb == mi;  // unique: gidx are distinct
-                V2_PROBE(2, (double)mi);
-                // the warp's second-best key (top-2 gap diagnostic)
-                const unsigned long long sk = wl ? k2 : kb;
-                const unsigned sh = __reduce_max_sync(0xffffffffu, (unsigned)(sk >> 32));
-                const unsigned sl = __reduce_max_sync(0xffffffffu, (unsigned)(sk >> 32) == sh ? (unsigned)sk : 0u);
+                V2_EV(2);
                 if (wl) {
                     double *r = pst + wid * REC;
                     reinterpret_cast<ulonglong2 *>(r)[0] =
                         make_ulonglong2(kb, ((unsigned long long)(unsigned)(tid + qb * TH) << 32) | (unsigned)gb);
-                    reinterpret_cast<unsigned long long *>(r)[RK2] = ((unsigned long long)sh << 32) | sl;
 #pragma unroll
                     for (int q = 0; q < CPT; q++) {
                         if (q == qb) {
 #pragma unroll
                             for (int k = 0; k < P; k++) r[RX + k] = xc[q][k];
                             *reinterpret_cast<double2 *>(r + RRHO) = make_double2(s[q], cov[q]);
-                            r[RYN] = tc[q];  // raw s, cov, t: the readers scale by 1/sqrt(s)
+                            *reinterpret_cast<double2 *>(r + RYN) = make_double2(tc[q], ac[q]);  // raw s, cov, t
 #pragma unroll
                             for (int a = 0; a < R; a += 2)
                                 *reinterpret_cast<double2 *>(r + RW + a) = make_double2(wr[q][a], wr[q][a + 1]);
                         }
                     }
                 }
-                V2_ARRIVE();
+                V2_EV(3);
                 __syncthreads();
                 // every warp: argmax over the warp posts
                 unsigned long long pk = 0;
@@ -362,23 +338,12 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
                 const unsigned qi = __reduce_min_sync(0xffffffffu, ptie ? pg : 0xffffffffu);
                 const int W = __ffs(__ballot_sync(0xffffffffu, ptie && pg == qi)) - 1;
                 rec = pst + W * REC;
-                V2_PROBE(3, (double)W);
-                if (wid == NW - 1) {  // top-2 gap: max(winner warp's second, other warps' best)
-                    const unsigned long long v =
-                        lane == W ? reinterpret_cast<const unsigned long long *>(pst + lane * REC)[RK2] : pk;
-                    const unsigned vh = __reduce_max_sync(0xffffffffu, (unsigned)(v >> 32));
-                    const unsigned vl = __reduce_max_sync(0xffffffffu, (unsigned)(v >> 32) == vh ? (unsigned)v : 0u);
-                    if (lane == 0) {
-                        const unsigned long long k1 = ((unsigned long long)qh << 32) | ql;
-                        const unsigned long long k2b = ((unsigned long long)vh << 32) | vl;
-                        const double d1 = __longlong_as_double((long long)(k1 - 1ull));
-                        const double d2 = k2b ? __longlong_as_double((long long)(k2b - 1ull)) : 0.0;
-                        const double gap = top2_gap(d1, d2);
-                        if (!(d1 > 0.0) || gap < kTieGap) near_tie = true;
-                        if (A.gap_out) A.gap_out[xi * G + (j - n0)] = gap;
-                        idx[j] = (int)qi;
-                    }
+                V2_EV(4);
+                if (wid == NW - 1) {  // log every warp's best key (the gaps are formed at the end)
+                    if (lane < NW) glog[(j - n0) * (NW + 1) + lane] = pk;
+                    if (lane == 0) idx[j] = (int)qi;
                 }
+                if (wid == W) sk2 = wl ? k2 : kb;  // reduced at the end of the step (off the path)
             }
             // ---- a4 on the factor: every candidate takes its new entry and downdates
             const unsigned long long ri = reinterpret_cast<const unsigned long long *>(rec)[RI];
@@ -386,8 +351,9 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
 #pragma unroll
             for (int q = 0; q < CPT; q++)
                 if (cstar == tid + q * TH) chosen[q] = true;
-            // the winner's tensor-memory entries [T0, j): its warp loads them (warp-collective)
-            // and publishes them in wtm; entries of a chunk beyond j are 0 on both sides
+            // the winner's tensor-memory entries [T0, j), published in wtm by its warp (a
+            // warp-collective load of its lane row; entries of a chunk beyond j are 0 on both
+            // sides); the other warps wait on s_pub only when they reach their TMEM dot
             const int mt = j <= T0 ? 0 : (j < T1 ? j : T1) - T0;
             if (mt > 0 && wid == ((cstar & (TH - 1)) >> 5)) {
                 const int qs = cstar / TH, wlane = cstar & 31;
@@ -401,12 +367,15 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
                             *reinterpret_cast<double2 *>(wtm + e + k) = make_double2(tm_d(r, k), tm_d(r, k + 1));
                     }
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&s_mbar);
+                if (lane == wlane) {
+                    __threadfence_block();
+                    s_pub = pubseq;
+                }
+                V2_EV(5);
             }
             // 1/rho = s*^{-1/2} (off the posting lanes' path: every thread forms it)
             const double rrho = rsqrt_nr(rec[RRHO]), znew = rec[RZN] * rrho, ynew = rec[RYN] * rrho;
-            V2_PROBE(4, rrho);
+            V2_EV(6);
             if (tid == TH - 1) {  // a5 state (summed once at the end)
                 zyv[0][j] = znew;
                 zyv[1][j] = ynew;
@@ -420,25 +389,25 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
 #pragma unroll
             for (int q = 0; q < CPT; q++) acc[q][0] = acc[q][1] = 0.0;
             auto kx_phase = [&](auto fastc) {
-                double d2[CPT][2];  // two partial sums: half the dependent-chain depth
+                // -|x_c - x*|^2 / theta = 2 (x_c - x).(x* - x) / theta - (a_c + a*), offsets from
+                // the reference location x (the pool lies in a ball around it)
+                double dt[CPT][2];  // two partial sums: half the dependent-chain depth
 #pragma unroll
-                for (int q = 0; q < CPT; q++) d2[q][0] = d2[q][1] = 0.0;
+                for (int q = 0; q < CPT; q++) dt[q][0] = dt[q][1] = 0.0;
 #pragma unroll
                 for (int k = 0; k < P; k++) {
                     const double xs = rec[RX + k];
 #pragma unroll
-                    for (int q = 0; q < CPT; q++) {
-                        const double diff = xc[q][k] - xs;
-                        d2[q][k & 1] = fma(diff, diff, d2[q][k & 1]);
-                    }
+                    for (int q = 0; q < CPT; q++) dt[q][k & 1] = fma(xc[q][k], xs, dt[q][k & 1]);
                 }
+                const double as = rec[RAC], r2 = 2.0 * rth;
 #pragma unroll
                 for (int q = 0; q < CPT; q++) {
-                    const double xa = -(d2[q][0] + d2[q][1]) * rth;
+                    const double xa = fma(dt[q][0] + dt[q][1], r2, -(ac[q] + as));
                     if constexpr (decltype(fastc)::value)
                         kx[q] = exp_nonpos_tab_inrange(xa, s_exptab);
                     else
-                        kx[q] = exp_nonpos_tab(xa, s_exptab);
+                        kx[q] = exp_nonpos_tab(fmin(xa, 0.0), s_exptab);
                 }
             };
             auto kx_any = [&]() {
@@ -446,6 +415,7 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
                     kx_phase(std::true_type{});
                 else
                     kx_phase(std::false_type{});
+                V2_EV(7);
             };
             auto dot_phase = [&]() {
                 // register entries (entries >= j are 0 on both sides)
@@ -508,37 +478,44 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
                             acc[q][0] = fma(wv, reinterpret_cast<const double *>(gown + q * TH)[0], acc[q][0]);
                     }
                 }
-                // tensor-memory entries [T0, T0 + mt): own rows by tcgen05.ld (8 entries per
-                // load), the winner's from wtm once its warp has published them
+                // tensor-memory entries [T0, T0 + mt): own rows by tcgen05.ld, TMC entries per
+                // load (the first chunk's loads issued before the publication wait); the
+                // winner's entries from wtm once its warp has published them
                 if (mt > 0) {
-                    mbar_wait(&s_mbar, mph);
-                    for (int e = 0; e < mt; e += TMC) {
-                        uint32_t r[CPT][2 * TMC];
+                    uint32_t ra[CPT][2 * TMC];
 #pragma unroll
-                        for (int q = 0; q < CPT; q++) tm_ld<TMC>(tbase + 2 * (q * T + e), r[q]);
+                    for (int q = 0; q < CPT; q++) tm_ld<TMC>(tbase + 2 * (q * T), ra[q]);
+                    V2_EV(9);
+                    while (s_pub != pubseq) {
+                    }
+                    __threadfence_block();
+                    V2_EV(10);
+                    for (int e = 0; e < mt; e += TMC) {
+                        if (e > 0)
+#pragma unroll
+                            for (int q = 0; q < CPT; q++) tm_ld<TMC>(tbase + 2 * (q * T + e), ra[q]);
                         tm_wait_ld();
 #pragma unroll
                         for (int k = 0; k < TMC; k += 2) {
                             const double2 wv = *reinterpret_cast<const double2 *>(wtm + e + k);
 #pragma unroll
                             for (int q = 0; q < CPT; q++) {
-                                acc[q][0] = fma(wv.x, tm_d(r[q], k), acc[q][0]);
-                                acc[q][1] = fma(wv.y, tm_d(r[q], k + 1), acc[q][1]);
+                                acc[q][0] = fma(wv.x, tm_d(ra[q], k), acc[q][0]);
+                                acc[q][1] = fma(wv.y, tm_d(ra[q], k + 1), acc[q][1]);
                             }
                         }
                     }
                 }
             };
-            if ((mode & 2) ? false : ((wid >> 2) & 1)) {  // warps w and w+4 share an SMSP: opposite orders
+            if (LAGP_V2_STAG_EXPR) {  // warps w and w+4 share an SMSP: opposite orders
                 dot_phase();
                 kx_any();
             } else {
                 kx_any();
-                V2_PROBE(5, kx[0]);
                 dot_phase();
-                V2_PROBE(6, acc[0][0] + acc[0][1]);
             }
-            if (mt > 0) mph ^= 1u;
+            V2_EV(8);
+            if (mt > 0) pubseq++;
             double wn[CPT];
 #pragma unroll
             for (int q = 0; q < CPT; q++) wn[q] = (kx[q] - (acc[q][0] + acc[q][1])) * rrho;
@@ -568,12 +545,44 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
                 cov[q] = fma(-znew, wn[q], cov[q]);
                 tc[q] = fma(-ynew, wn[q], tc[q]);
             }
+            V2_EV(11);
+            if (sk2 != ~0ull) {  // (warp-uniform) the winner warp's second-best key, for the top-2 gap
+                const unsigned sh = __reduce_max_sync(0xffffffffu, (unsigned)(sk2 >> 32));
+                const unsigned sl = __reduce_max_sync(0xffffffffu, (unsigned)(sk2 >> 32) == sh ? (unsigned)sk2 : 0u);
+                if (lane == 0) glog[(j - n0) * (NW + 1) + NW] = ((unsigned long long)sh << 32) | sl;
+            }
         }
 
         // ---- flags and a5: mean = z^T y~, psi = ||y~||^2, s2 = psi (1 + eta - ||z||^2) / j
         const bool any_sent = __syncthreads_or((fl & LAGP_FLAG_SENTINEL) != 0);
         const bool any_nonf = __syncthreads_or((fl & LAGP_FLAG_NONFINITE) != 0);
-        if (wid == NW - 1) {  // the warp holding near_tie (its lane 0)
+        if (wid == NW - 1) {
+            // top-2 gap of every step: d1 = the best warp key, d2 = max(the winner warp's
+            // second best, the other warps' best keys); equal best keys give gap 0
+            const int ns = (j > n0 ? j : n0) - n0;  // greedy steps taken
+            bool tie_any = false;
+            for (int t = lane; t < ns; t += 32) {
+                const unsigned long long *lg = glog + t * (NW + 1);
+                unsigned long long k1 = 0, k2b = lg[NW];
+                int wb = 0;
+#pragma unroll
+                for (int w = 0; w < NW; w++) {
+                    const unsigned long long v = lg[w];
+                    if (v > k1) {
+                        k1 = v;
+                        wb = w;
+                    }
+                }
+#pragma unroll
+                for (int w = 0; w < NW; w++)
+                    if (w != wb && lg[w] > k2b) k2b = lg[w];
+                const double d1 = __longlong_as_double((long long)(k1 - 1ull));
+                const double d2 = k2b ? __longlong_as_double((long long)(k2b - 1ull)) : 0.0;
+                const double gap = top2_gap(d1, d2);
+                if (!(d1 > 0.0) || gap < kTieGap) tie_any = true;
+                if (A.gap_out) A.gap_out[xi * G + t] = gap;
+            }
+            const bool near_tie = __any_sync(0xffffffffu, tie_any);
             double mu = 0.0, psi = 0.0, zz = 0.0;
             for (int a = lane; a < j; a += 32) {
                 mu = fma(zyv[0][a], zyv[1][a], mu);
@@ -597,10 +606,9 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
             if (A.var) A.var[xi] = vr;
             if (A.flags) A.flags[xi] = f;
             if (f & (LAGP_FLAG_EXHAUSTED | LAGP_FLAG_NONFINITE)) atomicAdd(A.n_partial, 1);
-            if (A.gap_out)
-                for (int t = (j > n0 ? j : n0) - n0; t < G; t++)
-                    A.gap_out[xi * G + t] = __longlong_as_double(0x7ff8000000000000LL);
             }
+            if (A.gap_out)
+                for (int t = ns + lane; t < G; t += 32) A.gap_out[xi * G + t] = __longlong_as_double(0x7ff8000000000000LL);
         }
         __syncthreads();
     }
@@ -638,9 +646,9 @@ static int v2_R(int p, int cpt, int th) {
 
 bool inc_v2_plan(int n, int p, int Nprime, size_t smem_optin, IncPlan &pl) {
     if (Nprime > 1024) return false;
-    int cpt = Nprime <= 512 ? 1 : 2, th = 512;
-    const char *ev = getenv("LAGP_V2_CPT");  // A/B experiments for N' in (512, 1024]: 4 (256 thr) or 1 (1024 thr)
-    if (ev && Nprime > 512 && ev[0] == '4') { cpt = 4; th = 256; }
+    int cpt = Nprime <= 512 ? 1 : 4, th = Nprime <= 512 ? 512 : 256;
+    const char *ev = getenv("LAGP_V2_CPT");  // A/B experiments for N' in (512, 1024]: 2 (512 thr) or 1 (1024 thr)
+    if (ev && Nprime > 512 && ev[0] == '2') { cpt = 2; th = 512; }
     if (ev && Nprime > 512 && ev[0] == '1') { cpt = 1; th = 1024; }
     const int R = v2_R(p, cpt, th);
     if (R < 0) return false;
@@ -651,7 +659,7 @@ bool inc_v2_plan(int n, int p, int Nprime, size_t smem_optin, IncPlan &pl) {
     if (sf && sf[0] == '1') mode |= 1;
     const char *ns = getenv("LAGP_V2_NOSTAGGER");  // A/B: every warp runs K(x_c,x*) before the dot
     if (ns && ns[0] == '1') mode |= 2;
-    const size_t fixed = ((size_t)2 * (th / 32) * v2_rec(R) + T) * sizeof(double);
+    const size_t fixed = ((size_t)2 * (th / 32) * v2_rec(R) + T + (size_t)n * (th / 32 + 1)) * sizeof(double);
     if (smem_optin < fixed + 2048) return false;
     const size_t pair_bytes = (size_t)npc * 2 * sizeof(double);
     int S = 2 * (int)((smem_optin - fixed - 2048) / pair_bytes);
@@ -694,8 +702,6 @@ cudaError_t launch_alc_incremental_v2(const AlcArgs &a, const IncPlan &pl, int g
 
 #ifdef LAGP_V2_PROF
 extern "C" int lagp_v2_prof(long long *out) {
-    int e = (int)cudaMemcpyFromSymbol(out, lagp::g_v2_prof, sizeof(lagp::g_v2_prof));
-    if (e) return e;
-    return (int)cudaMemcpyFromSymbol(out + 160 * 8, lagp::g_v2_arrive, sizeof(lagp::g_v2_arrive));
+    return (int)cudaMemcpyFromSymbol(out, lagp::g_v2_ev, sizeof(lagp::g_v2_ev));
 }
 #endif

@@ -1,7 +1,12 @@
-"""Clock-probe timeline of the v2 incremental kernel (thread 0, first location of
-CTA 0), from the profiling build liblagp_b200_prof.so (-DLAGP_V2_PROF).
+"""Clock-probe timeline of the incremental v2 kernel: lane 0 of every warp of CTA 0
+on its first location, per greedy step, from the profiling build
+liblagp_b200_prof.so (python -m paper_1310_5182_b200.build --prof; -DLAGP_V2_PROF).
 
-    python scripts/v2_probe.py [--config C2] [--M 2000]
+    python scripts/v2_probe.py [--config C2] [--M 10000] [--steps 10,20,30,40]
+Events: 0 step start, 1 keys, 2 warp argmax, 3 posted (at the barrier), 4 after the
+barrier (winner known), 5 winner TMEM published (publishing warps), 6 1/rho formed,
+7 K(x_c,x*) done, 9/10 before/after the TMEM-publication wait, 8 dot done,
+11 downdate done. Times are cycles after the step's earliest event 0.
 """
 import argparse
 import ctypes
@@ -18,7 +23,8 @@ from lagp_data import make_config  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C2")
-ap.add_argument("--M", type=int, default=2000)
+ap.add_argument("--M", type=int, default=10000)
+ap.add_argument("--steps", default="8,20,30,40,48")
 a = ap.parse_args()
 lagp._LIB = lagp._lib.load(os.path.join(ROOT, "paper_1310_5182_b200", "liblagp_b200_prof.so"))
 cfg = make_config(a.config, M=a.M)
@@ -27,30 +33,27 @@ X, Z, XX = (torch.from_numpy(cfg[k]).to(dev) for k in ("X", "Z", "XX"))
 r = lagp.alc_batch(X, Z, XX, cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"], form="incremental", timing=True)
 torch.cuda.synchronize()
 print(r["timing"])
-buf = (ctypes.c_longlong * (160 * 8 + 160 * 32))()
+NEV = 12
+buf = (ctypes.c_longlong * (128 * 32 * NEV))()
 lagp._LIB.lagp_v2_prof(buf)
-allv = np.frombuffer(buf, dtype=np.int64)
-t = allv[:160 * 8].reshape(160, 8)
-arr = allv[160 * 8:].reshape(160, 32)
-n = cfg["n"]
-names = ["start", "keys", "warpredux", "xwarp", "record", "kx", "dot", "downdate"]
-print("step " + " ".join(f"{x:>9s}" for x in names[1:]) + "      total")
-for j in range(n):
-    row = t[j]
-    nxt = t[j + 1][0] if j + 1 < n else row[7]
-    d = []
-    prev = row[0]
-    for k in range(1, 8):
-        if row[k] == 0:
-            d.append("        -")
-            continue
-        d.append(f"{row[k] - prev:9d}")
-        prev = row[k]
-    print(f"{j:4d} " + " ".join(d) + f" {nxt - row[0]:10d}")
-print("barrier arrivals per step (cycles after the first warp; the last warp's id)")
-for j in range(cfg["n0"], n, 4):
-    a = arr[j][:16]
-    if a.min() <= 0:
+ev = np.frombuffer(buf, dtype=np.int64).reshape(128, 32, NEV).astype(np.float64)
+n, n0 = cfg["n"], cfg["n0"]
+nw = int((ev[n0, :, 0] > 0).sum())
+ev = ev[:, :nw]
+ev[ev == 0] = np.nan
+names = ["start", "keys", "wargmax", "posted", "winner", "publ", "rrho", "kx", "dot", "wait0", "wait1", "downd"]
+t0 = np.nanmin(ev[:, :, 0], axis=1)
+rel = ev - t0[:, None, None]
+step = np.append(np.diff(t0), np.nan)
+print(f"warps {nw}; cycles per step (j = n0..n-2): mean {np.nanmean(step[n0:n-1]):.0f}")
+print("mean over steps n0..n-2 of (max over warps | mean over warps) per event:")
+for k in range(NEV):
+    v = rel[n0:n - 1, :, k]
+    if np.all(np.isnan(v)):
         continue
-    rel = a - a.min()
-    print(f"{j:4d} spread {rel.max():6d}  last warp {int(rel.argmax()):2d}  " + " ".join(f"{v:5d}" for v in rel))
+    print(f"  {k:2d} {names[k]:8s} max {np.nanmean(np.nanmax(v, axis=1)):7.0f}  mean {np.nanmean(v):7.0f}")
+for j in [int(x) for x in a.steps.split(",")]:
+    print(f"step {j}: {step[j]:.0f} cycles")
+    print("  warp " + " ".join(f"{nm:>7s}" for nm in names))
+    for w in range(nw):
+        print(f"  {w:4d} " + " ".join("      -" if np.isnan(x) else f"{x:7.0f}" for x in rel[j, w]))

@@ -393,7 +393,7 @@ def test_generic_dimension(torch_dev, lagp, p, form):
     check(g, o, cfg, form)
 
 
-@pytest.mark.parametrize("env", [{"LAGP_V2_CPT": "4"}, {"LAGP_V2_CPT": "1"}, {"LAGP_V2_SFIRST": "1"},
+@pytest.mark.parametrize("env", [{"LAGP_V2_CPT": "2"}, {"LAGP_V2_CPT": "1"}, {"LAGP_V2_SFIRST": "1"},
                                  {"LAGP_V2_NOSTAGGER": "1"}, {"LAGP_INC_V1": "1"}, {"LAGP_NN_MMA": "1"},
                                  {"LAGP_NN_MMA": "0"}, {"LAGP_NN_CELLS": "0"}, {"LAGP_NN_Q": "4"},
                                  {"LAGP_NN_Q": "8"}, {"LAGP_NN_Q": "16"}])
