@@ -353,12 +353,14 @@ __global__ void nn_cell_scatter_kernel(const double *__restrict__ XX, int64_t n,
         qperm[atomicAdd(cur + nn_cell_of(XX + r * p, p, kmin, kmax, gx, gy), 1)] = (int32_t)r;
 }
 
-// FP32 centred copy of X in cell order (perm[position] = row), its FP32 norms, and
+// FP32 centred copy of X in cell order (perm[position] = row), its FP32 norms, the
+// FP64 rows in cell order (the exact keys read them without the perm indirection) and
 // B = max ||x~||^2 in FP64 (the margin's bound)
 __global__ void nn_prep_kernel(const double *__restrict__ X, int64_t N, int p, float *__restrict__ X32,
                                float *__restrict__ rn2f, unsigned long long *__restrict__ maxn2,
                                const unsigned long long *__restrict__ kmin, const unsigned long long *__restrict__ kmax,
-                               int gx, int gy, int32_t *__restrict__ cur, int32_t *__restrict__ perm) {
+                               int gx, int gy, int32_t *__restrict__ cur, int32_t *__restrict__ perm,
+                               double *__restrict__ X64c) {
     double mx = 0.0;
     double c[LAGP_PMAX];
     for (int k = 0; k < p; k++) c[k] = nn_centre(kmin, kmax, k);
@@ -368,6 +370,7 @@ __global__ void nn_prep_kernel(const double *__restrict__ X, int64_t N, int p, f
         double n2 = 0.0;
         float f2 = 0.f;
         for (int k = 0; k < p; k++) {
+            X64c[pos * p + k] = X[r * p + k];
             const double v = X[r * p + k] - c[k];
             const float vf = (float)v;
             X32[pos * p + k] = vf;
@@ -665,7 +668,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                int sorted, int32_t *__restrict__ pool_out, double *__restrict__ d2_out, int32_t *__restrict__ bufc_ws,
                uint64_t *__restrict__ bufk_ws, int32_t *__restrict__ bufi_ws, int *__restrict__ fallback_count, int gx,
                int gy, const int32_t *__restrict__ cstart, const int32_t *__restrict__ perm,
-               const int32_t *__restrict__ qperm, int qg) {
+               const int32_t *__restrict__ qperm, int qg, const double *__restrict__ X64c) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     NNSmem &s = *reinterpret_cast<NNSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
@@ -688,6 +691,34 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
     const int segcap = bufcap / nw;
     const double Bn2 = __longlong_as_double((long long)*maxn2_bits);
     const double u32 = 5.9604644775390625e-08;  // 2^-24, FP32 unit roundoff
+
+    // the pool of query q from its c exact survivors K/I (global, or s.key/s.idx):
+    // sorted (laGP_nn_pool: bitonic sort in shared memory) or selected (select_pool)
+    auto emit = [&](int q, uint64_t *K, int32_t *I, int c) {
+        int32_t *po = pool_out + (int64_t)s.qid[q] * Nprime;
+        if (sorted) {  // c <= NN_CAP here (bufcap is capped for the sorted output)
+            if (K != s.key)
+                for (int t = tid; t < c; t += blockDim.x) {
+                    s.key[t] = K[t];
+                    s.idx[t] = I[t];
+                }
+            int npow = 1;
+            while (npow < c) npow <<= 1;
+            for (int t = c + tid; t < npow; t += blockDim.x) {
+                s.key[t] = ~0ull;
+                s.idx[t] = 0x7fffffff;
+            }
+            __syncthreads();
+            bitonic_sort(s, npow);
+            for (int t = tid; t < Nprime; t += blockDim.x) {
+                po[t] = s.idx[t];
+                if (d2_out) d2_out[(int64_t)s.qid[q] * Nprime + t] = __longlong_as_double((long long)s.key[t]);
+            }
+            __syncthreads();
+        } else {
+            select_pool(s, K, I, c, Nprime, n0, po);
+        }
+    };
 
     for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
         const int64_t q0 = grp * qg;
@@ -1039,7 +1070,9 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
             }
             __syncthreads();
             // dense exact pass over the prefilter survivors (the warp segments read as
-            // one range): FP64 key, keep d2 <= tau, compacted into bufk/bufc
+            // one range): FP64 key, keep d2 <= tau, compacted into shared memory (s.key /
+            // s.idx) when the prefilter count fits, else into bufk/bufc; a query whose count
+            // lands in [N', bufcap] is selected and written at once (state 3)
             for (int q = 0; q < NN_Q; q++) {
                 if (!((act >> q) & 1u)) continue;
                 if (s.ovf[q]) {  // too many survivors: rescale below
@@ -1050,6 +1083,9 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 }
                 int tot = 0;
                 for (int w = 0; w < nw; w++) tot += s.wcnt[w][q];
+                const bool in_smem = tot <= NN_CAP;  // uniform
+                uint64_t *ok_k = in_smem ? s.key : bufk + (size_t)q * bufcap;
+                int32_t *ok_i = in_smem ? s.idx : bufc + (size_t)q * bufcap;
                 if (tid == 0) s.misc[3] = 0;
                 __syncthreads();
                 for (int tb = tid - lane; tb < tot; tb += blockDim.x) {  // warp-uniform bound
@@ -1060,9 +1096,10 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                     if (t < tot) {
                         int w = 0, off = t;
                         while (off >= s.wcnt[w][q]) { off -= s.wcnt[w][q]; w++; }
-                        r = __ldg(perm + bufi[q * bufcap + w * segcap + off]);  // stored position -> row of X
+                        const int sp = bufi[q * bufcap + w * segcap + off];  // stored position
+                        r = __ldg(perm + sp);                                // -> row of X
                         double xr[P ? P : LAGP_PMAX];
-                        load_row<P>(X, r, p, xr);
+                        load_row<P>(X64c, sp, p, xr);  // = row r of X
                         d2 = row_d2<P>(xr, s.qx[q], p);
                         ok = d2 <= s.tau[q];
                     }
@@ -1072,15 +1109,20 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                         if (lane == 0) pos = atomicAdd(&s.misc[3], __popc(m));
                         pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(m & ((1u << lane) - 1u));
                         if (ok) {
-                            bufk[q * bufcap + pos] = d2_key(d2);
-                            bufc[q * bufcap + pos] = r;
+                            ok_k[pos] = d2_key(d2);
+                            ok_i[pos] = r;
                         }
                     }
                 }
                 __syncthreads();
+                const int c = s.misc[3];
                 if (tid == 0) {
-                    s.valid[q] = s.misc[3];  // exact d2 <= tau, all of them in bufk/bufc
-                    s.cnt[q] = s.misc[3];
+                    s.valid[q] = c;  // exact d2 <= tau, all of them in ok_k/ok_i
+                    s.cnt[q] = c;
+                }
+                if (in_smem && c >= Nprime && c <= bufcap) {
+                    emit(q, s.key, s.idx, c);
+                    if (tid == 0) s.state[q] = 3;
                 }
                 __syncthreads();
             }
@@ -1108,10 +1150,10 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
         if (tid < NN_Q && s.state[tid] == 0) s.state[tid] = 2;
         __syncthreads();
 
-        // ---- per-query exact selection and output
+        // ---- per-query exact selection and output (queries not written yet)
         for (int q = 0; q < nq; q++) {
+            if (s.state[q] == 3) continue;
             int c;
-            int32_t *po = pool_out + (int64_t)s.qid[q] * Nprime;
             uint64_t *qk = bufk + (size_t)q * bufcap;
             int32_t *qi = bufc + (size_t)q * bufcap;
             if (s.state[q] == 2) {
@@ -1122,27 +1164,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 c = s.cnt[q];
             }
             __syncthreads();
-            if (sorted) {  // c <= NN_CAP here (bufcap is capped for the sorted output)
-                for (int t = tid; t < c; t += blockDim.x) {
-                    s.key[t] = qk[t];
-                    s.idx[t] = qi[t];
-                }
-                int npow = 1;
-                while (npow < c) npow <<= 1;
-                for (int t = c + tid; t < npow; t += blockDim.x) {
-                    s.key[t] = ~0ull;
-                    s.idx[t] = 0x7fffffff;
-                }
-                __syncthreads();
-                bitonic_sort(s, npow);
-                for (int t = tid; t < Nprime; t += blockDim.x) {
-                    po[t] = s.idx[t];
-                    if (d2_out) d2_out[(int64_t)s.qid[q] * Nprime + t] = __longlong_as_double((long long)s.key[t]);
-                }
-                __syncthreads();
-            } else {
-                select_pool(s, qk, qi, c, Nprime, n0, po);  // in the query's global buffer
-            }
+            emit(q, qk, qi, c);
         }
     }
 }
@@ -1179,9 +1201,10 @@ static void nn_cells(int64_t N, int p, int *gx, int *gy) {
 
 // Workspace layout: [maxn2 bits, per-dimension min / max keys (512 B)] [X32: N*p floats] [rn2f: N floats]
 // [perm: N] [cell counts, starts (C+1), cursors] for the rows and again for the queries [qperm: Mmax]
+// [X64c: N*p doubles, X in cell order]
 // [compacted rows] [survivor keys] [filter rows], the last three bufcap per query
 struct NNLayout {
-    size_t x32, rn2f, perm, rcnt, rstart, rcur, qcnt, qstart, qcur, qperm, rest;
+    size_t x32, rn2f, perm, rcnt, rstart, rcur, qcnt, qstart, qcur, qperm, x64c, rest;
     int gx, gy;
 };
 static inline size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -1200,6 +1223,7 @@ static NNLayout nn_layout(int64_t N, int p, int64_t Mmax) {
     L.qstart = o; o += al256((C + 1) * sizeof(int32_t));
     L.qcur = o; o += al256(C * sizeof(int32_t));
     L.qperm = o; o += al256((size_t)(Mmax > 0 ? Mmax : 1) * sizeof(int32_t));
+    L.x64c = o; o += al256((size_t)N * p * sizeof(double));
     L.rest = o;
     return L;
 }
@@ -1213,7 +1237,7 @@ static cudaError_t launch_nn_t(const double *X, const float *X32, const float *r
                                const unsigned long long *kmin, const unsigned long long *kmax, int64_t N, int p,
                                const double *XX, int64_t M, int Nprime, int n0, int sorted, int32_t *pool, double *d2,
                                char *w, int grid, int *fb, cudaStream_t st, int gx, int gy, const int32_t *cstart,
-                               const int32_t *perm, const int32_t *qperm, int qg) {
+                               const int32_t *perm, const int32_t *qperm, int qg, const double *X64c) {
     size_t smem = sizeof(NNSmem);
     cudaError_t e = cudaFuncSetAttribute(nn_pool_kernel<P, MMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1224,7 +1248,7 @@ static cudaError_t launch_nn_t(const double *X, const float *X32, const float *r
     w += (size_t)grid * NN_Q * bc * sizeof(uint64_t);
     int32_t *bi = (int32_t *)w;
     nn_pool_kernel<P, MMA><<<grid, NN_THREADS, smem, st>>>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, bc, sorted,
-                                                      pool, d2, bcmp, bk, bi, fb, gx, gy, cstart, perm, qperm, qg);
+                                                      pool, d2, bcmp, bk, bi, fb, gx, gy, cstart, perm, qperm, qg, X64c);
     return cudaGetLastError();
 }
 
@@ -1276,6 +1300,7 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
             *rcur = (int32_t *)(w + L.rcur), *qcnt = (int32_t *)(w + L.qcnt), *qstart = (int32_t *)(w + L.qstart),
             *qcur = (int32_t *)(w + L.qcur), *qperm = (int32_t *)(w + L.qperm);
     char *rest = w + L.rest;
+    double *X64c = (double *)(w + L.x64c);
     cudaError_t e;
     if (!prepared) {
         e = cudaMemsetAsync(mx, 0, sizeof(unsigned long long) * (1 + LAGP_PMAX), st);  // maxn2, kmin
@@ -1292,7 +1317,7 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
         nn_bounds_kernel<<<blocks < 148 ? blocks : 148, 256, 0, st>>>(X, N, p, kmin, kmax);
         nn_cell_hist_kernel<<<blocks, 256, 0, st>>>(X, N, p, kmin, kmax, L.gx, L.gy, rcnt);
         nn_cell_scan_kernel<<<1, 1024, 0, st>>>(rcnt, C, rstart, rcur);
-        nn_prep_kernel<<<blocks, 256, 0, st>>>(X, N, p, X32, rn2f, mx, kmin, kmax, L.gx, L.gy, rcur, perm);
+        nn_prep_kernel<<<blocks, 256, 0, st>>>(X, N, p, X32, rn2f, mx, kmin, kmax, L.gx, L.gy, rcur, perm, X64c);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         if (launches) (*launches) += 4;
@@ -1314,7 +1339,7 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
     const char *evm = getenv("LAGP_NN_MMA");
     const bool mma = p == 8 && (evm ? evm[0] == '1' : (double)Nprime <= 0.004 * (double)N);
     const int qg = nn_group_size(M, grid, p, mma);
-#define NN_ARGS X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st, L.gx, L.gy, rstart, perm, qperm, qg
+#define NN_ARGS X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st, L.gx, L.gy, rstart, perm, qperm, qg, X64c
     switch (p) {
         case 1: return launch_nn_t<1, false>(NN_ARGS);
         case 2: return launch_nn_t<2, false>(NN_ARGS);
