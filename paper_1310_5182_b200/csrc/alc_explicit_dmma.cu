@@ -13,18 +13,20 @@
 // Shared-memory strides are chosen so every fragment load is conflict-free:
 // K^{-1} row stride KL ≡ 4 (mod 16) doubles, k_c tile row stride 68 ≡ 4 (mod 16).
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "block_ops.cuh"
 #include "launch.h"
 
 namespace lagp {
 
-constexpr int DM_THREADS = 256;  // 8 warps
-constexpr int DM_T = 64;         // candidates per tile: 8 per warp
-// tile row stride (doubles). 64-bit shared loads are served per half-warp, so the
-// B fragment tile[4s+k][c0+g] (k, g < 4 within a half-warp) is conflict-free iff
+// NWD warps per CTA (8: two CTAs per SM; 16: one CTA per SM, so that the per-CTA k_c
+// caches of all resident CTAs — 148 x n x N' doubles — stay inside L2); each warp owns 8
+// candidate columns of a tile of DM_T = 8 NWD candidates.
+// Tile row stride DM_T + 4 (doubles). 64-bit shared loads are served per half-warp, so
+// the B fragment tile[4s+k][c0+g] (k, g < 4 within a half-warp) is conflict-free iff
 // TL ≡ 4 (mod 16); the same rule gives KL ≡ 4 (mod 16) for the A fragment.
-constexpr int DM_TL = 68;
+__host__ __device__ constexpr int dm_tl(int nwd) { return 8 * nwd + 4; }
 
 __host__ __device__ inline int dm_kl(int n) {
     int kl = (n + 3) & ~3;
@@ -34,10 +36,10 @@ __host__ __device__ inline int dm_kl(int n) {
 __host__ __device__ inline int dm_kr(int n) { return (n + 7) & ~7; }
 __host__ __device__ inline int dm_vl(int n) { return dm_kr(n) > dm_kl(n) ? dm_kr(n) : dm_kl(n); }
 // smem (doubles): K kr*kl | tiles 2*kr*TL | Xj r4(n*p) | h,w,ks,us,yv 5*vl | red 160
-__host__ __device__ inline size_t dm_smem_bytes(int n, int p, int Npad) {
+__host__ __device__ inline size_t dm_smem_bytes(int n, int p, int Npad, int nwd) {
     const int kl = dm_kl(n), kr = dm_kr(n);
     (void)Npad;  // kappa_c / chosen live in the CTA's global slab: smem does not grow with N'
-    return ((size_t)kr * kl + 2 * (size_t)kr * DM_TL + (size_t)((n * p + 3) & ~3) + 5 * (size_t)dm_vl(n) + 160) *
+    return ((size_t)kr * kl + 2 * (size_t)kr * dm_tl(nwd) + (size_t)((n * p + 3) & ~3) + 5 * (size_t)dm_vl(n) + 160) *
            sizeof(double);
 }
 
@@ -47,9 +49,20 @@ __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double
         : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void cp_async16_dm(void *smem, const void *gmem) {
+// The per-CTA k_c caches (n x N' doubles each) are the kernel's working set in L2;
+// their loads and stores carry an evict_last policy so that the streaming inputs (pool
+// indices, the rows of X) are evicted first.
+__device__ __forceinline__ uint64_t l2_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void cp_async16_dm(void *smem, const void *gmem, uint64_t pol) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol));
+}
+__device__ __forceinline__ void st_keep(double *p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
 
 // out[a] = sum_b K[a][b] v[b] (row-major, stride kl); warp per row, lanes over b.
@@ -88,8 +101,10 @@ __device__ __forceinline__ double rm_append(double *K, int kl, int j, const doub
     return s;
 }
 
-__global__ void __launch_bounds__(DM_THREADS, 2)
+template <int NWD>
+__global__ void __launch_bounds__(32 * NWD, 16 / NWD)
 alc_explicit_dmma_kernel(AlcArgs A) {
+    constexpr int DM_T = 8 * NWD, DM_TL = dm_tl(NWD);
     extern __shared__ __align__(16) double sm[];
     const int n = A.n, p = A.p, Np = A.Nprime, Npad = A.Npad;
     const int kl = dm_kl(n), kr = dm_kr(n);
@@ -115,6 +130,7 @@ alc_explicit_dmma_kernel(AlcArgs A) {
     unsigned char *chosen = reinterpret_cast<unsigned char *>(kap + Npad);
     const double eta = A.eta;
     const int G = n - A.n0;
+    const uint64_t pol = l2_evict_last();
 
     for (int64_t xi = blockIdx.x; xi < A.M; xi += gridDim.x) {
         const double rth = A.theta_vec ? 1.0 / A.theta_vec[xi] : A.rtheta;  // per-location theta (Fig 1 step 4)
@@ -150,8 +166,8 @@ alc_explicit_dmma_kernel(AlcArgs A) {
                 if (!(s > 0.0) && tid == 0) fl_s |= LAGP_FLAG_NONFINITE;
             }
             for (int c = tid; c < Np; c += blockDim.x)
-                cache[(size_t)t * Npad + c] =
-                    corr_from_d2(sqdist_fma_strided(Xj + t * p, coords + c, Npad, p), rth);
+                st_keep(cache + (size_t)t * Npad + c, corr_from_d2(sqdist_fma_strided(Xj + t * p, coords + c, Npad, p), rth),
+                        pol);
             __syncthreads();
         }
         rm_matvec(K, kl, A.n0, A.n0, h, w);
@@ -169,8 +185,8 @@ alc_explicit_dmma_kernel(AlcArgs A) {
             auto load_tile = [&](int t, double *dst) {
                 const int t0 = t * DM_T;
                 for (int e = tid; e < j * (DM_T / 2); e += blockDim.x) {
-                    const int a = e >> 5, c2 = e & 31;
-                    cp_async16_dm(dst + a * DM_TL + 2 * c2, cache + (size_t)a * Npad + t0 + 2 * c2);
+                    const int a = e / (DM_T / 2), c2 = e % (DM_T / 2);
+                    cp_async16_dm(dst + a * DM_TL + 2 * c2, cache + (size_t)a * Npad + t0 + 2 * c2, pol);
                 }
                 asm volatile("cp.async.commit_group;\n" ::);
             };
@@ -278,8 +294,8 @@ alc_explicit_dmma_kernel(AlcArgs A) {
             rm_matvec(K, kl, j + 1, j + 1, h, w);
             if (j + 1 < n)
                 for (int c = tid; c < Np; c += blockDim.x)
-                    cache[(size_t)j * Npad + c] =
-                        corr_from_d2(sqdist_fma_strided(Xj + j * p, coords + c, Npad, p), rth);
+                    st_keep(cache + (size_t)j * Npad + c,
+                            corr_from_d2(sqdist_fma_strided(Xj + j * p, coords + c, Npad, p), rth), pol);
             __syncthreads();
         }
 
@@ -301,28 +317,45 @@ alc_explicit_dmma_kernel(AlcArgs A) {
     }
 }
 
-cudaError_t launch_alc_explicit_dmma(const AlcArgs &a, int grid, cudaStream_t st) {
-    size_t smem = dm_smem_bytes(a.n, a.p, a.Npad);
+// LAGP_DM_WARPS=16 (A/B): one 16-warp CTA per SM instead of two 8-warp CTAs
+static int dm_warps() {
+    const char *ev = getenv("LAGP_DM_WARPS");
+    return (ev && ev[0] == '1') ? 16 : 8;
+}
+
+template <int NWD>
+static cudaError_t dm_launch_t(const AlcArgs &a, int grid, cudaStream_t st) {
+    size_t smem = dm_smem_bytes(a.n, a.p, a.Npad, NWD);
     cudaError_t e =
-        cudaFuncSetAttribute(alc_explicit_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(alc_explicit_dmma_kernel<NWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    alc_explicit_dmma_kernel<<<grid, DM_THREADS, smem, st>>>(a);
+    alc_explicit_dmma_kernel<NWD><<<grid, 32 * NWD, smem, st>>>(a);
     return cudaGetLastError();
 }
 
-int alc_explicit_dmma_blocks_per_sm(int n, int p, int Npad) {
+cudaError_t launch_alc_explicit_dmma(const AlcArgs &a, int grid, cudaStream_t st) {
+    return dm_warps() == 8 ? dm_launch_t<8>(a, grid, st) : dm_launch_t<16>(a, grid, st);
+}
+
+template <int NWD>
+static int dm_bps_t(int n, int p, int Npad) {
     int nb = 0;
-    size_t smem = dm_smem_bytes(n, p, Npad);
-    if (cudaFuncSetAttribute(alc_explicit_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    size_t smem = dm_smem_bytes(n, p, Npad, NWD);
+    if (cudaFuncSetAttribute(alc_explicit_dmma_kernel<NWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess) {
         cudaGetLastError();  // do not leave a sticky error for the next launch check
         return 0;
     }
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, alc_explicit_dmma_kernel, DM_THREADS, smem) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, alc_explicit_dmma_kernel<NWD>, 32 * NWD, smem) !=
+        cudaSuccess) {
         cudaGetLastError();
         nb = 0;
     }
     return nb;
+}
+
+int alc_explicit_dmma_blocks_per_sm(int n, int p, int Npad) {
+    return dm_warps() == 8 ? dm_bps_t<8>(n, p, Npad) : dm_bps_t<16>(n, p, Npad);
 }
 
 }  // namespace lagp
