@@ -53,13 +53,16 @@ namespace lagp {
 #ifndef LAGP_V2_STAG_EXPR
 #define LAGP_V2_STAG_EXPR ((mode & 2) ? false : ((wid >> 2) & 1))
 #endif
+#ifndef LAGP_V2R_C2
+#define LAGP_V2R_C2 2
+#endif
 #ifndef LAGP_V2R_C4
 #define LAGP_V2R_C4 6
 #endif
 template <int P, int CPT, int TH>
 struct V2R {
     static constexpr int value =
-        (TH == 1024) ? 2 : (CPT == 1) ? 16 : (CPT == 2 ? (P <= 4 ? 8 : 4) : (P <= 4 ? 8 : LAGP_V2R_C4));
+        (TH == 1024) ? 2 : (CPT == 1) ? 16 : (CPT == 2 ? (P <= 4 ? 8 : LAGP_V2R_C2) : (P <= 4 ? 8 : LAGP_V2R_C4));
 };
 
 // TMEM entries per candidate: each thread owns 256 KB / TH of tensor memory (its warp's
@@ -357,6 +360,7 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
             const int mt = j <= T0 ? 0 : (j < T1 ? j : T1) - T0;
             if (mt > 0 && wid == ((cstar & (TH - 1)) >> 5)) {
                 const int qs = cstar / TH, wlane = cstar & 31;
+                tm_wait_st();  // the previous steps' TMEM stores (off the key/argmax path)
                 for (int e = 0; e < mt; e += 8) {
                     uint32_t r[16];
                     tm_ld<8>(tbase + 2 * (qs * T + e), r);
@@ -483,6 +487,7 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
                 // winner's entries from wtm once its warp has published them
                 if (mt > 0) {
                     uint32_t ra[CPT][2 * TMC];
+                    tm_wait_st();  // this thread's TMEM stores of the previous steps
 #pragma unroll
                     for (int q = 0; q < CPT; q++) tm_ld<TMC>(tbase + 2 * (q * T), ra[q]);
                     V2_EV(9);
@@ -529,7 +534,6 @@ alc_incremental_v2_kernel(AlcArgs A, int S, int mode) {
             } else if (j >= T0 && j < T1) {
 #pragma unroll
                 for (int q = 0; q < CPT; q++) tm_st1(tbase + 2 * (q * T + (j - T0)), wn[q]);
-                tm_wait_st();  // this step's stores land before the next reads
             } else if (j >= S0 && j < S1) {
                 double *dst = reinterpret_cast<double *>(wsm2 + ((j - S0) >> 1) * NPC + tid) + ((j - S0) & 1);
 #pragma unroll

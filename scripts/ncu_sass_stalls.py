@@ -34,3 +34,8 @@ for _, _, s, _, st in recs:
         agg[k] = agg.get(k, 0) + v
 ta = sum(agg.values()) or 1
 print("by reason: " + ", ".join(f"{k[6:]} {100 * v / ta:.1f}%" for k, v in sorted(agg.items(), key=lambda kv: -kv[1])[:12]))
+if "--reason" in sys.argv:
+    rs = "stall_" + sys.argv[sys.argv.index("--reason") + 1]
+    print(f"top by {rs}:")
+    for addr, src, s, ie, st in sorted(recs, key=lambda x: -x[4].get(rs, 0))[:40]:
+        print(f"{addr - base:6x} {100 * st.get(rs, 0) / tot:5.2f}% {src[:60]}")
