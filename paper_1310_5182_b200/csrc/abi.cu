@@ -185,8 +185,10 @@ lagp_status plan_design(int32_t p, int32_t n, int32_t Nprime, int64_t M, int32_t
     if (alc_form == LAGP_ALC_AUTO) {
         lagp::IncPlan probe{};
         const bool v2 = lagp::inc_v2_plan(n, p, Nprime, (size_t)optin - 2048, probe);
-        alc_form = (v2 || lagp::inc_plan(n, p, Nprime, P.Npad, (size_t)optin - 2048).ok) ? LAGP_ALC_INCREMENTAL
-                                                                                          : LAGP_ALC_EXPLICIT;
+        alc_form = (v2 || lagp::inc_plan(n, p, Nprime, P.Npad, (size_t)optin - 2048).ok ||
+                    lagp::inc_stream_plan(n, p, Nprime, probe))
+                       ? LAGP_ALC_INCREMENTAL
+                       : LAGP_ALC_EXPLICIT;
     }
     P.form = alc_form;
     P.incremental = alc_form == LAGP_ALC_INCREMENTAL;
@@ -198,22 +200,34 @@ lagp_status plan_design(int32_t p, int32_t n, int32_t Nprime, int64_t M, int32_t
         // 1024-thread kernel of alc_incremental.cu (kept for N' > 1024 and other p)
         const char *v1 = getenv("LAGP_INC_V1");
         const bool force_v1 = v1 && v1[0] == '1';
-        if (force_v1 || !lagp::inc_v2_plan(n, p, Nprime, (size_t)optin - 2048, P.inc)) {
+        // the HBM-streaming kernel for pools beyond the v1 kernel (N' > 8192), or by
+        // LAGP_INC_STREAM=1 for any N' > 1024 (A/B)
+        const char *sv = getenv("LAGP_INC_STREAM");
+        const bool want_stream =
+            Nprime > 1024 &&
+            (sv ? sv[0] == '1' : !lagp::inc_plan(n, p, Nprime, P.Npad, (size_t)optin - 2048).ok);
+        alc_bps = 1;
+        if (!force_v1 && !want_stream && lagp::inc_v2_plan(n, p, Nprime, (size_t)optin - 2048, P.inc)) {
+            P.cache_stride = P.inc.cache_doubles;
+        } else if (want_stream && lagp::inc_stream_plan(n, p, Nprime, P.inc)) {
+            P.cache_stride = P.inc.cache_doubles;
+            alc_bps = 2;
+            // keep the slabs (N' x (p + 3 + n) doubles per CTA) under ~16 GiB
+            const int64_t cap = ((int64_t)16 << 30) / (P.cache_stride * (int64_t)sizeof(double));
+            if (cap < (int64_t)alc_bps * P.sms) alc_bps = -(int)(cap > 1 ? cap : 1);  // negative: absolute grid
+        } else {
             P.inc = lagp::inc_plan(n, p, Nprime, P.Npad, (size_t)optin - 2048);
             if (!P.inc.ok)
                 return fail(LAGP_EINVAL, "incremental form: Nprime=%d / n=%d exceed this build's limits", Nprime, n);
             P.cache_stride = (int64_t)P.inc.global_entries * P.Npad + 1024;
-        } else {
-            P.cache_stride = P.inc.cache_doubles;
         }
-        alc_bps = 1;
     } else {
         alc_bps = P.use_dmma ? lagp::alc_explicit_dmma_blocks_per_sm(n, p, P.Npad)
                              : lagp::alc_explicit_blocks_per_sm(P.ld, n, p, P.Npad);
     }
-    if (alc_bps <= 0)
+    if (alc_bps == 0)
         return fail(LAGP_EINVAL, "local-design state does not fit in shared memory (n=%d, Nprime=%d)", n, Nprime);
-    const int alc_grid_max = alc_bps * P.sms;
+    const int alc_grid_max = alc_bps > 0 ? alc_bps * P.sms : -alc_bps;
     // chunk of locations per NN+ALC round: bounds the pool buffer (chunk × N' int32)
     // (at most 65,536 locations and a ~1 GiB pool buffer per chunk)
     P.chunk = M < 65536 ? M : 65536;
@@ -226,6 +240,7 @@ lagp_status plan_design(int32_t p, int32_t n, int32_t Nprime, int64_t M, int32_t
 
 cudaError_t launch_design(const DesignPlan &P, const lagp::AlcArgs &a, cudaStream_t st) {
     const int grid = (int)(a.M < P.alc_grid ? a.M : P.alc_grid);
+    if (P.incremental && P.inc.stream) return lagp::launch_alc_incremental_stream(a, grid, st);
     if (P.incremental && P.inc.v2) return lagp::launch_alc_incremental_v2(a, P.inc, grid, st);
     if (P.incremental) return lagp::launch_alc_incremental(a, P.inc, grid, st);
     return P.use_dmma ? lagp::launch_alc_explicit_dmma(a, grid, st) : lagp::launch_alc_explicit(a, grid, st);
@@ -271,7 +286,8 @@ lagp_status alc_batch_impl(const double *X, int64_t N, int32_t p, const double *
     LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(P.nn_grid, N, p, Nprime, false, P.chunk)));
     LAGP_CUDA(ws.alloc((void **)&cache, (size_t)P.alc_grid * P.cache_stride * sizeof(double)));
     // per-CTA slab: pool coordinates [p][Npad] (+ kappa and chosen flags for the DFMA kernel)
-    LAGP_CUDA(ws.alloc((void **)&coords, (size_t)P.alc_grid * (p + 2) * P.Npad * sizeof(double)));
+    if (!(P.incremental && (P.inc.v2 || P.inc.stream)))  // pool-coordinate slabs: explicit forms and v1
+        LAGP_CUDA(ws.alloc((void **)&coords, (size_t)P.alc_grid * (p + 2) * P.Npad * sizeof(double)));
     LAGP_CUDA(ws.alloc((void **)&counters, 2 * sizeof(int)));
     LAGP_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int), st));
     if (timing)
@@ -501,7 +517,8 @@ lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *
     LAGP_CUDA(ws.alloc((void **)&pool, (size_t)P.chunk * Nprime * sizeof(int32_t)));
     LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(P.nn_grid, N, p, Nprime, false, P.chunk)));
     LAGP_CUDA(ws.alloc((void **)&cache, (size_t)P.alc_grid * P.cache_stride * sizeof(double)));
-    LAGP_CUDA(ws.alloc((void **)&coords, (size_t)P.alc_grid * (p + 2) * P.Npad * sizeof(double)));
+    if (!(P.incremental && (P.inc.v2 || P.inc.stream)))  // pool-coordinate slabs: explicit forms and v1
+        LAGP_CUDA(ws.alloc((void **)&coords, (size_t)P.alc_grid * (p + 2) * P.Npad * sizeof(double)));
     // counters: [0] final-stage EXHAUSTED/NONFINITE flags (the last design and the
     // last MLE/prediction: the flags the caller gets), [1] NN fallbacks, [2] the
     // earlier stages' flags (not reported: a later stage replaces that design)

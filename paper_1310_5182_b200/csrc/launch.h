@@ -56,12 +56,16 @@ struct IncPlan {
     int64_t cache_doubles;  // per-CTA slab doubles (v2)
     int tfirst;             // v2 mode: bit 0 shared-memory entries before the tensor-memory ones, bit 1 no stagger
     int threads;            // v2: threads per CTA
+    bool stream;            // alc_incremental_stream.cu (state in HBM, N' <= 65536)
 };
 IncPlan inc_plan(int n, int p, int Nprime, int Npad, size_t smem_optin);
 // alc_incremental_v2.cu: one barrier per step, 512 threads, 1-2 candidates per thread
 bool inc_v2_plan(int n, int p, int Nprime, size_t smem_optin, IncPlan &pl);
 cudaError_t launch_alc_incremental_v2(const AlcArgs &a, const IncPlan &pl, int grid, cudaStream_t st);
 cudaError_t launch_alc_incremental(const AlcArgs &a, const IncPlan &pl, int grid, cudaStream_t st);
+// alc_incremental_stream.cu: per-candidate state in an HBM slab (cache_doubles per CTA), 2 CTAs/SM
+bool inc_stream_plan(int n, int p, int Nprime, IncPlan &pl);
+cudaError_t launch_alc_incremental_stream(const AlcArgs &a, int grid, cudaStream_t st);
 int alc_explicit_dmma_blocks_per_sm(int n, int p, int Npad);
 
 // mle.cu (row f2): local MLE of theta on given designs + prediction at theta-hat

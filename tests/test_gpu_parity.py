@@ -227,12 +227,14 @@ def test_large_pool_explicit(torch_dev, lagp, form):
     check(g, o, cfg, form)
 
 
-def test_incremental_rejects_large_pool(torch_dev, lagp):
+@pytest.mark.parametrize("Nprime,n,p", [(9000, 20, 2), (12000, 30, 2), (20000, 24, 8)])
+def test_incremental_stream_large_pool(torch_dev, lagp, Nprime, n, p):
+    """N' > 8192 (the paper's LGBB N' = 10,000 variant, C5's large pools): the
+    incremental form on the HBM-streaming kernel (per-candidate state in HBM)."""
     torch, dev = torch_dev
-    cfg = make_config("C5_2d", M=2, Nprime=9000, n=20)
-    with pytest.raises(lagp.LagpError, match="incremental"):
-        lagp.alc_batch(T(torch, dev, cfg["X"]), T(torch, dev, cfg["Z"]), T(torch, dev, cfg["XX"]), cfg["d"], cfg["g"],
-                       cfg["n0"], cfg["n"], cfg["Nprime"], form="incremental")
+    cfg = make_config("C5_2d" if p == 2 else "C5_8d", M=3, Nprime=Nprime, n=n)
+    g, o = run_both(torch, dev, lagp, cfg, form="incremental")
+    check(g, o, cfg, "incremental")
 
 
 @pytest.mark.parametrize("form", FORMS)
@@ -371,14 +373,26 @@ def _synthetic(seed, N, M, p):
     return X, Z, XX
 
 
+@pytest.mark.parametrize("stream", ["0", "1"])
 @pytest.mark.parametrize("Nprime,p,n", [(1500, 2, 30), (4000, 8, 40), (8192, 2, 24), (2048, 3, 70)])
-def test_incremental_large_pools(torch_dev, lagp, Nprime, p, n):
+def test_incremental_large_pools(torch_dev, lagp, Nprime, p, n, stream):
     """1024 < N' <= 8192: the 1024-thread incremental kernel with several
-    candidates per thread (the v2 kernel covers N' <= 1024)."""
+    candidates per thread (the v2 kernel covers N' <= 1024), and the HBM-streaming
+    kernel on the same shapes (LAGP_INC_STREAM=1)."""
+    import os
+
     torch, dev = torch_dev
     X, Z, XX = _synthetic(Nprime + p, 40000, 6, p)
     cfg = dict(X=X, Z=Z, XX=XX, d=0.02 * p, g=1e-4, n0=6, n=n, Nprime=Nprime)
-    g, o = run_both(torch, dev, lagp, cfg, form="incremental")
+    old = os.environ.get("LAGP_INC_STREAM")
+    os.environ["LAGP_INC_STREAM"] = stream
+    try:
+        g, o = run_both(torch, dev, lagp, cfg, form="incremental")
+    finally:
+        if old is None:
+            os.environ.pop("LAGP_INC_STREAM", None)
+        else:
+            os.environ["LAGP_INC_STREAM"] = old
     check(g, o, cfg, "incremental")
 
 
@@ -450,4 +464,4 @@ def test_north_star_entry_point(torch_dev, lagp):
     big = make_config("C5_2d", M=2, Nprime=12000, n=20)
     rb = lagp.alc_batch(*(T(torch, dev, big[k]) for k in ("X", "Z", "XX")), big["d"], big["g"], big["n0"], big["n"],
                         big["Nprime"], timing=True)
-    assert rb["timing"]["alc_form"] == "explicit"
+    assert rb["timing"]["alc_form"] == "incremental"  # the HBM-streaming kernel
