@@ -9,7 +9,11 @@ want = ["Kernel Name", "gpu__time_duration.sum", "sm__pipe_fp64_cycles_active.av
         "sm__warps_active.avg.pct_of_peak_sustained_active", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "lts__t_sector_hit_rate.pct",
         "sm__inst_executed_pipe_fp64.sum", "smsp__inst_executed.sum", "launch__grid_size",
-        "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed"]
+        "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+        "SM_C.TriageCompute.smsp__pipe_tensor_subpipe_dmma_cycles_active.avg",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
 for val in rows[2:]:
     d = dict(zip(hdr, val)); u = dict(zip(hdr, units))
     for k in want:

@@ -20,11 +20,13 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--form", default="explicit")
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--n", type=int, default=None)
+ap.add_argument("--Nprime", type=int, default=None)
 ap.add_argument("--lib", default=None, help="experiment build of the library (e.g. an ablation .so)")
 a = ap.parse_args()
 if a.lib:
     lagp._LIB = lagp._lib.load(a.lib)
-cfg = make_config(a.config, M=a.M) if a.n is None else make_config(a.config, M=a.M, n=a.n)
+over = {k: v for k, v in (("n", a.n), ("Nprime", a.Nprime)) if v is not None}
+cfg = make_config(a.config, M=a.M, **over)
 dev = torch.device("cuda", 0)
 X, Z, XX = (torch.from_numpy(cfg[k]).to(dev) for k in ("X", "Z", "XX"))
 for _ in range(a.reps):
