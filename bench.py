@@ -388,7 +388,9 @@ def main():
                 "explicit_dfma": "alc_explicit_kernel"}[ran]
         roof = {"bound": "alu", "kernel": kern, "alc_form": ran,
                 "achieved": achieved, "peak": nominal, "unit": "TFLOP/s", "frac": achieved / nominal,
-                "traffic": traffic_for(workload, ran, design_launches),
+                "traffic": (traffic_for(workload, ran, design_launches) or {}).get("bytes_per_launch"),
+                "traffic_unit": "bytes per launch (dram read + write, ncu --set full of the same workload)",
+                "traffic_source": (traffic_for(workload, ran, design_launches) or {}).get("profile"),
                 "work": ("incremental: (N'-j-1)(2j+3p+8) flop per location-step j=0..n-1, FP64, exp not counted"
                          if ran == "incremental" else
                          "paper count (N'-j)(2j^2+4j) flop per location-step (SURVEY §8d), FP64"),

@@ -19,4 +19,17 @@ $NCU -k regex:alc_explicit_dmma -o gpurun_out/prof_expl_$R python scripts/profil
 $NCU -k regex:mle_kernel -o gpurun_out/prof_mle_$R python scripts/mle_profile.py --M 10000 --reps 1 > /dev/null 2>&1
 $NCU -k regex:alc_scores_gemm -o gpurun_out/prof_f4_$R python scripts/fig4_sweep.py --nmin 512 --nmax 512 --reps 1 --check "" > /dev/null 2>&1
 $NCU -k regex:alc_incremental_stream -o gpurun_out/prof_stream_$R python scripts/profile_run.py --config C5_8d --M 512 --Nprime 20000 --n 50 --form incremental > /dev/null 2>&1
-ls gpurun_out | grep "_$R"
+# summaries on the box (the reports together exceed gpurun's 64 MiB copy-back); keep the
+# v2 and NN reports
+for f in gpurun_out/prof_*_$R.ncu-rep; do
+  b=$(basename $f .ncu-rep)
+  python scripts/ncu_summary.py $f > gpurun_out/sum_${b#prof_}.txt 2>&1
+done
+python scripts/traffic_json.py $R C2:incremental:gpurun_out/prof_v2_$R.ncu-rep C2:nn:gpurun_out/prof_nn_$R.ncu-rep \
+  C4:incremental:gpurun_out/prof_v2_c4_$R.ncu-rep C4:nn:gpurun_out/prof_nn_c4_$R.ncu-rep \
+  C2:explicit:gpurun_out/prof_expl_$R.ncu-rep C2:mle:gpurun_out/prof_mle_$R.ncu-rep \
+  F4:scores_gemm:gpurun_out/prof_f4_$R.ncu-rep C5_20000:stream:gpurun_out/prof_stream_$R.ncu-rep > gpurun_out/traffic_$R.log 2>&1
+cp profiles/ncu_traffic.json gpurun_out/ncu_traffic_$R.json
+rm -f gpurun_out/prof_nn_c4_$R.ncu-rep gpurun_out/prof_v2_c4_$R.ncu-rep gpurun_out/prof_expl_$R.ncu-rep \
+  gpurun_out/prof_mle_$R.ncu-rep gpurun_out/prof_f4_$R.ncu-rep gpurun_out/prof_stream_$R.ncu-rep
+ls gpurun_out

@@ -1,8 +1,9 @@
-"""Write profiles/ncu_traffic.json (dram bytes per launch of each bench kernel)
-from the round's ncu --set full reports (run here after gpurun):
+"""Write profiles/ncu_traffic.json — DRAM bytes (read + write) per launch of each
+bench kernel at each workload — from the round's ncu --set full reports (each a
+single-launch capture, -c 1), for bench.py's roofline.traffic:
 
-    python scripts/traffic_json.py rNN gpurun_out/prof_alc_incremental_rNN.ncu-rep:incremental \
-        gpurun_out/prof_alc_explicit_dmma_rNN.ncu-rep:explicit gpurun_out/prof_nn_pool_rNN.ncu-rep:nn
+    python scripts/traffic_json.py rNN WORKLOAD:KEY:report.ncu-rep [...]
+    -> {WORKLOAD: {KEY: {"bytes": B, "launches": 1, "profile": ..., "kernel": ..., "ncu_duration_ms": t}}}
 """
 import csv
 import io
@@ -15,19 +16,24 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rnd = sys.argv[1]
 out = {}
 for spec in sys.argv[2:]:
-    rep, key = spec.rsplit(":", 1)
+    workload, key, rep = spec.split(":", 2)
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
                           "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
+    if len(rows) < 3:
+        print(f"skip {spec}: no data")
+        continue
     hdr, units, val = rows[0], rows[1], rows[2]
     d = dict(zip(hdr, val))
     u = dict(zip(hdr, units))
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    tscale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
+    tscale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3, "ns": 1e-6, "us": 1e-3, "ms": 1.0,
+              "s": 1e3}
     b = sum(float(d[k].replace(",", "")) * scale[u[k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     t = float(d["gpu__time_duration.sum"].replace(",", "")) * tscale[u["gpu__time_duration.sum"]]
-    out[key] = {"dram_bytes_per_launch": b, "kernel": d["Kernel Name"][:80], "ncu_duration_ms": t,
-                "source": f"{os.path.basename(rep)} (ncu --set full, M=10000, round {rnd})"}
+    out.setdefault(workload, {})[key] = {"bytes": b, "launches": 1, "kernel": d["Kernel Name"][:80],
+                                         "ncu_duration_ms": t,
+                                         "profile": f"{os.path.basename(rep)} (ncu --set full, round {rnd})"}
 json.dump(out, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
 print(json.dumps(out, indent=1))
