@@ -15,6 +15,13 @@
 
 #include "launch.h"
 
+// NVTX ranges (header-only NVTX v3: no link dependency; inert unless a profiler is attached)
+#include <nvtx3/nvToolsExt.h>
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 namespace {
 
 thread_local std::string g_err;
@@ -297,8 +304,11 @@ lagp_status alc_batch_impl(const double *X, int64_t N, int32_t p, const double *
     for (int64_t m0 = 0; m0 < M; m0 += P.chunk) {
         const int64_t mc = (M - m0) < P.chunk ? (M - m0) : P.chunk;
         if (timing) LAGP_CUDA(cudaEventRecord(ev[1], st));
-        LAGP_CUDA(lagp::launch_nn(X, N, p, XX + m0 * p, mc, P.chunk, Nprime, n0, false, pool, nullptr, nnws,
-                                  lagp::nn_grid(mc, P.sms, Nprime), counters + 1, st, m0 > 0, &launches));
+        {
+            NvtxRange nv_nn("lagp: a1 NN pool");
+            LAGP_CUDA(lagp::launch_nn(X, N, p, XX + m0 * p, mc, P.chunk, Nprime, n0, false, pool, nullptr, nnws,
+                                      lagp::nn_grid(mc, P.sms, Nprime), counters + 1, st, m0 > 0, &launches));
+        }
         if (timing) LAGP_CUDA(cudaEventRecord(ev[2], st));
         lagp::AlcArgs a = design_args(P, X, N, p, Z, d, g, n0, n, Nprime);
         a.XX = XX + m0 * p; a.M = mc;
@@ -311,7 +321,10 @@ lagp_status alc_batch_impl(const double *X, int64_t N, int32_t p, const double *
         a.gap_out = gap_out ? gap_out + m0 * (n - n0) : nullptr;
         a.cache = cache; a.coords = coords;
         a.n_partial = counters;
-        LAGP_CUDA(launch_design(P, a, st));
+        {
+            NvtxRange nv_d("lagp: a2-a5 local design");
+            LAGP_CUDA(launch_design(P, a, st));
+        }
         launches++;
         if (timing) {
             LAGP_CUDA(cudaEventRecord(ev[3], st));
@@ -469,7 +482,10 @@ lagp_status laGP_mle(const double *X, int64_t N, int32_t p, const double *Z, con
         if (!mp.smem) LAGP_CUDA(ws.alloc((void **)&a.ws, mp.ws));
         LAGP_CUDA(ws.alloc((void **)&a.n_partial, sizeof(int)));
         LAGP_CUDA(cudaMemsetAsync(a.n_partial, 0, sizeof(int), st));
-        LAGP_CUDA(lagp::launch_mle(a, mp.grid, st));
+        {
+            NvtxRange nv_m("lagp: f2 local MLE");
+            LAGP_CUDA(lagp::launch_mle(a, mp.grid, st));
+        }
         LAGP_CUDA(cudaMemcpyAsync(&host_partial, a.n_partial, sizeof(int), cudaMemcpyDeviceToHost, st));
         LAGP_CUDA(cudaStreamSynchronize(st));
         if (host_partial > 0) st_ret = fail(LAGP_PARTIAL, "%d location(s) flagged NONFINITE", host_partial);
@@ -533,8 +549,11 @@ lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *
     for (int64_t m0 = 0; m0 < M; m0 += P.chunk) {
         const int64_t mc = (M - m0) < P.chunk ? (M - m0) : P.chunk;
         if (timing) LAGP_CUDA(cudaEventRecord(ev[1], st));
-        LAGP_CUDA(lagp::launch_nn(X, N, p, XX + m0 * p, mc, P.chunk, Nprime, n0, false, pool, nullptr, nnws,
-                                  lagp::nn_grid(mc, P.sms, Nprime), counters + 1, st, m0 > 0, &launches));
+        {
+            NvtxRange nv_nn("lagp: a1 NN pool");
+            LAGP_CUDA(lagp::launch_nn(X, N, p, XX + m0 * p, mc, P.chunk, Nprime, n0, false, pool, nullptr, nnws,
+                                      lagp::nn_grid(mc, P.sms, Nprime), counters + 1, st, m0 > 0, &launches));
+        }
         if (timing) {
             LAGP_CUDA(cudaEventRecord(ev[2], st));
             LAGP_CUDA(cudaEventSynchronize(ev[2]));
@@ -557,7 +576,10 @@ lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *
             a.gap_out = nullptr;
             a.cache = cache; a.coords = coords;
             a.n_partial = s == stages - 1 ? counters : counters + 2;
+            {
+                NvtxRange nv_d("lagp: a2-a5 local design");
             LAGP_CUDA(launch_design(P, a, st));
+            }
             launches++;
             if (timing) LAGP_CUDA(cudaEventRecord(ev[3], st));
             // step 3: theta_x = theta-hat_n(x) | D_n(x, theta_x), and step 5 at it
@@ -572,7 +594,10 @@ lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *
             ma.ws = mlews;
             ma.n_partial = s == stages - 1 ? counters : counters + 2;
             const int mgrid = (int)(mc < mp.grid ? mc : mp.grid);
-            LAGP_CUDA(lagp::launch_mle(ma, mgrid, st));
+            {
+                NvtxRange nv_m("lagp: f2 local MLE");
+                LAGP_CUDA(lagp::launch_mle(ma, mgrid, st));
+            }
             launches++;
             if (timing) {
                 LAGP_CUDA(cudaEventRecord(ev[4], st));
