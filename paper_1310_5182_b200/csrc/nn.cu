@@ -9,7 +9,7 @@
 // queries. The pass is a paired-FP32 (FFMA2, sm_100) prefilter on an FP32 copy
 // of X with a rigorous rounding margin; only rows that pass it get the exact
 // FP64 key, which alone decides membership. Selection is threshold-then-sort: a strided sample of X gives a
-// per-query threshold tau at ~1.5 N' expected survivors; the filter pass
+// per-query threshold tau at ~1.25 N' expected survivors (NN_TGT); the filter pass
 // appends (d^2, i) with d^2 <= tau to a per-query buffer; the buffer is
 // bitonic-sorted in shared memory by (key bits, index) and its first N' rows
 // are the pool. If the count lands outside [N', NN_CAP] the threshold is
@@ -27,6 +27,12 @@ constexpr int NN_THREADS = 256;
 constexpr int NN_Q = 16;
 constexpr int NN_CAP = 8192;
 constexpr int NN_MAX_ROUNDS = 6;
+#ifndef NN_S2F
+#define NN_S2F 128    // T2 sample rows per N/N' (measured: 64 -> 128 with the 1.25 target below, C2/C4/C3 NN -5/-6/-9 %)
+#endif
+#ifndef NN_TGT
+#define NN_TGT 1.25   // expected survivors per N' under the sampled threshold
+#endif
 
 struct NNSmem {
     uint64_t key[NN_CAP];
@@ -675,12 +681,12 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
     const int64_t ngroups = (M + qg - 1) / qg;  // qg = 8 or 16 query locations per group
     // sample sizes and target ranks (see the threshold phase)
     const int S1 = (int)(N < 1024 ? N : 1024);
-    int64_t s2 = (int64_t)64 * N / (Nprime > 0 ? Nprime : 1);
+    int64_t s2 = (int64_t)NN_S2F * N / (Nprime > 0 ? Nprime : 1);
     if (s2 < S1) s2 = S1;
     if (s2 > 65536) s2 = 65536;
     if (s2 > N) s2 = N;
     const int S2 = (int)s2;
-    const int r2 = (int)ceil(1.5 * (double)Nprime * (double)S2 / (double)N) + 12;
+    const int r2 = (int)ceil(NN_TGT * (double)Nprime * (double)S2 / (double)N) + 12;
     int r1 = (int)ceil(4.0 * (double)r2 * (double)S1 / (double)S2) + 4;
     if (Nprime >= N) r1 = S1 + 1;
     // per query: bufi = filter survivors (stored positions, cell order) in NN_THREADS/32 warp segments of segcap rows;
@@ -750,7 +756,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
         //     target, so it bounds the T2 order statistic with margin).
         // T2: S2 = min(N, 64 N / N') strided rows; the T2 distances below tau1 are
         //     listed (~4 r2 per query) and tau = their r2-th smallest, where r2 puts
-        //     ~1.5 N' expected survivors under tau (relative spread ~1/sqrt(r2) = 10 %).
+        //     ~NN_TGT N' expected survivors under tau (relative spread ~1/sqrt(r2) ~ 6 %).
         {
             float *t1 = reinterpret_cast<float *>(s.key);  // NN_Q x 1024 floats (64 KB)
             const double step1 = (double)N / (double)S1;
