@@ -43,6 +43,7 @@ struct NNSmem {
     float qn2f[NN_Q];            // ||q~||^2 in FP32
     double tau[NN_Q];
     float thrf[NN_Q];            // FP32 prefilter threshold: tau + rounding margin, rounded up
+    float thq[NN_Q];             // thrf - ||q~||^2, rounded up (the FFMA2 filter's test)
     double qn2[NN_Q];            // ||x_q||^2 (for the margin)
     int cnt[NN_Q];
     int rank[NN_Q];
@@ -866,6 +867,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 s.thrf[q] = isfinite(thr) ? __double2float_ru(thr) : INFINITY;
             }
             if (tid < NN_Q && s.state[tid] != 0) s.thrf[tid] = __int_as_float(0x7fc00000);  // NaN: inactive
+            if (tid < NN_Q) s.thq[tid] = __fsub_ru(s.thrf[tid], s.qn2f[tid]);
             __syncthreads();
             unsigned act = 0;
             for (int q = 0; q < NN_Q; q++) act |= (s.state[q] == 0 ? 1u : 0u) << q;
@@ -1041,12 +1043,14 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                         float qv[P ? P : LAGP_PMAX];
     #pragma unroll
                         for (int k = 0; k < (P ? P : LAGP_PMAX); k++) qv[k] = s.qf[q][k];
-                        const float qn = s.qn2f[q], thr = s.thrf[q];
+                        // ||x~||^2 - 2 x~.q~ <= thr - ||q~||^2 (rounded up): one rounding fewer than
+                        // evaluating ||q~||^2 + ||x~||^2 first, inside the margin's factor 2
+                        const float thq = s.thq[q];
                         bool hit[4];
                         unsigned mm[4];
     #pragma unroll
                         for (int u = 0; u < 4; u++) {
-                            hit[u] = fmaf(-2.f, row_dotf<P>(xf[u], qv, p), qn + rn[u]) <= thr;
+                            hit[u] = fmaf(-2.f, row_dotf<P>(xf[u], qv, p), rn[u]) <= thq;
                             mm[u] = __ballot_sync(0xffffffffu, hit[u]);
                         }
                         // append to this warp's own segment of the query's buffer: the warp
