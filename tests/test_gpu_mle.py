@@ -110,7 +110,8 @@ def test_alc_batch_per_location_theta(torch_dev, lagp, form):
 
 @pytest.mark.parametrize(
     "name,M,N,over",
-    [("C1", 48, None, {}), ("C2", 16, 20000, {}), ("C3", 24, None, {}), ("C1", 4, 60, dict(n0=5, n=60, Nprime=60))],
+    [("C1", 48, None, {}), ("C2", 16, 20000, {}), ("C3", 24, None, {}), ("C1", 4, 60, dict(n0=5, n=60, Nprime=60)),
+     ("C5_2d", 3, None, dict(n=20, Nprime=9000))],  # N' > 8192: the HBM-streaming design kernel, per-location theta
 )
 @pytest.mark.parametrize("form", ["explicit", "incremental"])
 def test_local_fit_vs_oracle(torch_dev, lagp, name, M, N, over, form):

@@ -407,6 +407,35 @@ def test_generic_dimension(torch_dev, lagp, p, form):
     check(g, o, cfg, form)
 
 
+@pytest.mark.parametrize("p", [1, 5])
+def test_incremental_stream_generic_p(torch_dev, lagp, p):
+    """The HBM-streaming kernel's p = 1 and generic-p (P = 0) instantiations (N' > 8192)."""
+    torch, dev = torch_dev
+    X, Z, XX = _synthetic(100 + p, 40000, 4, p)
+    cfg = dict(X=X, Z=Z, XX=XX, d=0.05 * p, g=1e-4, n0=5, n=24, Nprime=9500)
+    g, o = run_both(torch, dev, lagp, cfg, form="incremental")
+    check(g, o, cfg, "incremental")
+
+
+def test_explicit_dmma_one_cta_per_sm(torch_dev, lagp):
+    """LAGP_DM_WARPS=16: the explicit DMMA kernel as one 16-warp CTA per SM (128-candidate
+    tiles) against the oracle."""
+    import os
+
+    torch, dev = torch_dev
+    cfg = make_config("C2", M=24, N=20000)
+    old = os.environ.get("LAGP_DM_WARPS")
+    os.environ["LAGP_DM_WARPS"] = "16"
+    try:
+        g, o = run_both(torch, dev, lagp, cfg, form="explicit")
+    finally:
+        if old is None:
+            os.environ.pop("LAGP_DM_WARPS", None)
+        else:
+            os.environ["LAGP_DM_WARPS"] = old
+    check(g, o, cfg, "explicit")
+
+
 @pytest.mark.parametrize("env", [{"LAGP_V2_CPT": "2"}, {"LAGP_V2_CPT": "1"}, {"LAGP_V2_SFIRST": "1"},
                                  {"LAGP_V2_NOSTAGGER": "1"}, {"LAGP_INC_V1": "1"}, {"LAGP_NN_MMA": "1"},
                                  {"LAGP_NN_MMA": "0"}, {"LAGP_NN_CELLS": "0"}, {"LAGP_NN_Q": "4"},
