@@ -100,7 +100,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
 
 if __name__ == "__main__":
     if "--prof" in sys.argv:  # clock-probe build of the incremental kernel (scripts/v2_probe.py)
-        print(build(force=True, defines=["LAGP_V2_PROF"], lib=os.path.join(PKG, "liblagp_b200_prof.so"),
+        print(build(force=True, defines=["LAGP_V2_PROF", "LAGP_MLE_PROF", "LAGP_NN_PROF"], lib=os.path.join(PKG, "liblagp_b200_prof.so"),
                     obj_dir=os.path.join(ROOT, "build", "obj_prof")))
     else:
         build(force="--force" in sys.argv, verbose=True)

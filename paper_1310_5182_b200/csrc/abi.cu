@@ -704,11 +704,17 @@ lagp_status laGP_nn_pool(const double *X, int64_t N, int32_t p, const double *XX
         void *nnws = nullptr;
         int *fb = nullptr;
         const int grid = lagp::nn_grid(M, num_sms(), Nprime);
-        LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(grid, N, p, Nprime, true, M)));
+        // test switch LAGP_NN_POOL_SELECT=<n0>: the pool as the design kernels receive it
+        // (selected, not sorted: the n0 nearest first in (d^2, index) order, the rest in
+        // any order; d2_out is not written)
+        const char *sel = getenv("LAGP_NN_POOL_SELECT");
+        const int n0s = sel ? atoi(sel) : -1;
+        const bool sorted = !(n0s >= 0 && n0s <= Nprime && n0s <= LAGP_NMAX);
+        LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(grid, N, p, Nprime, sorted, M)));
         LAGP_CUDA(ws.alloc((void **)&fb, sizeof(int)));
         LAGP_CUDA(cudaMemsetAsync(fb, 0, sizeof(int), st));
-        LAGP_CUDA(lagp::launch_nn(X, N, p, XX, M, M, Nprime, Nprime, true, pool_out, d2_out, nnws, grid, fb, st, false,
-                                  nullptr));
+        LAGP_CUDA(lagp::launch_nn(X, N, p, XX, M, M, Nprime, sorted ? Nprime : n0s, sorted, pool_out,
+                                  sorted ? d2_out : nullptr, nnws, grid, fb, st, false, nullptr));
     cleanup:;
     }
     cudaError_t e = cudaStreamSynchronize(st);

@@ -33,6 +33,31 @@ constexpr int MLE_THREADS = 128;
 constexpr int MLE_NW = MLE_THREADS / 32;
 constexpr int MLE_MAXIT = 64;
 
+#ifdef LAGP_MLE_PROF
+// phase clocks (profiling builds only): thread 0 of CTA b accumulates cycles per phase
+// 0 K + Cholesky, 1 inverse, 2 W^T W, 3 a = A Y + psi, 4 v = P a, 5 tr(APAP), 6 traces,
+// 7 evaluations counted
+__device__ long long g_mle_ph[1024][8];
+#define MLE_PH(k)                                                                   \
+    do {                                                                            \
+        if (threadIdx.x == 0 && blockIdx.x < 1024) {                                \
+            long long t_;                                                           \
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_)::"memory");            \
+            g_mle_ph[blockIdx.x][k] += t_ - ph_t0;                                  \
+            ph_t0 = t_;                                                             \
+        }                                                                           \
+    } while (0)
+#define MLE_PH0()                                                                   \
+    long long ph_t0 = 0;                                                            \
+    if (threadIdx.x == 0) {                                                         \
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(ph_t0)::"memory");             \
+        if (blockIdx.x < 1024) g_mle_ph[blockIdx.x][7] += 1;                        \
+    }
+#else
+#define MLE_PH(k) do {} while (0)
+#define MLE_PH0() do {} while (0)
+#endif
+
 struct MleEval {
     double l, g, h, psi;
     bool ok;
@@ -291,12 +316,16 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, double *X, double *Y,
     const int hv_ = nv >= 24 ? nv / 2 : nv;
     double *Tb = vec + 5 * nv + nv * p, *tp = Tb + (nv - hv_) * hv_, *red = tp + 64 * MLE_NW;
     const double theta = exp(tau), rth = 1.0 / theta;
+    MLE_PH0();
     if (!mle_chol(Y, X, n, rth, eta, deriv)) {
         r.ok = false;
         return r;
     }
+    MLE_PH(0);
     const double ld = mle_inverse(X, Y, rd, Tb, n);
+    MLE_PH(1);
     mle_wtw(Y, X, n);
+    MLE_PH(2);
     double pp[2] = {0.0, ld};
     for (int a = tid; a < n; a += blockDim.x) {
         double sa = 0.0;
@@ -305,6 +334,7 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, double *X, double *Y,
         pp[0] = fma(Yr[a], sa, pp[0]);
     }
     cta_sum<2>(pp, red);  // (also orders the al writes)
+    MLE_PH(3);
     const double psi = pp[0], logdet = 2.0 * pp[1];
     r.psi = psi;
     if (!(psi > 0.0)) {
@@ -321,6 +351,7 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, double *X, double *Y,
         for (int b = 0; b < n; b++) sa = fma(symP(X, n, a, b), al[b], sa);
         v[a] = sa;
     }
+    MLE_PH(4);
     // tr(APAP) = sum_ab T_ab T_ba with T = A P: 8x8 tiles of T on DMMA, a tile pair (I, J),
     // I <= J, per warp; the partner tile's transpose through the warp's 8x8 scratch
     double tTT = 0.0;
@@ -356,6 +387,7 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, double *X, double *Y,
         }
     }
     __syncthreads();  // v
+    MLE_PH(5);
     double tAP = 0.0, tAQ = 0.0, aQa = 0.0, aPa = 0.0, vAv = 0.0;
     // the lower triangle (off-diagonal terms twice; P and Q vanish on the diagonal)
     for (int a = wid; a < n; a += MLE_NW)
@@ -375,6 +407,7 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, double *X, double *Y,
         }
     double t6[6] = {tAP, tAQ, tTT, aQa, aPa, vAv};
     cta_sum<6>(t6, red);
+    MLE_PH(6);
     const double qv = t6[4] / psi;
     r.g = -0.5 * t6[0] + hn * qv;
     r.h = -0.5 * t6[1] + 0.5 * t6[2] - hn * (2.0 * t6[5] - t6[3]) / psi + hn * qv * qv;
@@ -528,3 +561,13 @@ cudaError_t launch_mle(const MleArgs &a, int grid, cudaStream_t st) {
 }
 
 }  // namespace lagp
+
+#ifdef LAGP_MLE_PROF
+extern "C" int lagp_mle_prof(long long *out, int reset) {
+    if (reset) {
+        static long long z[1024][8];
+        return (int)cudaMemcpyToSymbol(lagp::g_mle_ph, z, sizeof(z));
+    }
+    return (int)cudaMemcpyFromSymbol(out, lagp::g_mle_ph, sizeof(lagp::g_mle_ph));
+}
+#endif

@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "lagp_internal.cuh"
 #include "launch.h"
 
@@ -32,6 +34,33 @@ constexpr int NN_MAX_ROUNDS = 6;
 #endif
 #ifndef NN_TGT
 #define NN_TGT 1.25   // expected survivors per N' under the sampled threshold
+#endif
+
+#ifdef LAGP_NN_PROF
+// phase clocks (profiling builds only): thread 0 of CTA b accumulates cycles per phase:
+// 0 group setup + T1, 1 T2, 2 cell list / runs, 3 filter, 4 exact pass, 5 rescale,
+// 6 selection + output, 7 groups (count); 8 rounds (count)
+__device__ long long g_nn_ph[1024][12];
+#define NN_PH(k)                                                                    \
+    do {                                                                            \
+        if (threadIdx.x == 0 && blockIdx.x < 1024) {                                \
+            long long t_;                                                           \
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_)::"memory");            \
+            g_nn_ph[blockIdx.x][k] += t_ - ph_t0;                                   \
+            ph_t0 = t_;                                                             \
+        }                                                                           \
+    } while (0)
+#define NN_PHC(k)                                                                   \
+    do {                                                                            \
+        if (threadIdx.x == 0 && blockIdx.x < 1024) g_nn_ph[blockIdx.x][k] += 1;     \
+    } while (0)
+#define NN_PH0()                                                                    \
+    long long ph_t0 = 0;                                                            \
+    if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%clock64;" : "=l"(ph_t0)::"memory");
+#else
+#define NN_PH(k) do {} while (0)
+#define NN_PHC(k) do {} while (0)
+#define NN_PH0() do {} while (0)
 #endif
 
 struct NNSmem {
@@ -58,6 +87,7 @@ struct NNSmem {
     unsigned long long n0k[LAGP_NMAX];  // the n0 nearest (select_pool)
     int n0i[LAGP_NMAX];
     int wcnt[NN_THREADS / 32][NN_Q];    // filter appends per (warp segment, query)
+    int fcnt[NN_Q];                     // filter appends per query (multi-axis cell list)
     int ovf[NN_Q];                      // a warp segment overflowed
     int nrng;                           // filter row ranges (in s.hist during the filter)
     int qid[NN_Q];                      // the group's query indices (cell order)
@@ -302,18 +332,35 @@ __device__ __forceinline__ int nn_cell_hi(double v, double lo, double invw, int 
     if (!(t < (double)G)) return G - 1;
     return t < 0.0 ? 0 : (int)t;
 }
+// The cell grid: s[k] equal-width slabs on coordinate k < nd (mixed-radix cell id,
+// coordinate 0 most significant). The two-axis grid (nd <= 2, the filter visits runs
+// of cell columns) is s = {gx, gy}; the multi-axis grid (multi = 1, p >= 4) cuts up to
+// NN_CELL_DIMS coordinates and the filter visits a per-query list of cells (see the
+// filter rounds).
+constexpr int NN_CELL_DIMS = 8;
+constexpr int NN_CELL_SMAX = 16;    // slabs per coordinate (multi-axis grid)
+constexpr int NN_CELL_LIST = 8192;  // cells of the multi-axis grid (the list lives in s.key / s.idx)
+struct NNGrid {
+    int s[NN_CELL_DIMS];
+    int nd;
+    int multi;
+    int ncell;
+};
 __device__ __forceinline__ int nn_cell_of(const double *x, int p, const unsigned long long *kmin,
-                                          const unsigned long long *kmax, int gx, int gy) {
-    const int cx = nn_cell_lo(x[0], nn_lo(kmin, 0), nn_invw(kmin, kmax, 0, gx), gx);
-    const int cy = (gy > 1 && p > 1) ? nn_cell_lo(x[1], nn_lo(kmin, 1), nn_invw(kmin, kmax, 1, gy), gy) : 0;
-    return cx * gy + cy;
+                                          const unsigned long long *kmax, const NNGrid &g) {
+    int c = 0;
+    for (int k = 0; k < g.nd && k < p; k++) {
+        const int G = g.s[k];
+        c = c * G + nn_cell_lo(x[k], nn_lo(kmin, k), nn_invw(kmin, kmax, k, G), G);
+    }
+    return c;
 }
 
 // cell histogram of n points (rows of X, or a chunk of query locations)
 __global__ void nn_cell_hist_kernel(const double *__restrict__ X, int64_t n, int p, const unsigned long long *__restrict__ kmin,
-                                    const unsigned long long *__restrict__ kmax, int gx, int gy, int32_t *__restrict__ counts) {
+                                    const unsigned long long *__restrict__ kmax, NNGrid g, int32_t *__restrict__ counts) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(counts + nn_cell_of(X + r * p, p, kmin, kmax, gx, gy), 1);
+        atomicAdd(counts + nn_cell_of(X + r * p, p, kmin, kmax, g), 1);
 }
 
 // exclusive scan of C <= 16384 cell counts by one block of 1024 threads:
@@ -354,10 +401,10 @@ __global__ void __launch_bounds__(1024) nn_cell_scan_kernel(const int32_t *__res
 
 // query locations in cell order: qperm[position] = location
 __global__ void nn_cell_scatter_kernel(const double *__restrict__ XX, int64_t n, int p, const unsigned long long *__restrict__ kmin,
-                                       const unsigned long long *__restrict__ kmax, int gx, int gy, int32_t *__restrict__ cur,
+                                       const unsigned long long *__restrict__ kmax, NNGrid g, int32_t *__restrict__ cur,
                                        int32_t *__restrict__ qperm) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
-        qperm[atomicAdd(cur + nn_cell_of(XX + r * p, p, kmin, kmax, gx, gy), 1)] = (int32_t)r;
+        qperm[atomicAdd(cur + nn_cell_of(XX + r * p, p, kmin, kmax, g), 1)] = (int32_t)r;
 }
 
 // FP32 centred copy of X in cell order (perm[position] = row), its FP32 norms, the
@@ -366,13 +413,13 @@ __global__ void nn_cell_scatter_kernel(const double *__restrict__ XX, int64_t n,
 __global__ void nn_prep_kernel(const double *__restrict__ X, int64_t N, int p, float *__restrict__ X32,
                                float *__restrict__ rn2f, unsigned long long *__restrict__ maxn2,
                                const unsigned long long *__restrict__ kmin, const unsigned long long *__restrict__ kmax,
-                               int gx, int gy, int32_t *__restrict__ cur, int32_t *__restrict__ perm,
+                               NNGrid g, int32_t *__restrict__ cur, int32_t *__restrict__ perm,
                                double *__restrict__ X64c) {
     double mx = 0.0;
     double c[LAGP_PMAX];
     for (int k = 0; k < p; k++) c[k] = nn_centre(kmin, kmax, k);
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t pos = atomicAdd(cur + nn_cell_of(X + r * p, p, kmin, kmax, gx, gy), 1);
+        const int64_t pos = atomicAdd(cur + nn_cell_of(X + r * p, p, kmin, kmax, g), 1);
         perm[pos] = (int32_t)r;
         double n2 = 0.0;
         float f2 = 0.f;
@@ -581,9 +628,119 @@ __device__ void radix_select_kv(NNSmem &s, const uint64_t *K, const int32_t *I, 
 // follow in any order (positions >= n0 never affect results: every candidate's
 // score and the (Delta, index) argmax are order-independent).
 // K/I may be shared or global memory (large pools select in the global buffers).
+//
+// With dmax (every live key's d2 <= dmax, finite, > 0) the two ranks are found in one
+// pass: a histogram over NN_SB value bins bin(d2) = min(NN_SB - 1, floor(d2 NN_SB / dmax))
+// (monotone in the key), the bins holding rank Nprime and rank n0 gathered to shared
+// memory and ranked there by counting under the (key, index) order. Bins too full for
+// the shared lists fall back to the radix selects.
+constexpr int NN_SB = 512;     // value bins (in s.whist)
+constexpr int NN_SB_L1 = 256;  // gathered entries of the rank-Nprime bin (in s.whist)
 __device__ void select_pool(NNSmem &s, uint64_t *K, int32_t *I, int c, int Nprime, int n0,
-                            int32_t *__restrict__ po) {
+                            int32_t *__restrict__ po, double dmax) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    unsigned long long kth, k0th;
+    int ith, i0th;
+#ifndef NN_FASTSEL
+#define NN_FASTSEL 1
+#endif
+    bool fast = NN_FASTSEL && dmax > 0.0 && dmax < INFINITY;  // uniform
+    if (fast) {
+        unsigned *hb = &s.whist[0][0];
+        uint64_t *l1k = reinterpret_cast<uint64_t *>(hb + NN_SB);
+        int32_t *l1i = reinterpret_cast<int32_t *>(l1k + NN_SB_L1);
+        const double sc = (double)NN_SB / dmax;
+        for (int b = tid; b < NN_SB; b += blockDim.x) hb[b] = 0;
+        if (tid == 0) { s.misc[2] = 0; s.misc[3] = 0; }
+        __syncthreads();
+        for (int base = tid - lane; base < c; base += blockDim.x) {  // warp-uniform bound
+            const int t = base + lane;
+            const unsigned long long k = t < c ? K[t] : ~0ull;
+            const bool live = k != ~0ull;
+            const unsigned bin = live ? (unsigned)min(NN_SB - 1, (int)(__longlong_as_double((long long)k) * sc)) : 0xffffu;
+            const unsigned m = __match_any_sync(0xffffffffu, bin);
+            if (live && (__ffs(m) - 1) == lane) atomicAdd(&hb[bin], (unsigned)__popc(m));
+        }
+        __syncthreads();
+        if (wid == 0) {  // bins of rank Nprime and rank n0: scan[0..2] / scan[3..5] = bin, rank in bin, count
+            constexpr int PL = NN_SB / 32;
+            unsigned loc[PL], tot = 0;
+#pragma unroll
+            for (int i = 0; i < PL; i++) { loc[i] = hb[lane * PL + i]; tot += loc[i]; }
+            unsigned incl = tot;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += y;
+            }
+            const unsigned excl = incl - tot;
+#pragma unroll
+            for (int r = 0; r < 2; r++) {
+                const unsigned need = r == 0 ? (unsigned)Nprime : (unsigned)n0;
+                if (need > 0 && excl < need && incl >= need) {
+                    unsigned acc = excl;
+                    for (int i = 0; i < PL; i++) {
+                        if (acc + loc[i] >= need) {
+                            s.scan[3 * r] = lane * PL + i;
+                            s.scan[3 * r + 1] = (int)(need - acc);
+                            s.scan[3 * r + 2] = (int)loc[i];
+                            break;
+                        }
+                        acc += loc[i];
+                    }
+                }
+            }
+            if (lane == 31 && incl < (unsigned)Nprime) s.scan[2] = 1 << 30;  // (never: c >= Nprime live keys)
+        }
+        __syncthreads();
+        const int b1 = s.scan[0], r1 = s.scan[1], c1 = s.scan[2];
+        const int b0 = n0 > 0 ? s.scan[3] : -1, r0 = s.scan[4], c0 = n0 > 0 ? s.scan[5] : 0;
+        fast = c1 <= NN_SB_L1 && c0 <= LAGP_NMAX;  // uniform
+        if (fast) {
+            for (int t = tid; t < c; t += blockDim.x) {
+                const unsigned long long k = K[t];
+                if (k == ~0ull) continue;
+                const int bin = min(NN_SB - 1, (int)(__longlong_as_double((long long)k) * sc));
+                if (bin == b1) {
+                    const int pos = atomicAdd(&s.misc[2], 1);
+                    l1k[pos] = k;
+                    l1i[pos] = I[t];
+                }
+                if (bin == b0) {
+                    const int pos = atomicAdd(&s.misc[3], 1);
+                    s.n0k[pos] = k;
+                    s.n0i[pos] = I[t];
+                }
+            }
+            __syncthreads();
+            for (int t = tid; t < c1 + c0; t += blockDim.x) {  // rank by counting inside the bin
+                const bool one = t < c1;
+                const int u = one ? t : t - c1, cn = one ? c1 : c0;
+                const uint64_t *bk = one ? l1k : reinterpret_cast<const uint64_t *>(s.n0k);
+                const int32_t *bi = one ? l1i : s.n0i;
+                const unsigned long long k = bk[u];
+                const int i = bi[u];
+                int r = 0;
+                for (int v = 0; v < cn; v++) r += kv_less(bk[v], bi[v], k, i) ? 1 : 0;
+                if (r == (one ? r1 : r0) - 1) {
+                    s.redk[one ? 0 : 1] = k;
+                    s.redi[one ? 0 : 1] = i;
+                }
+            }
+            __syncthreads();
+            kth = s.redk[0];
+            ith = s.redi[0];
+            if (n0 > 0) {
+                k0th = s.redk[1];
+                i0th = s.redi[1];
+            } else {
+                k0th = 0ull;
+                i0th = -1;
+            }
+            __syncthreads();
+        }
+    }
+    if (!fast) {
     // range of the live keys
     unsigned long long kmin = ~0ull, kmax = 0ull;
     for (int t = tid; t < c; t += blockDim.x) {
@@ -611,14 +768,13 @@ __device__ void select_pool(NNSmem &s, uint64_t *K, int32_t *I, int c, int Nprim
         kmax = b > kmax ? b : kmax;
     }
     __syncthreads();
-    unsigned long long kth, k0th;
-    int ith, i0th;
     radix_select_kv(s, K, I, c, Nprime, kmin, kmax, kth, ith);
     if (n0 > 0) {
         radix_select_kv(s, K, I, c, n0, kmin, kmax, k0th, i0th);
     } else {
         k0th = 0ull;
         i0th = -1;  // no entry is <= (0, -1)
+    }
     }
     if (tid == 0) { s.misc[2] = 0; s.misc[3] = n0; }
     __syncthreads();
@@ -668,17 +824,18 @@ __device__ __forceinline__ float row_dotf(const float *xf, const float *qf, int 
 // worth it when survivors are rare (N'/N small, e.g. C4), since every hit costs a
 // serial append; the FFMA2 path is faster for denser pools (C2: 3.3 vs 3.9 ms).
 template <int P, bool MMA>
-__global__ void __launch_bounds__(NN_THREADS)
+__global__ void __launch_bounds__(NN_THREADS, 2)
 nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, const float *__restrict__ rn2f,
                const unsigned long long *maxn2_bits, const unsigned long long *__restrict__ kmin,
                const unsigned long long *__restrict__ kmax, int64_t N, int p, const double *__restrict__ XX, int64_t M, int Nprime, int n0, int bufcap,
                int sorted, int32_t *__restrict__ pool_out, double *__restrict__ d2_out, int32_t *__restrict__ bufc_ws,
-               uint64_t *__restrict__ bufk_ws, int32_t *__restrict__ bufi_ws, int *__restrict__ fallback_count, int gx,
-               int gy, const int32_t *__restrict__ cstart, const int32_t *__restrict__ perm,
+               uint64_t *__restrict__ bufk_ws, int32_t *__restrict__ bufi_ws, int *__restrict__ fallback_count, NNGrid cg,
+               const int32_t *__restrict__ cstart, const int32_t *__restrict__ perm,
                const int32_t *__restrict__ qperm, int qg, const double *__restrict__ X64c) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     NNSmem &s = *reinterpret_cast<NNSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    const int gx = cg.s[0], gy = cg.nd > 1 ? cg.s[1] : 1;  // two-axis grid (runs of cell columns)
     const int64_t ngroups = (M + qg - 1) / qg;  // qg = 8 or 16 query locations per group
     // sample sizes and target ranks (see the threshold phase)
     const int S1 = (int)(N < 1024 ? N : 1024);
@@ -723,11 +880,94 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
             }
             __syncthreads();
         } else {
-            select_pool(s, K, I, c, Nprime, n0, po);
+            select_pool(s, K, I, c, Nprime, n0, po, s.state[q] == 2 ? -1.0 : s.tau[q]);
         }
     };
 
+    // multi-axis grid: the list of cells (stored-row range [lst_a, lst_b), mask lst_m of the
+    // queries in actm it can hold a row with d^2 <= thrf for) in s.key / s.idx (free
+    // between the threshold samples and the exact pass); count in s.nrng
+    int *lst_a = reinterpret_cast<int *>(s.key), *lst_b = lst_a + NN_CELL_LIST;
+    unsigned *lst_m = reinterpret_cast<unsigned *>(s.idx);
+    auto build_list = [&](unsigned act) {
+        // A row of cell c has |x_k - q_k| >= gap_k(c, q) on every cut coordinate, so
+        // d^2(x, q) >= lb(c, q) = sum_k gap_k^2; a cell is listed for query q unless
+        // lb > thr (>= tau). Per-coordinate terms gap_k^2 are tabulated per query and
+        // slab (rounded down; the slab box is widened by a margin that covers the
+        // rounding of the cell arithmetic) and summed with round-down adds, so the
+        // computed lb never exceeds the exact one: no row with d^2 <= tau is pruned.
+        float *dlb = reinterpret_cast<float *>(&s.whist[0][0]);  // [NN_Q][NN_CELL_DIMS][NN_CELL_SMAX]
+        for (int e = tid; e < NN_Q * NN_CELL_DIMS * NN_CELL_SMAX; e += blockDim.x) {
+            const int q = e / (NN_CELL_DIMS * NN_CELL_SMAX), k = (e / NN_CELL_SMAX) % NN_CELL_DIMS,
+                      i = e % NN_CELL_SMAX;
+            float v = 0.f;
+            if (k < cg.nd && i < cg.s[k] && ((act >> q) & 1u)) {
+                const int G = cg.s[k];
+                const double lo = nn_lo(kmin, k), iw = nn_invw(kmin, kmax, k, G);
+                if (iw > 0.0) {
+                    const double rw = 1.0 / iw;
+                    const double mg = 1e-6 * rw + 1e-14 * (fabs(lo) + (double)G * rw);
+                    const double blo = i == 0 ? -INFINITY : lo + (double)i * rw - mg;
+                    const double bhi = i == G - 1 ? INFINITY : lo + (double)(i + 1) * rw + mg;
+                    const double qk = s.qx[q][k];
+                    const double gp = fmax(0.0, fmax(blo - qk, qk - bhi)) * (1.0 - 0x1p-40);
+                    v = __double2float_rd(gp * gp);
+                }
+            }
+            dlb[e] = v;
+        }
+        if (tid == 0) s.nrng = 0;
+        __syncthreads();
+        const int C = cg.ncell, per = (C + (int)blockDim.x - 1) / (int)blockDim.x;
+        const int c0 = tid * per, c1 = min(c0 + per, C);
+        int dg[NN_CELL_DIMS];  // mixed-radix digits of cell c (odometer)
+        {
+            int c = c0;
+#pragma unroll
+            for (int k = NN_CELL_DIMS - 1; k >= 0; k--) {
+                dg[k] = 0;
+                if (k < cg.nd) {
+                    dg[k] = c % cg.s[k];
+                    c /= cg.s[k];
+                }
+            }
+        }
+        for (int c = c0; c < c1; c++) {
+            unsigned m = 0, aq = act;
+            while (aq) {
+                const int q = __ffs(aq) - 1;
+                aq &= aq - 1;
+                const float *dq = dlb + q * NN_CELL_DIMS * NN_CELL_SMAX;
+                float lb = 0.f;
+#pragma unroll
+                for (int k = 0; k < NN_CELL_DIMS; k++)
+                    if (k < cg.nd) lb = __fadd_rd(lb, dq[k * NN_CELL_SMAX + dg[k]]);
+                if (!(lb > s.thrf[q])) m |= 1u << q;
+            }
+            if (m) {
+                const int a = cstart[c], b = cstart[c + 1];
+                if (b > a) {
+                    const int e = atomicAdd(&s.nrng, 1);
+                    lst_a[e] = a;
+                    lst_b[e] = b;
+                    lst_m[e] = m;
+                }
+            }
+            bool carry = true;  // next cell: increment the odometer
+#pragma unroll
+            for (int k = NN_CELL_DIMS - 1; k >= 0; k--)
+                if (carry && k < cg.nd) {
+                    dg[k]++;
+                    carry = dg[k] >= cg.s[k];
+                    if (carry) dg[k] = 0;
+                }
+        }
+        __syncthreads();
+    };
+
     for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        NN_PH0();
+        NN_PHC(7);
         const int64_t q0 = grp * qg;
         const int nq = (int)((M - q0) < qg ? (M - q0) : qg);
         if (tid < NN_Q) s.qid[tid] = tid < nq ? (qperm ? qperm[q0 + tid] : (int32_t)(q0 + tid)) : 0;
@@ -778,28 +1018,17 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 }
             }
             __syncthreads();
+            NN_PH(0);
             if (S2 > S1 && r2 <= S2) {
                 float *lst = reinterpret_cast<float *>(bufk);  // per query bufcap floats
                 const double step2 = (double)N / (double)S2;
                 // 4 sample rows per thread per pass, each query's coordinates read from
-                // shared memory once per 4 rows (as in the filter pass)
-                for (int64_t wb = (int64_t)wid * 128; wb < S2; wb += (int64_t)nw * 128) {
-                    float xf[4][P ? P : LAGP_PMAX];
-                    bool ok[4];
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const int64_t t = wb + 32 * u + lane;
-                        ok[u] = t < S2;
-                        if (ok[u]) {
-                            int64_t r = (int64_t)((double)t * step2);  // strided sample row (no 64-bit division)
-                            load_row32<P>(X32, r < N ? r : N - 1, p, xf[u]);
-                        } else {
-#pragma unroll
-                            for (int k = 0; k < (P ? P : LAGP_PMAX); k++) xf[u][k] = 0.f;
-                        }
-                    }
-#pragma unroll 1
-                    for (int q = 0; q < nq; q++) {
+                // shared memory once per 4 rows (as in the filter pass); the T2 distances
+                // <= tau1 are listed
+                auto t2_eval = [&](const float (&xf)[4][P ? P : LAGP_PMAX], const bool (&ok)[4], unsigned qm) {
+                    while (qm) {
+                        const int q = __ffs(qm) - 1;
+                        qm &= qm - 1;
                         float qv[P ? P : LAGP_PMAX];
 #pragma unroll
                         for (int k = 0; k < (P ? P : LAGP_PMAX); k++) qv[k] = s.nqf[q][k];
@@ -824,6 +1053,24 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                             }
                         }
                     }
+                };
+                const unsigned allq = nq < 32 ? (1u << nq) - 1u : ~0u;
+                for (int64_t wb = (int64_t)wid * 128; wb < S2; wb += (int64_t)nw * 128) {
+                    float xf[4][P ? P : LAGP_PMAX];
+                    bool ok[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int64_t t = wb + 32 * u + lane;
+                        ok[u] = t < S2;
+                        if (ok[u]) {
+                            int64_t r = (int64_t)((double)t * step2);  // strided sample row (no 64-bit division)
+                            load_row32<P>(X32, r < N ? r : N - 1, p, xf[u]);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < (P ? P : LAGP_PMAX); k++) xf[u][k] = 0.f;
+                        }
+                    }
+                    t2_eval(xf, ok, allq);
                 }
                 __syncthreads();
                 for (int q = wid; q < NN_Q; q += nw) {
@@ -846,10 +1093,14 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
             }
         }
 
+        NN_PH(1);
         // ---- filter rounds
         for (int round = 0; round < NN_MAX_ROUNDS; round++) {
             for (int e = tid; e < nw * NN_Q; e += blockDim.x) (&s.wcnt[0][0])[e] = 0;
-            if (tid < NN_Q) s.ovf[tid] = 0;
+            if (tid < NN_Q) {
+                s.ovf[tid] = 0;
+                s.fcnt[tid] = 0;
+            }
             if (tid < NN_Q && s.state[tid] == 0) {  // only queries still searching
                 const int q = tid;
                 s.cnt[q] = 0;
@@ -875,7 +1126,8 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
             // the cells that meet the active queries' box |x_k - q_k| <= sqrt(thr), k = 0, 1,
             // as maximal runs of stored rows (cell order is row-major: one run per cell column)
             int *rng_a = reinterpret_cast<int *>(s.hist), *rng_b = rng_a + 128;
-            if (wid == 0) {
+            if (cg.multi) build_list(act);
+            if (!cg.multi && wid == 0) {
                 double lo0 = INFINITY, hi0 = -INFINITY, lo1 = INFINITY, hi1 = -INFINITY;
                 if (lane < NN_Q && s.state[lane] == 0) {
                     const double r = sqrt((double)s.thrf[lane]);
@@ -937,13 +1189,77 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 }
             }
             __syncthreads();
+            NN_PH(2);
+            NN_PHC(8);
             const int nrng = s.nrng;
             // 4 rows per thread per iteration: each query's coordinates are loaded
             // from shared memory once per 4 rows
             // (the loop bound is warp-uniform: the ballots below need whole warps)
             // per-warp append counters in registers: lane q holds this warp's count for query q
             int wcr = 0;
-            if constexpr (MMA && P == 8) {
+            if (cg.multi) {
+                // The listed cells, one warp per cell, in passes of 128 rows (4 per lane)
+                // and a 64- or 32-row pass for the cell's tail; only the cell's listed
+                // queries are evaluated; appends through a shared per-query counter (one
+                // atomic per warp, query and pass with a hit).
+                const unsigned lt = (1u << lane) - 1u;
+                constexpr int PP = P ? P : LAGP_PMAX;
+                auto pass = [&](auto uc, int base, int b, unsigned m) {
+                    constexpr int U = decltype(uc)::value;
+                    float xf[U][PP], rn[U];
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int r = base + 32 * u + lane;
+                        if (r < b) {
+                            load_row32<P>(X32, r, p, xf[u]);
+                            rn[u] = __ldg(rn2f + r);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < PP; k++) xf[u][k] = 0.f;
+                            rn[u] = __int_as_float(0x7fc00000);  // NaN: never <= thr
+                        }
+                    }
+                    while (m) {
+                        const int q = __ffs(m) - 1;
+                        m &= m - 1;
+                        float qv[PP];
+#pragma unroll
+                        for (int k = 0; k < PP; k++) qv[k] = s.qf[q][k];
+                        const float thq = s.thq[q];
+                        bool hit[U];
+                        unsigned mm[U], tot = 0;
+#pragma unroll
+                        for (int u = 0; u < U; u++) {
+                            hit[u] = fmaf(-2.f, row_dotf<P>(xf[u], qv, p), rn[u]) <= thq;
+                            mm[u] = __ballot_sync(0xffffffffu, hit[u]);
+                            tot += __popc(mm[u]);
+                        }
+                        if (tot) {
+                            int pos = 0;
+                            if (lane == 0) pos = atomicAdd(&s.fcnt[q], (int)tot);
+                            pos = __shfl_sync(0xffffffffu, pos, 0);
+                            int32_t *qb = bufi + q * bufcap;
+#pragma unroll
+                            for (int u = 0; u < U; u++) {
+                                const int pu = pos + __popc(mm[u] & lt);
+                                if (hit[u] && pu < bufcap) qb[pu] = base + 32 * u + lane;
+                                pos += __popc(mm[u]);
+                            }
+                        }
+                    }
+                };
+                for (int e = wid; e < nrng; e += nw) {  // warp-uniform
+                    const int b = lst_b[e];
+                    const unsigned m = lst_m[e];
+                    int base = lst_a[e];
+                    for (; b - base > 96; base += 128) pass(std::integral_constant<int, 4>{}, base, b, m);
+                    if (b - base > 32) {
+                        pass(std::integral_constant<int, 2>{}, base, b, m);
+                        base += 64;
+                    }
+                    if (b - base > 0) pass(std::integral_constant<int, 1>{}, base, b, m);
+                }
+            } else if constexpr (MMA && P == 8) {
                 // Tensor-core filter (mma.sync m16n8k8 TF32): a warp takes 16 rows x 8
                 // queries per MMA, D = X~[16x8] Q~^T[8x8]; MMA coordinate k is x~ coordinate
                 // perm(k), perm(t) = 2t, perm(t + 4) = 2t + 1, so each thread's A elements
@@ -1074,11 +1390,18 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 }
                 }
             }
-            if (lane < NN_Q) {
+            if (cg.multi) {  // one segment (warp 0's) of up to bufcap rows per query
+                __syncthreads();
+                if (tid < NN_Q) {
+                    s.wcnt[0][tid] = s.fcnt[tid];
+                    if (s.fcnt[tid] > bufcap) s.ovf[tid] = 1;
+                }
+            } else if (lane < NN_Q) {
                 s.wcnt[wid][lane] = wcr;
                 if (wcr > segcap) s.ovf[lane] = 1;
             }
             __syncthreads();
+            NN_PH(3);
             // dense exact pass over the prefilter survivors (the warp segments read as
             // one range): FP64 key, keep d2 <= tau, compacted into shared memory (s.key /
             // s.idx) when the prefilter count fits, else into bufk/bufc; a query whose count
@@ -1131,11 +1454,24 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                     s.cnt[q] = c;
                 }
                 if (in_smem && c >= Nprime && c <= bufcap) {
+#ifdef LAGP_NN_PROF
+                    long long te0 = 0;
+                    if (tid == 0) asm volatile("mov.u64 %0, %%clock64;" : "=l"(te0)::"memory");
+#endif
                     emit(q, s.key, s.idx, c);
+#ifdef LAGP_NN_PROF
+                    if (tid == 0 && blockIdx.x < 1024) {
+                        long long te1;
+                        asm volatile("mov.u64 %0, %%clock64;" : "=l"(te1)::"memory");
+                        g_nn_ph[blockIdx.x][9] += te1 - te0;
+                        g_nn_ph[blockIdx.x][10] += 1;
+                    }
+#endif
                     if (tid == 0) s.state[q] = 3;
                 }
                 __syncthreads();
             }
+            NN_PH(4);
             // missed queries: rescale tau (the count of rows inside the d^2 <= tau ball
             // grows like tau^(p/2)), aiming at ~1.5 N' survivors
             if (tid < NN_Q && s.state[tid] == 0) {
@@ -1156,6 +1492,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
             }
             __syncthreads();
         }
+        NN_PH(5);
         // queries still active after the rounds fall back as well
         if (tid < NN_Q && s.state[tid] == 0) s.state[tid] = 2;
         __syncthreads();
@@ -1176,6 +1513,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
             __syncthreads();
             emit(q, qk, qi, c);
         }
+        NN_PH(6);
     }
 }
 
@@ -1190,23 +1528,71 @@ static int nn_bufcap(int Nprime, bool sorted) {
     return c;
 }
 
-// Cell grid (see nn_cell_of): gx x gy cells on coordinates 0 and 1, ~64 rows per
-// cell; gx <= 128 when gy > 1 (the filter loads one run per cell column in parallel)
-static void nn_cells(int64_t N, int p, int *gx, int *gy) {
-    const char *ev = getenv("LAGP_NN_CELLS");  // A/B: 0 = one cell (no pruning)
+// Cell grid (see nn_cell_of).
+// Two-axis grid (p <= 3, or the tensor-core filter): gx x gy cells on coordinates 0
+// and 1, ~64 rows per cell; gx <= 128 when gy > 1 (the filter loads one run per cell
+// column in parallel).
+// Multi-axis grid (p >= 4): slabs on up to NN_CELL_DIMS coordinates, ~NN_CELL_ROWS rows
+// per cell, one more slab at a time on the coordinate with the fewest (lowest first):
+// C2 (N = 10^5, p = 8) 3 x 2^7 = 384 cells, C4 (N = 10^6) 3^6 x 2^2 = 2,916 cells.
+// LAGP_NN_CELLS (A/B): 0 = one cell (no pruning), 2 = the two-axis grid.
+// rows per cell: 128 up to N = 5e5, else 256 (measured: C2 NN 1.95 vs 2.10 ms at 128 vs
+// 256; C4 18.2 vs 20.9 ms per 65,536 queries at 256 vs 128, where the 6,561-cell list
+// costs more than the finer cells save); LAGP_NN_CR overrides (A/B)
+static int nn_cell_rows(int64_t N) {
+    const char *ev = getenv("LAGP_NN_CR");
+    const int v = ev ? atoi(ev) : 0;
+    return v >= 16 ? v : (N > 500000 ? 256 : 128);
+}
+static NNGrid nn_cells(int64_t N, int p, bool mma) {
+    NNGrid g{};
+    for (int k = 0; k < NN_CELL_DIMS; k++) g.s[k] = 1;
+    g.nd = 1;
+    g.multi = 0;
+    const char *ev = getenv("LAGP_NN_CELLS");
     if (ev && ev[0] == '0') {
-        *gx = 1;
-        *gy = 1;
+        // one cell
+    } else if (p >= 4 && !mma && !(ev && ev[0] == '2')) {
+        const int nd = p < NN_CELL_DIMS ? p : NN_CELL_DIMS;
+        const double R = (double)nn_cell_rows(N);
+        int64_t prod = 1;
+        for (;;) {
+            int k = 0;
+            for (int t = 1; t < nd; t++)
+                if (g.s[t] < g.s[k]) k = t;
+            if (g.s[k] + 1 > NN_CELL_SMAX) break;
+            const int64_t np = prod / g.s[k] * (g.s[k] + 1);
+            if ((double)N / (double)np < R || np > NN_CELL_LIST) break;
+            prod = np;
+            g.s[k]++;
+        }
+        g.nd = 1;
+        for (int k = 0; k < nd; k++)
+            if (g.s[k] > 1) g.nd = k + 1;
+        g.multi = 1;
     } else if (p == 1) {
-        int64_t g = N / 64;
-        *gx = (int)(g < 1 ? 1 : (g > 16384 ? 16384 : g));
-        *gy = 1;
+        int64_t c = N / 64;
+        g.s[0] = (int)(c < 1 ? 1 : (c > 16384 ? 16384 : c));
     } else {
-        int g = (int)sqrt((double)N / 64.0);
-        g = g < 1 ? 1 : (g > 128 ? 128 : g);
-        *gx = g;
-        *gy = g;
+        int c = (int)sqrt((double)N / 64.0);
+        c = c < 1 ? 1 : (c > 128 ? 128 : c);
+        g.s[0] = c;
+        g.s[1] = c;
+        g.nd = 2;
     }
+    g.ncell = 1;
+    for (int k = 0; k < g.nd; k++) g.ncell *= g.s[k];
+    return g;
+}
+// the tensor-core filter (two-axis grid) when survivors are rare and the grid is not
+// multi-axis; LAGP_NN_MMA=1 forces it (with the two-axis grid), 0 disables it
+static bool nn_use_mma(int64_t N, int p, int Nprime) {
+    if (p != 8) return false;
+    const char *evm = getenv("LAGP_NN_MMA");
+    if (evm) return evm[0] == '1';
+    const char *ev = getenv("LAGP_NN_CELLS");
+    const bool two_axis = ev && (ev[0] == '0' || ev[0] == '2');
+    return two_axis && (double)Nprime <= 0.004 * (double)N;
 }
 
 // Workspace layout: [maxn2 bits, per-dimension min / max keys (512 B)] [X32: N*p floats] [rn2f: N floats]
@@ -1215,13 +1601,15 @@ static void nn_cells(int64_t N, int p, int *gx, int *gy) {
 // [compacted rows] [survivor keys] [filter rows], the last three bufcap per query
 struct NNLayout {
     size_t x32, rn2f, perm, rcnt, rstart, rcur, qcnt, qstart, qcur, qperm, x64c, rest;
-    int gx, gy;
+    NNGrid g;
+    bool mma;
 };
 static inline size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
-static NNLayout nn_layout(int64_t N, int p, int64_t Mmax) {
+static NNLayout nn_layout(int64_t N, int p, int64_t Mmax, int Nprime) {
     NNLayout L;
-    nn_cells(N, p, &L.gx, &L.gy);
-    const size_t C = (size_t)L.gx * L.gy;
+    L.mma = nn_use_mma(N, p, Nprime);
+    L.g = nn_cells(N, p, L.mma);
+    const size_t C = (size_t)L.g.ncell;
     size_t o = 512;
     L.x32 = o; o += al256((size_t)N * p * sizeof(float));
     L.rn2f = o; o += al256((size_t)N * sizeof(float));
@@ -1239,14 +1627,14 @@ static NNLayout nn_layout(int64_t N, int p, int64_t Mmax) {
 }
 size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime, bool sorted, int64_t Mmax) {
     const size_t bc = (size_t)nn_bufcap(Nprime, sorted);
-    return nn_layout(N, p, Mmax).rest + (size_t)grid * NN_Q * bc * (sizeof(uint64_t) + 2 * sizeof(int32_t)) + 256;
+    return nn_layout(N, p, Mmax, Nprime).rest + (size_t)grid * NN_Q * bc * (sizeof(uint64_t) + 2 * sizeof(int32_t)) + 256;
 }
 
 template <int P, bool MMA>
 static cudaError_t launch_nn_t(const double *X, const float *X32, const float *rn2f, const unsigned long long *mx,
                                const unsigned long long *kmin, const unsigned long long *kmax, int64_t N, int p,
                                const double *XX, int64_t M, int Nprime, int n0, int sorted, int32_t *pool, double *d2,
-                               char *w, int grid, int *fb, cudaStream_t st, int gx, int gy, const int32_t *cstart,
+                               char *w, int grid, int *fb, cudaStream_t st, NNGrid cg, const int32_t *cstart,
                                const int32_t *perm, const int32_t *qperm, int qg, const double *X64c) {
     size_t smem = sizeof(NNSmem);
     cudaError_t e = cudaFuncSetAttribute(nn_pool_kernel<P, MMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1258,7 +1646,7 @@ static cudaError_t launch_nn_t(const double *X, const float *X32, const float *r
     w += (size_t)grid * NN_Q * bc * sizeof(uint64_t);
     int32_t *bi = (int32_t *)w;
     nn_pool_kernel<P, MMA><<<grid, NN_THREADS, smem, st>>>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, bc, sorted,
-                                                      pool, d2, bcmp, bk, bi, fb, gx, gy, cstart, perm, qperm, qg, X64c);
+                                                      pool, d2, bcmp, bk, bi, fb, cg, cstart, perm, qperm, qg, X64c);
     return cudaGetLastError();
 }
 
@@ -1300,8 +1688,8 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
                       int *launches) {
     if (M > Mmax) return cudaErrorInvalidValue;
     char *w = (char *)ws;
-    const NNLayout L = nn_layout(N, p, Mmax);
-    const int C = L.gx * L.gy;
+    const NNLayout L = nn_layout(N, p, Mmax, Nprime);
+    const int C = L.g.ncell;
     unsigned long long *mx = (unsigned long long *)w;
     unsigned long long *kmin = mx + 1, *kmax = mx + 1 + LAGP_PMAX;  // 8 + 2*16*8 = 264 <= 512 B
     float *X32 = (float *)(w + L.x32);
@@ -1325,9 +1713,9 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
         if (blocks > 4096) blocks = 4096;
         // few blocks: every block ends in 2p same-address global atomics (592 blocks: 32 us)
         nn_bounds_kernel<<<blocks < 148 ? blocks : 148, 256, 0, st>>>(X, N, p, kmin, kmax);
-        nn_cell_hist_kernel<<<blocks, 256, 0, st>>>(X, N, p, kmin, kmax, L.gx, L.gy, rcnt);
+        nn_cell_hist_kernel<<<blocks, 256, 0, st>>>(X, N, p, kmin, kmax, L.g, rcnt);
         nn_cell_scan_kernel<<<1, 1024, 0, st>>>(rcnt, C, rstart, rcur);
-        nn_prep_kernel<<<blocks, 256, 0, st>>>(X, N, p, X32, rn2f, mx, kmin, kmax, L.gx, L.gy, rcur, perm, X64c);
+        nn_prep_kernel<<<blocks, 256, 0, st>>>(X, N, p, X32, rn2f, mx, kmin, kmax, L.g, rcur, perm, X64c);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         if (launches) (*launches) += 4;
@@ -1338,18 +1726,17 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
         int blocks = (int)((M + 255) / 256);
         if (blocks > 4096) blocks = 4096;
         if (blocks < 1) blocks = 1;
-        nn_cell_hist_kernel<<<blocks, 256, 0, st>>>(XX, M, p, kmin, kmax, L.gx, L.gy, qcnt);
+        nn_cell_hist_kernel<<<blocks, 256, 0, st>>>(XX, M, p, kmin, kmax, L.g, qcnt);
         nn_cell_scan_kernel<<<1, 1024, 0, st>>>(qcnt, C, qstart, qcur);
-        nn_cell_scatter_kernel<<<blocks, 256, 0, st>>>(XX, M, p, kmin, kmax, L.gx, L.gy, qcur, qperm);
+        nn_cell_scatter_kernel<<<blocks, 256, 0, st>>>(XX, M, p, kmin, kmax, L.g, qcur, qperm);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         if (launches) (*launches) += 3;
     }
     if (launches) (*launches)++;
-    const char *evm = getenv("LAGP_NN_MMA");
-    const bool mma = p == 8 && (evm ? evm[0] == '1' : (double)Nprime <= 0.004 * (double)N);
+    const bool mma = L.mma;
     const int qg = nn_group_size(M, grid, p, mma);
-#define NN_ARGS X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st, L.gx, L.gy, rstart, perm, qperm, qg, X64c
+#define NN_ARGS X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st, L.g, rstart, perm, qperm, qg, X64c
     switch (p) {
         case 1: return launch_nn_t<1, false>(NN_ARGS);
         case 2: return launch_nn_t<2, false>(NN_ARGS);
@@ -1366,3 +1753,13 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
 }
 
 }  // namespace lagp
+
+#ifdef LAGP_NN_PROF
+extern "C" int lagp_nn_prof(long long *out, int reset) {
+    if (reset) {
+        static long long z[1024][12];
+        return (int)cudaMemcpyToSymbol(lagp::g_nn_ph, z, sizeof(z));
+    }
+    return (int)cudaMemcpyFromSymbol(out, lagp::g_nn_ph, sizeof(lagp::g_nn_ph));
+}
+#endif

@@ -82,6 +82,65 @@ def test_nn_pool_cells_bit_exact(torch_dev, lagp, case, Nprime):
         assert np.array_equal(d2[i], rd2), name
 
 
+def _multi_cell_cases():
+    """Inputs for the multi-axis cell grid (p >= 4, nn.cu nn_cells / build_list): zero-width
+    cut axes, a tight 8-d cluster holding 40 % of the rows (a crowded cell and near-equal
+    keys in one value bin of the selection), a coarse 4-d grid (exact key ties everywhere),
+    a tiny box far from the origin (cell margins with |lo| >> slab width), queries far
+    outside the box, and very unequal axis scales."""
+    rng = np.random.default_rng(91)
+    out = []
+    X = rng.random((30000, 8)); X[:, 1] = 0.5; X[:, 4] = -2.0          # constant cut axes
+    out.append(("const_axes_8d", X, rng.random((24, 8))))
+    X = rng.random((30000, 8)); X[:12000] = 0.3 + 1e-7 * rng.standard_normal((12000, 8))
+    out.append(("cluster_8d", X, np.vstack([rng.random((16, 8)), np.full((4, 8), 0.3)])))
+    X = np.floor(rng.random((40000, 4)) * 5) / 5                      # ties everywhere
+    out.append(("grid_4d", X, np.floor(rng.random((20, 4)) * 5) / 5))
+    X = 1e6 + rng.random((30000, 6)) * 1e-3
+    out.append(("offset_6d", X, 1e6 + rng.random((20, 6)) * 1e-3))
+    X = rng.random((30000, 8))
+    out.append(("far_8d", X, np.vstack([rng.random((8, 8)) * 20 - 10, rng.random((8, 8))])))
+    X = rng.standard_normal((40000, 5)) * [1e3, 1e-3, 1, 1, 1]
+    out.append(("scales_5d", X, rng.standard_normal((16, 5)) * [1e3, 1e-3, 1, 1, 1]))
+    return out
+
+
+@pytest.mark.parametrize("case", range(6))
+@pytest.mark.parametrize("Nprime", [1, 50, 1000])
+def test_nn_pool_multi_cells_bit_exact(torch_dev, lagp, case, Nprime):
+    """The multi-axis cell grid (per-query cell lists) on its edge cases: the sorted pool
+    and its d^2 bit-exact against the oracle."""
+    torch, dev = torch_dev
+    name, X, XX = _multi_cell_cases()[case]
+    pool, d2 = lagp.nn_pool(T(torch, dev, X), T(torch, dev, XX), Nprime, with_d2=True)
+    pool, d2 = pool.cpu().numpy(), d2.cpu().numpy()
+    for i in range(XX.shape[0]):
+        ref, rd2 = oracle.nn(X, XX[i], Nprime)
+        assert np.array_equal(pool[i], ref), (name, i, np.where(pool[i] != ref)[0][:5])
+        assert np.array_equal(d2[i], rd2), name
+
+
+@pytest.mark.parametrize("case", range(6))
+@pytest.mark.parametrize("Nprime,n0", [(50, 6), (1000, 6), (1000, 0), (3000, 128)])
+def test_nn_pool_selected_bit_exact(torch_dev, lagp, case, Nprime, n0):
+    """The pool as the design kernels receive it (LAGP_NN_POOL_SELECT=n0: the value-bin
+    selection of select_pool, with its radix fallback on crowded bins): the n0 nearest
+    first in the oracle's (d^2, index) order, the whole pool the oracle's set."""
+    import os
+
+    torch, dev = torch_dev
+    name, X, XX = _multi_cell_cases()[case]
+    os.environ["LAGP_NN_POOL_SELECT"] = str(n0)
+    try:
+        pool = lagp.nn_pool(T(torch, dev, X), T(torch, dev, XX), Nprime).cpu().numpy()
+    finally:
+        os.environ.pop("LAGP_NN_POOL_SELECT", None)
+    for i in range(XX.shape[0]):
+        ref, _ = oracle.nn(X, XX[i], Nprime)
+        assert np.array_equal(pool[i, :n0], ref[:n0]), (name, i)
+        assert np.array_equal(np.sort(pool[i]), np.sort(ref)), (name, i)
+
+
 def test_nn_pool_massive_ties_fallback(torch_dev, lagp):
     """Every row at the same distance -> threshold filter cannot split; the exact
     radix-select fallback must return the lowest indices."""
@@ -438,11 +497,13 @@ def test_explicit_dmma_one_cta_per_sm(torch_dev, lagp):
 
 @pytest.mark.parametrize("env", [{"LAGP_V2_CPT": "2"}, {"LAGP_V2_CPT": "1"}, {"LAGP_V2_SFIRST": "1"},
                                  {"LAGP_V2_NOSTAGGER": "1"}, {"LAGP_INC_V1": "1"}, {"LAGP_NN_MMA": "1"},
-                                 {"LAGP_NN_MMA": "0"}, {"LAGP_NN_CELLS": "0"}, {"LAGP_NN_Q": "4"},
+                                 {"LAGP_NN_MMA": "0"}, {"LAGP_NN_CELLS": "0"}, {"LAGP_NN_CELLS": "2"},
+                                 {"LAGP_NN_CR": "16"}, {"LAGP_NN_CR": "4096"}, {"LAGP_NN_Q": "4"},
                                  {"LAGP_NN_Q": "8"}, {"LAGP_NN_Q": "16"}])
 def test_kernel_variants_agree(torch_dev, lagp, env):
     """Every A/B switch of the library (CTA shapes, tier order, phase order, v1
-    kernel; NN: TF32 filter on/off, no spatial cells, 4/8/16-query groups) against
+    kernel; NN: TF32 filter on/off, no spatial cells, the two-axis grid, multi-axis
+    cells of 16 / 4096 rows, 4/8/16-query groups) against
     the oracle on the same C2 sample as the default path, with n = 64 so the
     shared-memory, tensor-memory and slab tiers are all in use."""
     import os
