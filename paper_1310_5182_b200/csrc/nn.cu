@@ -29,11 +29,22 @@ constexpr int NN_THREADS = 256;
 constexpr int NN_Q = 16;
 constexpr int NN_CAP = 8192;
 constexpr int NN_MAX_ROUNDS = 6;
+// T2 sample rows per N/N' and expected survivors per N' under the sampled threshold.
+// Two-axis grid: 128 and 1.25 (measured: 64 -> 128, C2/C4/C3 NN -5/-6/-9 % with that
+// filter). Multi-axis grid, whose filter costs less per survivor: 64 and 1.15 (C2 NN
+// 1.94 -> 1.85 ms, C4 19.4 -> 18.8 ms per 65,536 queries; 1-2 % of groups take a second
+// filter round).
 #ifndef NN_S2F
-#define NN_S2F 128    // T2 sample rows per N/N' (measured: 64 -> 128 with the 1.25 target below, C2/C4/C3 NN -5/-6/-9 %)
+#define NN_S2F 128
+#endif
+#ifndef NN_S2F_MULTI
+#define NN_S2F_MULTI 64
 #endif
 #ifndef NN_TGT
-#define NN_TGT 1.25   // expected survivors per N' under the sampled threshold
+#define NN_TGT 1.25
+#endif
+#ifndef NN_TGT_MULTI
+#define NN_TGT_MULTI 1.15
 #endif
 
 #ifdef LAGP_NN_PROF
@@ -839,12 +850,12 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
     const int64_t ngroups = (M + qg - 1) / qg;  // qg = 8 or 16 query locations per group
     // sample sizes and target ranks (see the threshold phase)
     const int S1 = (int)(N < 1024 ? N : 1024);
-    int64_t s2 = (int64_t)NN_S2F * N / (Nprime > 0 ? Nprime : 1);
+    int64_t s2 = (int64_t)(cg.multi ? NN_S2F_MULTI : NN_S2F) * N / (Nprime > 0 ? Nprime : 1);
     if (s2 < S1) s2 = S1;
     if (s2 > 65536) s2 = 65536;
     if (s2 > N) s2 = N;
     const int S2 = (int)s2;
-    const int r2 = (int)ceil(NN_TGT * (double)Nprime * (double)S2 / (double)N) + 12;
+    const int r2 = (int)ceil((cg.multi ? NN_TGT_MULTI : NN_TGT) * (double)Nprime * (double)S2 / (double)N) + 12;
     int r1 = (int)ceil(4.0 * (double)r2 * (double)S1 / (double)S2) + 4;
     if (Nprime >= N) r1 = S1 + 1;
     // per query: bufi = filter survivors (stored positions, cell order) in NN_THREADS/32 warp segments of segcap rows;
