@@ -154,14 +154,29 @@ __device__ bool mle_chol(const double *Y, double *X, int n, double rth, double e
             }
         }
         const int j0 = k + (two ? 2 : 1);
+        // this lane's trailing columns jj = j0 + lane + 32 m: their two factors formed once
+        // per step (the same values for every row), then each row's rank-2 update
+        double lj[4], lj1[4];
+#pragma unroll
+        for (int m = 0; m < 4; m++) {
+            const int jj = j0 + lane + 32 * m;
+            lj[m] = lj1[m] = 0.0;
+            if (jj < n) {
+                lj[m] = X[jj * n + k] * rl;
+                if (two) lj1[m] = fma(-lj[m], c10, X[jj * n + k + 1]) * rl2;
+            }
+        }
         for (int i = j0 + wid; i < n; i += MLE_NW) {
             const double lik = X[i * n + k] * rl;
             const double lik1 = two ? fma(-lik, c10, X[i * n + k + 1]) * rl2 : 0.0;
-            for (int jj = j0 + lane; jj <= i; jj += 32) {
-                const double ljk = X[jj * n + k] * rl;
-                double v = fma(-lik, ljk, X[i * n + jj]);
-                if (two) v = fma(-lik1, fma(-ljk, c10, X[jj * n + k + 1]) * rl2, v);
-                X[i * n + jj] = v;
+#pragma unroll
+            for (int m = 0; m < 4; m++) {
+                const int jj = j0 + lane + 32 * m;
+                if (jj <= i) {
+                    double v = fma(-lik, lj[m], X[i * n + jj]);
+                    if (two) v = fma(-lik1, lj1[m], v);
+                    X[i * n + jj] = v;
+                }
             }
         }
         __syncthreads();
@@ -273,24 +288,43 @@ __device__ double mle_inverse(const double *X, double *Y, double *rd, double *Tb
 // A = W^T W into X's lower triangle (L is no longer needed), DMMA over the lower 8x8
 // tiles; W lower triangular: tile (a0, b0) sums t >= max(a0, b0)
 __device__ void mle_wtw(const double *Y, double *X, int n) {
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int g = lane >> 2, q = lane & 3, nt = (n + 7) >> 3;
-    for (int tile = tid >> 5; tile < nt * (nt + 1) / 2; tile += MLE_NW) {
-        int ti = 0;
-        while ((ti + 1) * (ti + 2) / 2 <= tile) ti++;
-        const int tj = tile - ti * (ti + 1) / 2;
-        const int a0 = ti * 8, b0 = tj * 8, ar = a0 + g, bc = b0 + g;
-        double c0 = 0.0, c1 = 0.0;
-        for (int kk = a0 & ~3; kk < n; kk += 4) {
-            const int t = kk + q;
-            const double av = (ar < n && t < n && t >= ar) ? Y[t * n + ar] : 0.0;
-            const double bv = (bc < n && t < n && t >= bc) ? Y[t * n + bc] : 0.0;
-            dmma884(c0, c1, av, bv);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int g = lane >> 2, q = lane & 3, nt = (n + 7) >> 3, ntile = nt * (nt + 1) / 2;
+    // two tiles per warp at a time (independent DMMA chains in one k loop; a tile's
+    // products below its start are exact zeros, so its sums are unchanged)
+    for (int tile = wid; tile < ntile; tile += 2 * MLE_NW) {
+        int ar[2], bc[2], b0[2];
+        bool has[2];
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            const int tl = tile + u * MLE_NW;
+            has[u] = tl < ntile;
+            int ti = 0;
+            while ((ti + 1) * (ti + 2) / 2 <= tl) ti++;
+            const int tj = tl - ti * (ti + 1) / 2;
+            ar[u] = ti * 8 + g;
+            b0[u] = tj * 8;
+            bc[u] = tj * 8 + g;
         }
-        const int cc = b0 + 2 * q;
-        if (ar < n) {
-            if (cc <= ar) X[ar * n + cc] = c0;
-            if (cc + 1 <= ar) X[ar * n + cc + 1] = c1;
+        const int a00 = (has[1] ? min(ar[0], ar[1]) : ar[0]) - g;  // the earlier tile row start
+        double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        for (int kk = a00 & ~3; kk < n; kk += 4) {
+            const int t = kk + q;
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                if (u == 1 && !has[1]) break;  // (warp-uniform)
+                const double av = (ar[u] < n && t < n && t >= ar[u]) ? Y[t * n + ar[u]] : 0.0;
+                const double bv = (bc[u] < n && t < n && t >= bc[u]) ? Y[t * n + bc[u]] : 0.0;
+                dmma884(c[u][0], c[u][1], av, bv);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            const int cc = b0[u] + 2 * q;
+            if (has[u] && ar[u] < n) {
+                if (cc <= ar[u]) X[ar[u] * n + cc] = c[u][0];
+                if (cc + 1 <= ar[u]) X[ar[u] * n + cc + 1] = c[u][1];
+            }
         }
     }
     __syncthreads();
@@ -363,16 +397,21 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, double *X, double *Y,
             while ((ti + 1) * (ti + 2) / 2 <= pr) ti++;
             const int tj = pr - ti * (ti + 1) / 2;  // tj <= ti
             double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-            for (int w2 = 0; w2 < 2; w2++) {
-                if (w2 == 1 && ti == tj) break;  // (warp-uniform)
-                const int I = w2 ? tj : ti, J = w2 ? ti : tj;
-                const int ar = I * 8 + g, bc = J * 8 + g;
+            {
+                // tiles (ti, tj) and (tj, ti) as two independent accumulation chains in one
+                // k loop (each tile's k order unchanged)
+                const bool two = ti != tj;  // (warp-uniform)
+                const int ar0 = ti * 8 + g, bc0 = tj * 8 + g;
                 for (int kk = 0; kk < n; kk += 4) {
                     const int k = kk + q;
-                    const double av = (ar < n && k < n) ? symA(X, n, ar, k) : 0.0;
-                    const double bv = (k < n && bc < n) ? symP(X, n, k, bc) : 0.0;
-                    dmma884(c[w2][0], c[w2][1], av, bv);
+                    const double av0 = (ar0 < n && k < n) ? symA(X, n, ar0, k) : 0.0;
+                    const double bv0 = (k < n && bc0 < n) ? symP(X, n, k, bc0) : 0.0;
+                    if (two) {
+                        const double av1 = (bc0 < n && k < n) ? symA(X, n, bc0, k) : 0.0;
+                        const double bv1 = (k < n && ar0 < n) ? symP(X, n, k, ar0) : 0.0;
+                        dmma884(c[1][0], c[1][1], av1, bv1);
+                    }
+                    dmma884(c[0][0], c[0][1], av0, bv0);
                 }
             }
             // tile (ti, tj) in c[0]; its partner (tj, ti) in c[1] (or c[0] on the diagonal)
