@@ -244,6 +244,29 @@ def traffic_for(workload, form, launches):
             "algorithmic_bytes_note": tr.get("note")}
 
 
+# FP32 (non-tensor) peak of one B200: 148 SM x 128 FP32 FMA/clk x 2 flop x 1.965 GHz
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def nn_roofline(head, m_rank, N, p):
+    """NN stage as work actually done (lagp_timing counters of the step): prefilter and
+    threshold-sample (row, query) pairs evaluated per second, each 2(p+1) FP32 flop (the
+    dot-form prefilter: p FMA + the norm FMA; the sample's difference form is 3p), against
+    the FP32 FMA peak; the pruned fraction of the M x N exhaustive pairs the cell lists
+    skipped; exact FP64 keys computed (filter survivors)."""
+    w = head.get("nn_work") or {}
+    fp, sp, ek = w.get("nn_filter_pairs", 0), w.get("nn_sample_pairs", 0), w.get("nn_exact_keys", 0)
+    t = head["nn_ms"] / 1000.0
+    flops = fp * 2 * (p + 1) + sp * 3 * p
+    return {"evaluated_pairs_per_sec": (fp + sp) / t, "filter_pairs": fp, "sample_pairs": sp, "exact_keys": ek,
+            "exhaustive_pairs": m_rank * N, "pruned_fraction": 1.0 - fp / float(m_rank * N),
+            "exact_keys_per_location": ek / float(m_rank), "achieved_tflops": flops / t / 1e12,
+            "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": flops / t / 1e12 / FP32_PEAK_TFLOPS,
+            "peak_basis": "148 SM x 128 FP32 FMA/clk x 2 x 1.965 GHz (FP32 FFMA2 pipe; no FP32 entry in MEASURED_PEAKS.json)",
+            "note": "whole NN stage time (cell prep, sample, filter, exact keys, selection) over the FP32 flops of "
+                    "the evaluated pairs; logical pairs the cells prune are not counted as work"}
+
+
 def form_work(form, n0, n, Np, p):
     """Algorithmic FP64 work per location of a local-design kernel.
 
@@ -406,9 +429,10 @@ def main():
             smem_peak = 128 * 148 * 1.965
             roof["state_stream"] = {"achieved_GBps": sb, "smem_peak_GBps": smem_peak, "frac": sb / smem_peak,
                                     "bytes": "sum_j (N'-j-1) j 8 B per location (w_c entries read per step)"}
+        tmg = res["timing"]  # NN work counters of the last step (identical every step)
         return dict(ms_step=ms_step, value=m_all / (ms_step / 1000.0), alc_ms=alc_step_ms,
                     nn_ms=float(t[2]) / steps, launches=launches, res=res, clk=clk, roofline=roof,
-                    form=ran)
+                    form=ran, nn_work={k: int(tmg[k]) for k in ("nn_filter_pairs", "nn_sample_pairs", "nn_exact_keys")})
 
     head = time_form(args.form, ClockSampler(local))
     others = {}
@@ -492,7 +516,8 @@ def main():
                  "metric": METRIC, "value": h4["value"], "unit": UNIT, "ms_per_step": h4["ms_step"],
                  "steps": min(args.steps, 3), "warmup": args.warmup,
                  "phase_ms_per_step": {"nn": h4["nn_ms"], "local_design": h4["alc_ms"]},
-                 "roofline": h4["roofline"], "clocks": h4["clk"], "gpu_launches": h4["launches"],
+                 "roofline": h4["roofline"], "nn_roofline": nn_roofline(h4, m4, c4["X"].shape[0], c4["X"].shape[1]),
+                 "clocks": h4["clk"], "gpu_launches": h4["launches"],
                  "locations_per_rank": m4, "status": int(h4["res"]["status"])}
         if world == 1 and not args.no_cpu_baseline:
             import oracle
@@ -524,10 +549,7 @@ def main():
         # the same numerator over the local-design kernel time (max over ranks),
         # the NN stage and the whole step against the FP64 ALU peak (paper counts)
         "alc_evals_per_sec_kernel": M_all * evals / (head["alc_ms"] / 1000.0),
-        "nn_roofline": {"work": "3p flop per (query, row) pair", "achieved_tflops":
-                        M_rank * cfg["X"].shape[0] * 3 * p / (head["nn_ms"] / 1000.0) / 1e12,
-                        "frac_fp64_peak": M_rank * cfg["X"].shape[0] * 3 * p / (head["nn_ms"] / 1000.0) / 1e12 / nominal,
-                        "note": "the filter runs in FP32x2 (and TF32 MMA for sparse pools); FP64 only on survivors"},
+        "nn_roofline": nn_roofline(head, M_rank, cfg["X"].shape[0], p),
         "end_to_end_paper_count": {
             "frac_fp64_peak": (M_all * (alc_paper_flops_per_location(n0, n, Np) + cfg["X"].shape[0] * 3 * p)
                                / (ms_step / 1000.0) / 1e12 / (world * nominal)),

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define LAGP_ABI_VERSION 3
+#define LAGP_ABI_VERSION 4
 #define LAGP_SCORES_JMAX 768 /* laGP_alc_scores: largest j (Fig 4 goes to 512) */
 #define LAGP_NMAX 128  /* largest local design size n of the greedy path (laGP_alc_scores: LAGP_SCORES_JMAX) */
 #define LAGP_PMAX 16   /* largest input dimension p */
@@ -94,6 +94,12 @@ typedef struct {
     int32_t launches; /* number of kernel launches this call issued          */
     int32_t nn_fallbacks; /* locations whose NN pool needed the exact radix-select fallback */
     int32_t alc_form; /* the formulation that ran (lagp_alc_form; LAGP_ALC_AUTO resolved) */
+    int32_t reserved; /* (alignment; 0) */
+    /* NN work of the call (ABI 4): (row, query) pairs the prefilter evaluated, pairs of
+     * the threshold sample, exact FP64 keys computed (filter survivors) */
+    int64_t nn_filter_pairs;
+    int64_t nn_sample_pairs;
+    int64_t nn_exact_keys;
 } lagp_timing;
 
 /*

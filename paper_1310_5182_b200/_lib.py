@@ -47,6 +47,10 @@ class Timing(ctypes.Structure):
         ("launches", ctypes.c_int32),
         ("nn_fallbacks", ctypes.c_int32),
         ("alc_form", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("nn_filter_pairs", ctypes.c_int64),
+        ("nn_sample_pairs", ctypes.c_int64),
+        ("nn_exact_keys", ctypes.c_int64),
     ]
 
     def as_dict(self):

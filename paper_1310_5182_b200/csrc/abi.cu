@@ -288,6 +288,7 @@ lagp_status alc_batch_impl(const double *X, int64_t N, int32_t p, const double *
     float nn_ms = 0.f, alc_ms = 0.f, tot_ms = 0.f;
     int launches = 0;
     int host_counters[2] = {0, 0};
+    unsigned long long host_pairs[3] = {0, 0, 0};
 
     LAGP_CUDA(ws.alloc((void **)&pool, (size_t)P.chunk * Nprime * sizeof(int32_t)));
     LAGP_CUDA(ws.alloc(&nnws, lagp::nn_ws_bytes(P.nn_grid, N, p, Nprime, false, P.chunk)));
@@ -337,6 +338,8 @@ lagp_status alc_batch_impl(const double *X, int64_t N, int32_t p, const double *
         }
     }
     LAGP_CUDA(cudaMemcpyAsync(host_counters, counters, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (timing)
+        LAGP_CUDA(cudaMemcpyAsync(host_pairs, lagp::nn_pair_counters(nnws), sizeof(host_pairs), cudaMemcpyDeviceToHost, st));
     if (timing) LAGP_CUDA(cudaEventRecord(ev[3], st));
     LAGP_CUDA(cudaStreamSynchronize(st));
     if (timing) {
@@ -348,6 +351,9 @@ lagp_status alc_batch_impl(const double *X, int64_t N, int32_t p, const double *
         timing->launches = launches;
         timing->nn_fallbacks = host_counters[1];
         timing->alc_form = P.form;
+        timing->nn_filter_pairs = (int64_t)host_pairs[0];
+        timing->nn_sample_pairs = (int64_t)host_pairs[1];
+        timing->nn_exact_keys = (int64_t)host_pairs[2];
     }
     if (host_counters[0] > 0) {
         fail(LAGP_PARTIAL, "%d location(s) flagged EXHAUSTED or NONFINITE", host_counters[0]);
@@ -528,6 +534,7 @@ lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *
     float nn_ms = 0.f, alc_ms = 0.f, mle_ms = 0.f, tot_ms = 0.f;
     int launches = 0;
     int host_counters[2] = {0, 0};
+    unsigned long long host_pairs[3] = {0, 0, 0};
     const MlePlan mp = plan_mle(P.chunk, n, p);
 
     LAGP_CUDA(ws.alloc((void **)&pool, (size_t)P.chunk * Nprime * sizeof(int32_t)));
@@ -611,6 +618,8 @@ lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *
         }
     }
     LAGP_CUDA(cudaMemcpyAsync(host_counters, counters, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (timing)
+        LAGP_CUDA(cudaMemcpyAsync(host_pairs, lagp::nn_pair_counters(nnws), sizeof(host_pairs), cudaMemcpyDeviceToHost, st));
     if (timing) LAGP_CUDA(cudaEventRecord(ev[4], st));
     LAGP_CUDA(cudaStreamSynchronize(st));
     if (timing) {
@@ -622,6 +631,9 @@ lagp_status laGP_local_fit(const double *X, int64_t N, int32_t p, const double *
         timing->launches = launches;
         timing->nn_fallbacks = host_counters[1];
         timing->alc_form = P.form;
+        timing->nn_filter_pairs = (int64_t)host_pairs[0];
+        timing->nn_sample_pairs = (int64_t)host_pairs[1];
+        timing->nn_exact_keys = (int64_t)host_pairs[2];
     }
     if (host_counters[0] > 0) {
         fail(LAGP_PARTIAL, "%d final-stage flag(s) EXHAUSTED or NONFINITE", host_counters[0]);

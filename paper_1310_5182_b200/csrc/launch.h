@@ -14,6 +14,8 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
                       bool sorted, int32_t *pool, double *d2, void *ws, int grid, int *fb, cudaStream_t st, bool prepared,
                       int *launches);
 size_t nn_ws_bytes(int grid, int64_t N, int p, int Nprime, bool sorted, int64_t Mmax);
+// NN work counters in an NN workspace: [0] prefilter pairs, [1] sample pairs, [2] exact keys
+unsigned long long *nn_pair_counters(void *ws);
 int nn_grid(int64_t M, int num_sms, int Nprime);
 
 // fused local-design kernels (rows a2-a5)

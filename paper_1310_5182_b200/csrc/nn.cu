@@ -842,7 +842,8 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                int sorted, int32_t *__restrict__ pool_out, double *__restrict__ d2_out, int32_t *__restrict__ bufc_ws,
                uint64_t *__restrict__ bufk_ws, int32_t *__restrict__ bufi_ws, int *__restrict__ fallback_count, NNGrid cg,
                const int32_t *__restrict__ cstart, const int32_t *__restrict__ perm,
-               const int32_t *__restrict__ qperm, int qg, const double *__restrict__ X64c) {
+               const int32_t *__restrict__ qperm, int qg, const double *__restrict__ X64c,
+               unsigned long long *__restrict__ pairc) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     NNSmem &s = *reinterpret_cast<NNSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
@@ -1066,6 +1067,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                     }
                 };
                 const unsigned allq = nq < 32 ? (1u << nq) - 1u : ~0u;
+                if (pairc && tid == 0) atomicAdd(pairc + 1, (unsigned long long)S2 * (unsigned)nq);
                 for (int64_t wb = (int64_t)wid * 128; wb < S2; wb += (int64_t)nw * 128) {
                     float xf[4][P ? P : LAGP_PMAX];
                     bool ok[4];
@@ -1215,8 +1217,10 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 // atomic per warp, query and pass with a hit).
                 const unsigned lt = (1u << lane) - 1u;
                 constexpr int PP = P ? P : LAGP_PMAX;
+                unsigned long long npair = 0;  // lane 0: (row, query) pairs this warp evaluated
                 auto pass = [&](auto uc, int base, int b, unsigned m) {
                     constexpr int U = decltype(uc)::value;
+                    npair += (unsigned long long)min(32 * U, b - base) * (unsigned)__popc(m);
                     float xf[U][PP], rn[U];
 #pragma unroll
                     for (int u = 0; u < U; u++) {
@@ -1270,6 +1274,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                     }
                     if (b - base > 0) pass(std::integral_constant<int, 1>{}, base, b, m);
                 }
+                if (pairc && lane == 0 && npair) atomicAdd(pairc, npair);
             } else if constexpr (MMA && P == 8) {
                 // Tensor-core filter (mma.sync m16n8k8 TF32): a warp takes 16 rows x 8
                 // queries per MMA, D = X~[16x8] Q~^T[8x8]; MMA coordinate k is x~ coordinate
@@ -1294,6 +1299,8 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 for (int ri = 0; ri < nrng; ri++) {
                 const int64_t ra = rng_a[ri], rend = rng_b[ri];
                 for (int64_t rb = ra + (int64_t)wid * 16 * NT; rb < rend; rb += (int64_t)nw * 16 * NT) {
+                    if (pairc && lane == 0)
+                        atomicAdd(pairc, (unsigned long long)(rend - rb < 16 * NT ? rend - rb : 16 * NT) * (unsigned)__popc(act));
                     float2 xa[NT], xb[NT];
                     float rnA[NT], rnB[NT];
 #pragma unroll
@@ -1351,6 +1358,14 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 const int64_t ra = rng_a[ri], rend = rng_b[ri];
                 for (int64_t wbase = ra + tid - lane; wbase < rend; wbase += 4 * (int64_t)blockDim.x) {
                     const int64_t base = wbase + lane;
+                    if (pairc && lane == 0) {
+                        long long rows = 0;
+                        for (int u = 0; u < 4; u++) {
+                            const long long r0 = wbase + u * (int64_t)blockDim.x;
+                            rows += r0 >= rend ? 0 : (rend - r0 < 32 ? rend - r0 : 32);
+                        }
+                        if (rows) atomicAdd(pairc, (unsigned long long)rows * (unsigned)__popc(act));
+                    }
                     float xf[4][P ? P : LAGP_PMAX];
                     float rn[4];
     #pragma unroll
@@ -1428,6 +1443,7 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 int tot = 0;
                 for (int w = 0; w < nw; w++) tot += s.wcnt[w][q];
                 const bool in_smem = tot <= NN_CAP;  // uniform
+                if (pairc && tid == 0) atomicAdd(pairc + 2, (unsigned long long)tot);
                 uint64_t *ok_k = in_smem ? s.key : bufk + (size_t)q * bufcap;
                 int32_t *ok_i = in_smem ? s.idx : bufc + (size_t)q * bufcap;
                 if (tid == 0) s.misc[3] = 0;
@@ -1529,6 +1545,12 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
 }
 
 size_t nn_smem_bytes() { return sizeof(NNSmem); }
+
+// the NN work counters in the workspace header (after maxn2 and the bounds keys):
+// [0] prefilter (row, query) pairs evaluated, [1] threshold-sample pairs, [2] exact keys
+unsigned long long *nn_pair_counters(void *ws) {
+    return reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(ws) + 384);
+}
 
 // per-query global survivor buffer: enough for ~1.5 N' plus sampling noise
 // (capped at the shared-memory sort capacity when the sorted pool is requested)
@@ -1646,7 +1668,8 @@ static cudaError_t launch_nn_t(const double *X, const float *X32, const float *r
                                const unsigned long long *kmin, const unsigned long long *kmax, int64_t N, int p,
                                const double *XX, int64_t M, int Nprime, int n0, int sorted, int32_t *pool, double *d2,
                                char *w, int grid, int *fb, cudaStream_t st, NNGrid cg, const int32_t *cstart,
-                               const int32_t *perm, const int32_t *qperm, int qg, const double *X64c) {
+                               const int32_t *perm, const int32_t *qperm, int qg, const double *X64c,
+                               unsigned long long *pairc) {
     size_t smem = sizeof(NNSmem);
     cudaError_t e = cudaFuncSetAttribute(nn_pool_kernel<P, MMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1657,7 +1680,7 @@ static cudaError_t launch_nn_t(const double *X, const float *X32, const float *r
     w += (size_t)grid * NN_Q * bc * sizeof(uint64_t);
     int32_t *bi = (int32_t *)w;
     nn_pool_kernel<P, MMA><<<grid, NN_THREADS, smem, st>>>(X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, bc, sorted,
-                                                      pool, d2, bcmp, bk, bi, fb, cg, cstart, perm, qperm, qg, X64c);
+                                                      pool, d2, bcmp, bk, bi, fb, cg, cstart, perm, qperm, qg, X64c, pairc);
     return cudaGetLastError();
 }
 
@@ -1703,6 +1726,7 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
     const int C = L.g.ncell;
     unsigned long long *mx = (unsigned long long *)w;
     unsigned long long *kmin = mx + 1, *kmax = mx + 1 + LAGP_PMAX;  // 8 + 2*16*8 = 264 <= 512 B
+    unsigned long long *pairc = nn_pair_counters(ws);                 // bytes 384..407
     float *X32 = (float *)(w + L.x32);
     float *rn2f = (float *)(w + L.rn2f);
     int32_t *perm = (int32_t *)(w + L.perm), *rcnt = (int32_t *)(w + L.rcnt), *rstart = (int32_t *)(w + L.rstart),
@@ -1717,6 +1741,8 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
         e = cudaMemsetAsync(kmin, 0xff, sizeof(unsigned long long) * LAGP_PMAX, st);
         if (e != cudaSuccess) return e;
         e = cudaMemsetAsync(kmax, 0, sizeof(unsigned long long) * LAGP_PMAX, st);
+        if (e != cudaSuccess) return e;
+        e = cudaMemsetAsync(pairc, 0, 3 * sizeof(unsigned long long), st);  // summed over the chunks
         if (e != cudaSuccess) return e;
         e = cudaMemsetAsync(rcnt, 0, sizeof(int32_t) * C, st);
         if (e != cudaSuccess) return e;
@@ -1747,7 +1773,7 @@ cudaError_t launch_nn(const double *X, int64_t N, int p, const double *XX, int64
     if (launches) (*launches)++;
     const bool mma = L.mma;
     const int qg = nn_group_size(M, grid, p, mma);
-#define NN_ARGS X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st, L.g, rstart, perm, qperm, qg, X64c
+#define NN_ARGS X, X32, rn2f, mx, kmin, kmax, N, p, XX, M, Nprime, n0, sorted ? 1 : 0, pool, d2, rest, grid, fb, st, L.g, rstart, perm, qperm, qg, X64c, pairc
     switch (p) {
         case 1: return launch_nn_t<1, false>(NN_ARGS);
         case 2: return launch_nn_t<2, false>(NN_ARGS);

@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(lagp):
     lib = lagp.lib()
     for s in declared_symbols():
         assert hasattr(lib, s), s
-    assert lagp.abi_version() == 3
+    assert lagp.abi_version() == 4
 
 
 def test_library_is_sm100a_only(lagp):
@@ -123,3 +123,25 @@ def test_alc_batch_sep_validates(lagp):
     assert st == 2 and "theta[1]" in lagp.last_error()
     st = lib.laGP_alc_batch_sep(1, 10, 2, 1, 1, 4, None, 1e-4, 2, 4, 6, 1, 1, 1, None, None, None, 1, None, None)
     assert st == 2 and "theta" in lagp.last_error()
+
+
+def test_timing_struct_layout_matches_header(tmp_path):
+    """The ctypes lagp_timing (paper_1310_5182_b200/_lib.py) has the C struct's size and
+    field offsets (include/lagp.h, ABI 4), checked with the host C compiler."""
+    import subprocess
+
+    from paper_1310_5182_b200 import _lib
+
+    fields = [f for f, _ in _lib.Timing._fields_]
+    src = tmp_path / "t.c"
+    src.write_text('#include <stddef.h>\n#include <stdio.h>\n#include "lagp.h"\nint main(void){printf("%zu'
+                   + "".join(" %zu" for _ in fields) + '\\n", sizeof(lagp_timing)'
+                   + "".join(f", offsetof(lagp_timing, {f})" for f in fields) + ");return 0;}\n")
+    exe = tmp_path / "t"
+    inc = os.path.join(ROOT, "include")
+    cuda_inc = "/usr/local/cuda/include"
+    subprocess.run(["gcc", "-I", inc, "-I", cuda_inc, str(src), "-o", str(exe)], check=True)
+    out = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert out[0] == ctypes.sizeof(_lib.Timing)
+    for f, off in zip(fields, out[1:]):
+        assert getattr(_lib.Timing, f).offset == off, f

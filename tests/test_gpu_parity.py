@@ -141,6 +141,38 @@ def test_nn_pool_selected_bit_exact(torch_dev, lagp, case, Nprime, n0):
         assert np.array_equal(np.sort(pool[i]), np.sort(ref)), (name, i)
 
 
+@pytest.mark.parametrize("env", [{}, {"LAGP_NN_CELLS": "2"}, {"LAGP_NN_CELLS": "0"}])
+def test_nn_work_counters(torch_dev, lagp, env):
+    """lagp_timing's NN work counters (ABI 4) obey their definitions: prefilter pairs
+    fewer than the M N exhaustive pairs with the multi-axis cells and at least M N with
+    one cell; sample pairs at most M N; exact keys (the filter survivors) at least N'
+    per location."""
+    import os
+
+    torch, dev = torch_dev
+    cfg = make_config("C2", M=200, N=20000)
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        X, Z, XX = (T(torch, dev, cfg[k]) for k in ("X", "Z", "XX"))
+        r = lagp.alc_batch(X, Z, XX, cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"], timing=True)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    t = r["timing"]
+    M, N = cfg["XX"].shape[0], cfg["X"].shape[0]
+    assert 0 < t["nn_filter_pairs"] <= 6 * M * N  # at most NN_MAX_ROUNDS filter rounds
+    if not env:
+        assert t["nn_filter_pairs"] < M * N  # the multi-axis cell lists prune
+    if env.get("LAGP_NN_CELLS") == "0":
+        assert t["nn_filter_pairs"] >= M * N  # one cell: every row for every active query, >= 1 round
+    assert 0 <= t["nn_sample_pairs"] <= M * N
+    assert t["nn_exact_keys"] >= M * cfg["Nprime"]
+
+
 def test_nn_pool_massive_ties_fallback(torch_dev, lagp):
     """Every row at the same distance -> threshold filter cannot split; the exact
     radix-select fallback must return the lowest indices."""
