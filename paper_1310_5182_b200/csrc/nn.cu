@@ -33,12 +33,17 @@ constexpr int NN_MAX_ROUNDS = 6;
 // Two-axis grid: 128 and 1.25 (measured: 64 -> 128, C2/C4/C3 NN -5/-6/-9 % with that
 // filter). Multi-axis grid, whose filter costs less per survivor: 64 and 1.15 (C2 NN
 // 1.94 -> 1.85 ms, C4 19.4 -> 18.8 ms per 65,536 queries; 1-2 % of groups take a second
-// filter round).
+// filter round). Sparse pools (N >= 500 N', e.g. C4) take 32 N/N' rows: there the
+// cell-list filter evaluates ~10 % of the rows per query, so the sample is a large share
+// of the work (C4 18.6 -> 17.3 ms per 65,536 queries; C2 prefers 64: 1.80 vs 1.84 ms).
 #ifndef NN_S2F
 #define NN_S2F 128
 #endif
 #ifndef NN_S2F_MULTI
 #define NN_S2F_MULTI 64
+#endif
+#ifndef NN_S2F_SPARSE
+#define NN_S2F_SPARSE 32
 #endif
 #ifndef NN_TGT
 #define NN_TGT 1.25
@@ -851,7 +856,8 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
     const int64_t ngroups = (M + qg - 1) / qg;  // qg = 8 or 16 query locations per group
     // sample sizes and target ranks (see the threshold phase)
     const int S1 = (int)(N < 1024 ? N : 1024);
-    int64_t s2 = (int64_t)(cg.multi ? NN_S2F_MULTI : NN_S2F) * N / (Nprime > 0 ? Nprime : 1);
+    const int s2f = !cg.multi ? NN_S2F : (N >= 500 * (int64_t)Nprime ? NN_S2F_SPARSE : NN_S2F_MULTI);
+    int64_t s2 = (int64_t)s2f * N / (Nprime > 0 ? Nprime : 1);
     if (s2 < S1) s2 = S1;
     if (s2 > 65536) s2 = 65536;
     if (s2 > N) s2 = N;
