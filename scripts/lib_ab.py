@@ -23,15 +23,19 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--M", type=int, default=None)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--form", default="auto")
+ap.add_argument("--flush", action="store_true", help="write 256 MiB before every rep (L2 flushed, as in bench.py)")
 a = ap.parse_args()
 cfg = make_config(a.config, M=a.M)
 dev = torch.device("cuda", 0)
 X, Z, XX = (torch.from_numpy(cfg[k]).to(dev) for k in ("X", "Z", "XX"))
 ref = None
+flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev) if a.flush else None
 for name in a.libs:
     lagp._LIB = lagp._lib.load(os.path.join(ROOT, "paper_1310_5182_b200", name))
     best = None
     for _ in range(a.reps):
+        if flush is not None:
+            flush.fill_(1.0)
         r = lagp.alc_batch(X, Z, XX, cfg["d"], cfg["g"], cfg["n0"], cfg["n"], cfg["Nprime"], form=a.form, timing=True)
         torch.cuda.synchronize()
         t = r["timing"]
