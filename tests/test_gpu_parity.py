@@ -318,6 +318,19 @@ def test_large_pool_explicit(torch_dev, lagp, form):
     check(g, o, cfg, form)
 
 
+@pytest.mark.parametrize("form,Nprime,n,p", [("explicit", 20000, 64, 8), ("explicit_dfma", 10000, 128, 2),
+                                             ("incremental", 20000, 128, 8)])
+def test_large_pool_deep_design(torch_dev, lagp, form, Nprime, n, p):
+    """Large pools with deep designs (C5's N' = 10^4-2*10^4 at n = 64 / 128, the shapes of
+    the C5 sweep's large-pool rows): the explicit DMMA kernel at its n = 64 limit, the
+    DFMA explicit kernel at n = LAGP_NMAX, and the HBM-streaming incremental kernel at
+    n = 128, against the oracle on two locations each."""
+    torch, dev = torch_dev
+    cfg = make_config("C5_2d" if p == 2 else "C5_8d", M=2, Nprime=Nprime, n=n)
+    g, o = run_both(torch, dev, lagp, cfg, form=form)
+    check(g, o, cfg, form)
+
+
 @pytest.mark.parametrize("Nprime,n,p", [(9000, 20, 2), (12000, 30, 2), (20000, 24, 8)])
 def test_incremental_stream_large_pool(torch_dev, lagp, Nprime, n, p):
     """N' > 8192 (the paper's LGBB N' = 10,000 variant, C5's large pools): the
