@@ -402,13 +402,23 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, double *X, double *Y,
                 // k loop (each tile's k order unchanged)
                 const bool two = ti != tj;  // (warp-uniform)
                 const int ar0 = ti * 8 + g, bc0 = tj * 8 + g;
-                for (int kk = 0; kk < n; kk += 4) {
+                // The four operands come from four offset streams of X (row-major):
+                //   x1 = X[ar0][k], x2 = X[k][ar0], x3 = X[bc0][k], x4 = X[k][bc0]
+                // A[ar0][k] = k <= ar0 ? x1 : x2    P[k][bc0] = k < bc0 ? x4 : (k > bc0 ? x3 : 0)
+                // A[bc0][k] = k <= bc0 ? x3 : x4    P[k][ar0] = k < ar0 ? x2 : (k > ar0 ? x1 : 0)
+                // (A in the lower triangle with the diagonal, P in the strict upper one).
+                const bool ra = ar0 < n, rb = bc0 < n;
+                int s1 = ar0 * n + q, s2 = q * n + ar0, s3 = bc0 * n + q, s4 = q * n + bc0;
+                for (int kk = 0; kk < n; kk += 4, s1 += 4, s2 += 4 * n, s3 += 4, s4 += 4 * n) {
                     const int k = kk + q;
-                    const double av0 = (ar0 < n && k < n) ? symA(X, n, ar0, k) : 0.0;
-                    const double bv0 = (k < n && bc0 < n) ? symP(X, n, k, bc0) : 0.0;
+                    const bool kv = k < n;
+                    const double x1 = (ra && kv) ? X[s1] : 0.0, x2 = (ra && kv) ? X[s2] : 0.0;
+                    const double x3 = (rb && kv) ? X[s3] : 0.0, x4 = (rb && kv) ? X[s4] : 0.0;
+                    const double av0 = k <= ar0 ? x1 : x2;
+                    const double bv0 = k < bc0 ? x4 : (k > bc0 ? x3 : 0.0);
                     if (two) {
-                        const double av1 = (bc0 < n && k < n) ? symA(X, n, bc0, k) : 0.0;
-                        const double bv1 = (k < n && ar0 < n) ? symP(X, n, k, ar0) : 0.0;
+                        const double av1 = k <= bc0 ? x3 : x4;
+                        const double bv1 = k < ar0 ? x2 : (k > ar0 ? x1 : 0.0);
                         dmma884(c[1][0], c[1][1], av1, bv1);
                     }
                     dmma884(c[0][0], c[0][1], av0, bv0);
