@@ -363,7 +363,10 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, double *X, double *Y,
     double pp[2] = {0.0, ld};
     for (int a = tid; a < n; a += blockDim.x) {
         double sa = 0.0;
-        for (int b = 0; b < n; b++) sa = fma(symA(X, n, a, b), Yr[b], sa);
+        // A[a][b]: row a of the lower triangle for b <= a, then column a below it (same
+        // b order as one symmetric loop)
+        for (int b = 0; b <= a; b++) sa = fma(X[a * n + b], Yr[b], sa);
+        for (int b = a + 1; b < n; b++) sa = fma(X[b * n + a], Yr[b], sa);
         al[a] = sa;
         pp[0] = fma(Yr[a], sa, pp[0]);
     }
@@ -382,7 +385,10 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, double *X, double *Y,
     // v = P al
     for (int a = tid; a < n; a += blockDim.x) {
         double sa = 0.0;
-        for (int b = 0; b < n; b++) sa = fma(symP(X, n, a, b), al[b], sa);
+        // P[a][b]: column a of the strict upper triangle for b < a, 0 at b = a, row a after
+        for (int b = 0; b < a; b++) sa = fma(X[b * n + a], al[b], sa);
+        sa = fma(0.0, al[a], sa);  // (the diagonal term, as the symmetric loop adds it)
+        for (int b = a + 1; b < n; b++) sa = fma(X[a * n + b], al[b], sa);
         v[a] = sa;
     }
     MLE_PH(4);
