@@ -156,12 +156,13 @@ __device__ bool mle_chol(const double *Y, double *X, int n, double rth, double e
         const int j0 = k + (two ? 2 : 1);
         // this lane's trailing columns jj = j0 + lane + 32 m: their two factors formed once
         // per step (the same values for every row), then each row's rank-2 update
+        const int nm = (n - j0 + 31) >> 5;  // column blocks of 32 in the trailing part (uniform)
         double lj[4], lj1[4];
 #pragma unroll
         for (int m = 0; m < 4; m++) {
             const int jj = j0 + lane + 32 * m;
             lj[m] = lj1[m] = 0.0;
-            if (jj < n) {
+            if (m < nm && jj < n) {
                 lj[m] = X[jj * n + k] * rl;
                 if (two) lj1[m] = fma(-lj[m], c10, X[jj * n + k + 1]) * rl2;
             }
@@ -171,6 +172,7 @@ __device__ bool mle_chol(const double *Y, double *X, int n, double rth, double e
             const double lik1 = two ? fma(-lik, c10, X[i * n + k + 1]) * rl2 : 0.0;
 #pragma unroll
             for (int m = 0; m < 4; m++) {
+                if (m >= nm) break;  // (uniform)
                 const int jj = j0 + lane + 32 * m;
                 if (jj <= i) {
                     double v = fma(-lik, lj[m], X[i * n + jj]);
@@ -308,14 +310,23 @@ __device__ void mle_wtw(const double *Y, double *X, int n) {
         }
         const int a00 = (has[1] ? min(ar[0], ar[1]) : ar[0]) - g;  // the earlier tile row start
         double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-        for (int kk = a00 & ~3; kk < n; kk += 4) {
+        const int k0 = a00 & ~3;
+        int oa[2], ob[2];  // offsets of W[t][ar], W[t][bc] (row-major Y), t = kk + q
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            oa[u] = (k0 + q) * n + ar[u];
+            ob[u] = (k0 + q) * n + bc[u];
+        }
+        for (int kk = k0; kk < n; kk += 4) {
             const int t = kk + q;
 #pragma unroll
             for (int u = 0; u < 2; u++) {
                 if (u == 1 && !has[1]) break;  // (warp-uniform)
-                const double av = (ar[u] < n && t < n && t >= ar[u]) ? Y[t * n + ar[u]] : 0.0;
-                const double bv = (bc[u] < n && t < n && t >= bc[u]) ? Y[t * n + bc[u]] : 0.0;
+                const double av = (ar[u] < n && t < n && t >= ar[u]) ? Y[oa[u]] : 0.0;
+                const double bv = (bc[u] < n && t < n && t >= bc[u]) ? Y[ob[u]] : 0.0;
                 dmma884(c[u][0], c[u][1], av, bv);
+                oa[u] += 4 * n;
+                ob[u] += 4 * n;
             }
         }
 #pragma unroll
