@@ -223,7 +223,20 @@ __device__ double mle_inverse(const double *X, double *Y, double *rd, double *Tb
     const int h = n >= 24 ? n / 2 : n;
     const int sub = tid & 3;
     const unsigned qmask = 0xfu << (tid & 28);
-    for (int c = tid >> 2; c < n; c += blockDim.x >> 2) {
+    // Columns in descending order of their row counts (h-1-c for c < h, n-1-c above),
+    // dealt to the quads in snake order (quad Q: positions Q, 2NQ-1-Q, 2NQ+Q, ...), so the
+    // longest substitution chains do not queue behind each other on one quad
+    const int nq4 = blockDim.x >> 2, d0 = n - 2 * h;
+    for (int pos = tid >> 2, rnd = 0; pos < n; rnd++, pos = (rnd & 1) ? (rnd + 1) * nq4 - 1 - (tid >> 2) : rnd * nq4 + (tid >> 2)) {
+        int c;
+        if (h == n) {
+            c = pos;
+        } else if (pos < d0) {
+            c = h + pos;
+        } else {
+            const int pi = (pos - d0) >> 1;
+            c = ((pos - d0) & 1) ? pi : h + d0 + pi;
+        }
         if (sub == 0) Y[c * n + c] = rd[c];
         __syncwarp(qmask);
         const int iend = c < h ? h : n;
