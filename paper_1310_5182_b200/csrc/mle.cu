@@ -105,13 +105,19 @@ __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double
 // row-major). Returns false when a pivot is not positive.
 __device__ bool mle_chol(const double *Y, double *X, int n, double rth, double eta, bool deriv) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    for (int a = wid; a < n; a += MLE_NW)
-        for (int b = lane; b <= a; b += 32) {
-            const double d = a == b ? 0.0 : Y[b * n + a];  // D_ab (upper storage)
-            const double c = exp_nonpos(-d * rth);
-            X[a * n + b] = c + (a == b ? eta : 0.0);
-            if (deriv && b < a) X[b * n + a] = c * (d * rth);
-        }
+    // the n(n+1)/2 lower-triangle entries dealt over all threads (row a of entry e from
+    // the triangular root, corrected in integers)
+    const int ne = n * (n + 1) / 2;
+    for (int e = tid; e < ne; e += blockDim.x) {
+        int a = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+        while (a * (a + 1) / 2 > e) a--;
+        while ((a + 1) * (a + 2) / 2 <= e) a++;
+        const int b = e - a * (a + 1) / 2;
+        const double d = a == b ? 0.0 : Y[b * n + a];  // D_ab (upper storage)
+        const double c = exp_nonpos(-d * rth);
+        X[a * n + b] = c + (a == b ? eta : 0.0);
+        if (deriv && b < a) X[b * n + a] = c * (d * rth);
+    }
     __shared__ int bad;
     if (tid == 0) bad = 0;
     __syncthreads();
