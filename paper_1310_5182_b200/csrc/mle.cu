@@ -391,14 +391,23 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, double *X, double *Y,
     mle_wtw(Y, X, n);
     MLE_PH(2);
     double pp[2] = {0.0, ld};
-    for (int a = tid; a < n; a += blockDim.x) {
+    // a = A Yr: two threads per row (adjacent lanes), each half of the b range (A[a][b]
+    // from row a of the lower triangle for b <= a, from column a below it), halves added
+    // by one shuffle
+    const int bm = n >> 1;
+    for (int a0 = 0; a0 < n; a0 += blockDim.x >> 1) {
+        const int a = a0 + (tid >> 1), hh = tid & 1;
         double sa = 0.0;
-        // A[a][b]: row a of the lower triangle for b <= a, then column a below it (same
-        // b order as one symmetric loop)
-        for (int b = 0; b <= a; b++) sa = fma(X[a * n + b], Yr[b], sa);
-        for (int b = a + 1; b < n; b++) sa = fma(X[b * n + a], Yr[b], sa);
-        al[a] = sa;
-        pp[0] = fma(Yr[a], sa, pp[0]);
+        if (a < n) {
+            const int b0 = hh ? bm : 0, b1 = hh ? n : bm, bs = a + 1 < b0 ? b0 : (a + 1 < b1 ? a + 1 : b1);
+            for (int b = b0; b < bs; b++) sa = fma(X[a * n + b], Yr[b], sa);
+            for (int b = bs; b < b1; b++) sa = fma(X[b * n + a], Yr[b], sa);
+        }
+        sa += __shfl_xor_sync(0xffffffffu, sa, 1);
+        if (a < n && hh == 0) {
+            al[a] = sa;
+            pp[0] = fma(Yr[a], sa, pp[0]);
+        }
     }
     cta_sum<2>(pp, red);  // (also orders the al writes)
     MLE_PH(3);
@@ -413,13 +422,18 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, double *X, double *Y,
     r.ok = isfinite(r.l);
     if (!deriv || !r.ok) return r;
     // v = P al
-    for (int a = tid; a < n; a += blockDim.x) {
+    // (two threads per row as for a; P[a][b] from column a of the strict upper triangle
+    // for b < a, from row a for b > a, 0 on the diagonal)
+    for (int a0 = 0; a0 < n; a0 += blockDim.x >> 1) {
+        const int a = a0 + (tid >> 1), hh = tid & 1;
         double sa = 0.0;
-        // P[a][b]: column a of the strict upper triangle for b < a, 0 at b = a, row a after
-        for (int b = 0; b < a; b++) sa = fma(X[b * n + a], al[b], sa);
-        sa = fma(0.0, al[a], sa);  // (the diagonal term, as the symmetric loop adds it)
-        for (int b = a + 1; b < n; b++) sa = fma(X[a * n + b], al[b], sa);
-        v[a] = sa;
+        if (a < n) {
+            const int b0 = hh ? bm : 0, b1 = hh ? n : bm, bs = a < b0 ? b0 : (a < b1 ? a : b1);
+            for (int b = b0; b < bs; b++) sa = fma(X[b * n + a], al[b], sa);
+            for (int b = (bs > a ? bs : a + 1); b < b1; b++) sa = fma(X[a * n + b], al[b], sa);
+        }
+        sa += __shfl_xor_sync(0xffffffffu, sa, 1);
+        if (a < n && hh == 0) v[a] = sa;
     }
     MLE_PH(4);
     // tr(APAP) = sum_ab T_ab T_ba with T = A P: 8x8 tiles of T on DMMA, a tile pair (I, J),
@@ -474,9 +488,14 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, double *X, double *Y,
     __syncthreads();  // v
     MLE_PH(5);
     double tAP = 0.0, tAQ = 0.0, aQa = 0.0, aPa = 0.0, vAv = 0.0;
-    // the lower triangle (off-diagonal terms twice; P and Q vanish on the diagonal)
-    for (int a = wid; a < n; a += MLE_NW)
-        for (int b = lane; b <= a; b += 32) {
+    // the lower triangle (off-diagonal terms twice; P and Q vanish on the diagonal), its
+    // entries dealt over all threads as in mle_chol
+    const int ne = n * (n + 1) / 2;
+    for (int e = tid; e < ne; e += blockDim.x) {
+            int a = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+            while (a * (a + 1) / 2 > e) a--;
+            while ((a + 1) * (a + 2) / 2 <= e) a++;
+            const int b = e - a * (a + 1) / 2;
             const double Aab = X[a * n + b];
             if (a == b) {
                 vAv = fma(v[a] * Aab, v[a], vAv);
