@@ -162,28 +162,64 @@ __device__ bool mle_chol(const double *Y, double *X, int n, double rth, double e
         const int j0 = k + (two ? 2 : 1);
         // this lane's trailing columns jj = j0 + lane + 32 m: their two factors formed once
         // per step (the same values for every row), then each row's rank-2 update
-        const int nm = (n - j0 + 31) >> 5;  // column blocks of 32 in the trailing part (uniform)
-        double lj[4], lj1[4];
+        if (two && ((n | j0) & 1) == 0) {
+            // pairs of columns per lane (jj = j0 + 2 lane + 64 m, 16-byte aligned since n and
+            // j0 are even): one LDS.128 / STS.128 per two entries. When jj = i the second
+            // entry is in the strict upper triangle (P, untouched here) and is written back
+            // unchanged. Same fma per entry as the scalar loop.
+            const int nm2 = (n - j0 + 63) >> 6;  // (uniform)
+            double lj[2][2], lj1[2][2];
 #pragma unroll
-        for (int m = 0; m < 4; m++) {
-            const int jj = j0 + lane + 32 * m;
-            lj[m] = lj1[m] = 0.0;
-            if (m < nm && jj < n) {
-                lj[m] = X[jj * n + k] * rl;
-                if (two) lj1[m] = fma(-lj[m], c10, X[jj * n + k + 1]) * rl2;
+            for (int m = 0; m < 2; m++)
+#pragma unroll
+                for (int h2 = 0; h2 < 2; h2++) {
+                    const int jj = j0 + 2 * lane + 64 * m + h2;
+                    lj[m][h2] = lj1[m][h2] = 0.0;
+                    if (m < nm2 && jj < n) {
+                        lj[m][h2] = X[jj * n + k] * rl;
+                        lj1[m][h2] = fma(-lj[m][h2], c10, X[jj * n + k + 1]) * rl2;
+                    }
+                }
+            for (int i = j0 + wid; i < n; i += MLE_NW) {
+                const double lik = X[i * n + k] * rl;
+                const double lik1 = fma(-lik, c10, X[i * n + k + 1]) * rl2;
+#pragma unroll
+                for (int m = 0; m < 2; m++) {
+                    if (m >= nm2) break;  // (uniform)
+                    const int jj = j0 + 2 * lane + 64 * m;
+                    if (jj <= i) {
+                        double2 *px = reinterpret_cast<double2 *>(X + i * n + jj);
+                        double2 x = *px;
+                        x.x = fma(-lik1, lj1[m][0], fma(-lik, lj[m][0], x.x));
+                        if (jj + 1 <= i) x.y = fma(-lik1, lj1[m][1], fma(-lik, lj[m][1], x.y));
+                        *px = x;
+                    }
+                }
             }
-        }
-        for (int i = j0 + wid; i < n; i += MLE_NW) {
-            const double lik = X[i * n + k] * rl;
-            const double lik1 = two ? fma(-lik, c10, X[i * n + k + 1]) * rl2 : 0.0;
+        } else {
+            const int nm = (n - j0 + 31) >> 5;  // column blocks of 32 in the trailing part (uniform)
+            double lj[4], lj1[4];
 #pragma unroll
             for (int m = 0; m < 4; m++) {
-                if (m >= nm) break;  // (uniform)
                 const int jj = j0 + lane + 32 * m;
-                if (jj <= i) {
-                    double v = fma(-lik, lj[m], X[i * n + jj]);
-                    if (two) v = fma(-lik1, lj1[m], v);
-                    X[i * n + jj] = v;
+                lj[m] = lj1[m] = 0.0;
+                if (m < nm && jj < n) {
+                    lj[m] = X[jj * n + k] * rl;
+                    if (two) lj1[m] = fma(-lj[m], c10, X[jj * n + k + 1]) * rl2;
+                }
+            }
+            for (int i = j0 + wid; i < n; i += MLE_NW) {
+                const double lik = X[i * n + k] * rl;
+                const double lik1 = two ? fma(-lik, c10, X[i * n + k + 1]) * rl2 : 0.0;
+#pragma unroll
+                for (int m = 0; m < 4; m++) {
+                    if (m >= nm) break;  // (uniform)
+                    const int jj = j0 + lane + 32 * m;
+                    if (jj <= i) {
+                        double v = fma(-lik, lj[m], X[i * n + jj]);
+                        if (two) v = fma(-lik1, lj1[m], v);
+                        X[i * n + jj] = v;
+                    }
                 }
             }
         }
