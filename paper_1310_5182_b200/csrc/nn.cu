@@ -3,18 +3,19 @@
 // NN candidate restriction P:484-487), exact by the key (d^2, row index) with
 // d^2 accumulated by fma in the order k = 0..p-1 (reading R8).
 //
-// B200 design: a persistent grid of CTAs, each handling NN_Q
-// queries at a time. One pass streams X through registers (coalesced rows) and
-// evaluates all NN_Q queries per row, so X is read from L2 once per NN_Q
-// queries. The pass is a paired-FP32 (FFMA2, sm_100) prefilter on an FP32 copy
-// of X with a rigorous rounding margin; only rows that pass it get the exact
-// FP64 key, which alone decides membership. Selection is threshold-then-sort: a strided sample of X gives a
-// per-query threshold tau at ~1.25 N' expected survivors (NN_TGT); the filter pass
-// appends (d^2, i) with d^2 <= tau to a per-query buffer; the buffer is
-// bitonic-sorted in shared memory by (key bits, index) and its first N' rows
-// are the pool. If the count lands outside [N', NN_CAP] the threshold is
-// re-chosen from the sample; after a few misses the query falls back to an
-// exact 8-bit radix select over the 64-bit keys (robust to massive ties).
+// B200 design: a persistent grid of CTAs (two per SM), each handling
+// a group of 8 or 16 spatially neighbouring queries at a time. Rows of X are stored
+// cell by cell: a two-axis grid for p <= 3, a multi-axis grid (slabs on up to 8
+// coordinates) for p >= 4. Per group: a two-level strided sample of X gives each query
+// a threshold tau at ~1.15-1.25 N' expected survivors; a paired-FP32 (FFMA2, sm_100)
+// prefilter on an FP32 copy of X with a rigorous rounding margin visits only the cells
+// that can hold a row with d^2 <= tau (per-query cell lists from rounded-down per-axis
+// gap bounds on the multi-axis grid, merged cell-column runs on the two-axis one);
+// survivors get the exact FP64 key, which alone decides membership. Selection: one
+// value-bin histogram pass locates ranks N' and n0 (radix select as the fallback), or
+// a bitonic sort for the sorted pool of laGP_nn_pool. A count outside [N', bufcap]
+// re-scales tau; after a few misses the query falls back to an exact 8-bit radix
+// select over the 64-bit keys of all rows (robust to massive ties).
 #include <cuda_runtime.h>
 #include <stdlib.h>
 
