@@ -120,6 +120,24 @@ def test_nn_pool_multi_cells_bit_exact(torch_dev, lagp, case, Nprime):
         assert np.array_equal(d2[i], rd2), name
 
 
+@pytest.mark.parametrize("p,N,Nprime", [(7, 30000, 500), (10, 40000, 1000), (16, 20000, 300), (12, 120000, 2000)])
+def test_nn_pool_multi_cells_generic_p(torch_dev, lagp, p, N, Nprime):
+    """The multi-axis grid on the generic-p kernel (p not in {1,2,3,4,8}; p > 8 cuts only
+    the first 8 coordinates): gaussian rows with unequal axis scales, queries inside and
+    outside the cloud; sorted pool and d^2 bit-exact against the oracle."""
+    torch, dev = torch_dev
+    rng = np.random.default_rng(100 + p)
+    sc = np.exp(rng.uniform(-2.0, 2.0, p))
+    X = rng.standard_normal((N, p)) * sc
+    XX = np.vstack([rng.standard_normal((12, p)) * sc, rng.standard_normal((4, p)) * sc * 4.0])
+    pool, d2 = lagp.nn_pool(T(torch, dev, X), T(torch, dev, XX), Nprime, with_d2=True)
+    pool, d2 = pool.cpu().numpy(), d2.cpu().numpy()
+    for i in range(XX.shape[0]):
+        ref, rd2 = oracle.nn(X, XX[i], Nprime)
+        assert np.array_equal(pool[i], ref), (p, i, np.where(pool[i] != ref)[0][:5])
+        assert np.array_equal(d2[i], rd2), p
+
+
 @pytest.mark.parametrize("case", range(6))
 @pytest.mark.parametrize("Nprime,n0", [(50, 6), (1000, 6), (1000, 0), (3000, 128)])
 def test_nn_pool_selected_bit_exact(torch_dev, lagp, case, Nprime, n0):
