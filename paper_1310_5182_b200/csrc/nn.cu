@@ -1576,13 +1576,14 @@ static int nn_bufcap(int Nprime, bool sorted) {
 // per cell, one more slab at a time on the coordinate with the fewest (lowest first):
 // C2 (N = 10^5, p = 8) 3 x 2^7 = 384 cells, C4 (N = 10^6) 3^6 x 2^2 = 2,916 cells.
 // LAGP_NN_CELLS (A/B): 0 = one cell (no pruning), 2 = the two-axis grid.
-// rows per cell: 128 up to N = 5e5, else 256 (measured: C2 NN 1.95 vs 2.10 ms at 128 vs
-// 256; C4 18.2 vs 20.9 ms per 65,536 queries at 256 vs 128, where the 6,561-cell list
-// costs more than the finer cells save); LAGP_NN_CR overrides (A/B)
+// rows per cell: 96 up to N = 5e5, else 256 (measured at C2: NN 1.76 / 1.81 / 2.17 ms at
+// 96 / 128 / 64 rows, 2.10 at 256; C4 18.2 vs 20.9 ms per 65,536 queries at 256 vs 128,
+// where the 6,561-cell list costs more than the finer cells save); LAGP_NN_CR overrides
+// (A/B)
 static int nn_cell_rows(int64_t N) {
     const char *ev = getenv("LAGP_NN_CR");
     const int v = ev ? atoi(ev) : 0;
-    return v >= 16 ? v : (N > 500000 ? 256 : 128);
+    return v >= 16 ? v : (N > 500000 ? 256 : 96);
 }
 static NNGrid nn_cells(int64_t N, int p, bool mma) {
     NNGrid g{};
