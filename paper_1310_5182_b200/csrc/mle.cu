@@ -94,6 +94,15 @@ __device__ __forceinline__ void cta_sum(double (&v)[K], double *red) {
     __syncthreads();
 }
 
+// row a of entry e of a lower triangle stored row by row (a(a+1)/2 <= e < (a+1)(a+2)/2):
+// the float root, corrected in integers
+__device__ __forceinline__ int tri_row(int e) {
+    int a = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+    while (a * (a + 1) / 2 > e) a--;
+    while ((a + 1) * (a + 2) / 2 <= e) a++;
+    return a;
+}
+
 __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
         : "+d"(c0), "+d"(c1)
@@ -109,9 +118,7 @@ __device__ bool mle_chol(const double *Y, double *X, int n, double rth, double e
     // the triangular root, corrected in integers)
     const int ne = n * (n + 1) / 2;
     for (int e = tid; e < ne; e += blockDim.x) {
-        int a = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
-        while (a * (a + 1) / 2 > e) a--;
-        while ((a + 1) * (a + 2) / 2 <= e) a++;
+        const int a = tri_row(e);
         const int b = e - a * (a + 1) / 2;
         const double d = a == b ? 0.0 : Y[b * n + a];  // D_ab (upper storage)
         const double c = exp_nonpos(-d * rth);
@@ -356,8 +363,7 @@ __device__ void mle_wtw(const double *Y, double *X, int n) {
         for (int u = 0; u < 2; u++) {
             const int tl = tile + u * MLE_NW;
             has[u] = tl < ntile;
-            int ti = 0;
-            while ((ti + 1) * (ti + 2) / 2 <= tl) ti++;
+            const int ti = tri_row(tl);
             const int tj = tl - ti * (ti + 1) / 2;
             ar[u] = ti * 8 + g;
             b0[u] = tj * 8;
@@ -479,8 +485,7 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, double *X, double *Y,
         const int g = lane >> 2, q = lane & 3, nt = (n + 7) >> 3;
         double *tw = tp + 64 * wid;
         for (int pr = wid; pr < nt * (nt + 1) / 2; pr += MLE_NW) {
-            int ti = 0;
-            while ((ti + 1) * (ti + 2) / 2 <= pr) ti++;
+            const int ti = tri_row(pr);
             const int tj = pr - ti * (ti + 1) / 2;  // tj <= ti
             double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
             {
@@ -528,9 +533,7 @@ __device__ MleEval mle_eval(double tau, bool deriv, int n, double *X, double *Y,
     // entries dealt over all threads as in mle_chol
     const int ne = n * (n + 1) / 2;
     for (int e = tid; e < ne; e += blockDim.x) {
-            int a = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
-            while (a * (a + 1) / 2 > e) a--;
-            while ((a + 1) * (a + 2) / 2 <= e) a++;
+            const int a = tri_row(e);
             const int b = e - a * (a + 1) / 2;
             const double Aab = X[a * n + b];
             if (a == b) {
