@@ -1455,15 +1455,23 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                 int32_t *ok_i = in_smem ? s.idx : bufc + (size_t)q * bufcap;
                 if (tid == 0) s.misc[3] = 0;
                 __syncthreads();
+                // the stored position of the thread's next survivor is loaded one iteration
+                // ahead (its L2 round trip overlaps this iteration's row loads and key)
+                auto surv_sp = [&](int t) -> int {
+                    if (t >= tot) return -1;
+                    int w = 0, off = t;
+                    while (off >= s.wcnt[w][q]) { off -= s.wcnt[w][q]; w++; }
+                    return bufi[q * bufcap + w * segcap + off];  // stored position
+                };
+                int sp_next = surv_sp(tid);
                 for (int tb = tid - lane; tb < tot; tb += blockDim.x) {  // warp-uniform bound
                     const int t = tb + lane;
+                    const int sp = sp_next;
+                    sp_next = surv_sp(t + blockDim.x);
                     bool ok = false;
                     int r = 0;
                     double d2 = 0.0;
                     if (t < tot) {
-                        int w = 0, off = t;
-                        while (off >= s.wcnt[w][q]) { off -= s.wcnt[w][q]; w++; }
-                        const int sp = bufi[q * bufcap + w * segcap + off];  // stored position
                         r = __ldg(perm + sp);                                // -> row of X
                         double xr[P ? P : LAGP_PMAX];
                         load_row<P>(X64c, sp, p, xr);  // = row r of X
