@@ -1241,21 +1241,8 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                             rn[u] = __int_as_float(0x7fc00000);  // NaN: never <= thr
                         }
                     }
-                    while (m) {
-                        const int q = __ffs(m) - 1;
-                        m &= m - 1;
-                        float qv[PP];
-#pragma unroll
-                        for (int k = 0; k < PP; k++) qv[k] = s.qf[q][k];
-                        const float thq = s.thq[q];
-                        bool hit[U];
-                        unsigned mm[U], tot = 0;
-#pragma unroll
-                        for (int u = 0; u < U; u++) {
-                            hit[u] = fmaf(-2.f, row_dotf<P>(xf[u], qv, p), rn[u]) <= thq;
-                            mm[u] = __ballot_sync(0xffffffffu, hit[u]);
-                            tot += __popc(mm[u]);
-                        }
+                    // two listed queries per iteration (independent dot chains)
+                    auto append = [&](int q, const bool (&hit)[U], const unsigned (&mm)[U], unsigned tot) {
                         if (tot) {
                             int pos = 0;
                             if (lane == 0) pos = atomicAdd(&s.fcnt[q], (int)tot);
@@ -1268,6 +1255,36 @@ nn_pool_kernel(const double *__restrict__ X, const float *__restrict__ X32, cons
                                 pos += __popc(mm[u]);
                             }
                         }
+                    };
+                    while (m) {
+                        const int q = __ffs(m) - 1;
+                        m &= m - 1;
+                        const int q2 = m ? __ffs(m) - 1 : q;  // (uniform)
+                        const bool two = m != 0;
+                        if (two) m &= m - 1;
+                        float qv[PP], qv2[PP];
+#pragma unroll
+                        for (int k = 0; k < PP; k++) {
+                            qv[k] = s.qf[q][k];
+                            qv2[k] = s.qf[q2][k];
+                        }
+                        const float thq = s.thq[q], thq2 = s.thq[q2];
+                        bool hit[U], hit2[U];
+                        unsigned mm[U], mm2[U], tot = 0, tot2 = 0;
+#pragma unroll
+                        for (int u = 0; u < U; u++) {
+                            hit[u] = fmaf(-2.f, row_dotf<P>(xf[u], qv, p), rn[u]) <= thq;
+                            hit2[u] = two && fmaf(-2.f, row_dotf<P>(xf[u], qv2, p), rn[u]) <= thq2;
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; u++) {
+                            mm[u] = __ballot_sync(0xffffffffu, hit[u]);
+                            mm2[u] = __ballot_sync(0xffffffffu, hit2[u]);
+                            tot += __popc(mm[u]);
+                            tot2 += __popc(mm2[u]);
+                        }
+                        append(q, hit, mm, tot);
+                        append(q2, hit2, mm2, tot2);
                     }
                 };
                 for (int e = wid; e < nrng; e += nw) {  // warp-uniform
